@@ -1,0 +1,140 @@
+/*
+ * se1p.h -- C ABI of the B200-native SE1P k-space library (libse1p.so).
+ *
+ * Method: Saffar Shamshirgar & Tornberg, "The Spectral Ewald method for singly periodic
+ * domains", arXiv:1611.09538.  "P:n" cites line n of the paper's text.
+ *
+ * Problem (Eq. (1), with P_1 periodicity P:79): N point charges q_n at x_n in
+ * [0,L1) x [0,L2) x [0,L3), periodic along axis 3 (z) only, free along axes 1,2.
+ * The library evaluates the Ewald1P split of the potential at every charge location:
+ *   se1p_kspace  ->  phi^F  = phi^{F,k3!=0} + phi^{F,k3=0}   (Alg. 1; Eqs. (4),(5))
+ *   se1p_real    ->  phi^R + phi^self                       (Eq. (3), Eq. (6))
+ * Their sum is the full potential phi of Eq. (2).
+ *
+ * Conventions for every entry point
+ *   - x: double[3*N], interleaved x0,y0,z0,x1,...; q: double[N]; phi_out: double[N].
+ *     The caller owns all three.  Inputs are never modified (z is folded into [0,L3)
+ *     internally).  phi_out is overwritten (phi_out[n] belongs to particle n).
+ *   - Pointers are CUDA DEVICE pointers on the current device unless opts->host_io != 0,
+ *     in which case they are host pointers and the library copies in and out (the copies
+ *     are part of the call).
+ *   - All arithmetic is IEEE fp64.  Results are bitwise reproducible for identical inputs
+ *     (no floating-point atomics; every reduction has a fixed order).
+ *   - The plain entries (se1p_kspace, se1p_real) are synchronous and return a complete
+ *     status including CUDA errors.  The _ex entries enqueue on `stream` (cudaStream_t,
+ *     NULL = legacy default stream) and, with opts->sync == 0, return after enqueueing;
+ *     argument errors are still returned synchronously.
+ *   - On any non-OK return, se1p_last_error() gives a thread-local message.
+ *   - Thread safety: calls on different threads are serialised by an internal mutex
+ *     (plans and workspaces are per device and shared).
+ */
+#ifndef SE1P_H
+#define SE1P_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SE1P_OK = 0,
+  SE1P_EINVAL = 1,       /* null pointer, N < 1, xi <= 0, L <= 0, rc <= 0, M < 2            */
+  SE1P_EDOMAIN = 2,      /* an x or y coordinate outside [0,L1) x [0,L2)  (free axes)          */
+  SE1P_ENONNEUTRAL = 3,  /* |sum q| > 1e-12 * sum |q|; Eq. (5) needs neutrality */
+  SE1P_EPARAM = 4,       /* L1/h or L2/h not an integer, L1/h != L2/h, P < 2 or P > M,
+                            eta not in (0,1), n_local > M/2, FFT extent < M+P or
+                            with a prime factor > 61                                         */
+  SE1P_ENOMEM = 5,
+  SE1P_ECUDA = 6,
+  SE1P_ENCCL = 7
+} se1p_status;
+
+/* Options for the _ex entries.  Zero-initialise and set what you need; every 0 means
+   "default".  Padded FFT extents are integers (reading R-5: the paper's s0, s_l are
+   factors relative to M~ = M_free + P and it asks for s M~ to be an integer). */
+typedef struct se1p_opts {
+  int Ntilde;       /* FFT extent of the free axes for the k3 in J modes (s = 1);
+                       0 -> planner (>= M~, FFT-friendly, widened per DESIGN.md).         */
+  int S0;           /* padded extent for k3 = 0 (the paper's s0 M~); 0 -> from s0         */
+  int SI;           /* padded extent for k3 in I (the paper's s_l M~); 0 -> from sf       */
+  int host_io;      /* 1: x, q, phi_out are host pointers (copied in/out inside the call) */
+  int skip_checks;  /* 1: skip the device-side domain and neutrality checks               */
+  int sync;         /* 1: synchronise the stream before returning (plain entries do)     */
+  int reserved[10];
+} se1p_opts;
+
+/* Derived sizes of a k-space plan (for reporting and tests). */
+typedef struct se1p_plan_info {
+  double h;         /* grid step L3/M (Alg. 1 step 1)                              */
+  double eta;       /* Gaussian split parameter (Eq. (comp_eta))                    */
+  int M;            /* periodic-axis points                                               */
+  int Mfree;        /* L1/h = L2/h                                                        */
+  int Mt;           /* M~ = Mfree + P                                             */
+  int P;
+  int n_local;      /* n_l: |k3| <= 2 pi n_l/L3 are upsampled (Eq. (I))             */
+  int Ntilde;       /* J-mode FFT extent                                                  */
+  int S0, SI;       /* padded extents of the k3 = 0 and I modes                            */
+  int LK;           /* FFT extent used on the device for the upsampled modes (>= 2 M~ - 1):
+                       their padded transform is applied as an exact aperiodic convolution
+                       with a plan-time kernel.                   */
+  int n_kernel_planes;  /* planes handled through LK (k3 = 0 and the I modes, k3 >= 0)   */
+  int n_planes;         /* M/2 + 1 (Hermitian half along z)                              */
+  int64_t grid_points;  /* M~^2 * M real grid points                                     */
+  int64_t workspace_bytes;
+} se1p_plan_info;
+
+/* k-space potential phi^F (Alg. 1 OUTPUT): no real-space and no self term.
+     M        grid points along the periodic axis; h = L[2]/M, free-axis counts L[0]/h, L[1]/h
+     P        Gaussian support points per dimension
+     eta      <= 0 -> P xi^2 h^2/(0.95^2 pi) (Eq. (comp_eta))
+     s0, sf   upsampling factors of k3 = 0 and of the I modes (Eq. (upsamplings));
+              <= 0 -> planner default.  Padded extents are ceil(s M~).
+     n_local  n_l (Eq. (I)); < 0 -> planner default.
+   sf == s0 with n_local == M/2 reproduces the plain upsampled FFT.              */
+int se1p_kspace(const double* x, const double* q, int64_t N, const double L[3], double xi,
+                int M, int P, double eta, double s0, double sf, int n_local, double* phi_out);
+
+int se1p_kspace_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                   int64_t N, const double L[3], double xi, int M, int P, double eta,
+                   double s0, double sf, int n_local, double* phi_out);
+
+/* Real-space erfc sum truncated at |x_m - x_n + alpha L3 e3| <= rc over z-images alpha
+   (Eq. (3); truncation P:120; cell lists P:161-162) plus the self term
+   -2 xi q_m/sqrt(pi) (Eq. (6)).  Any rc > 0 (all images within rc are included). */
+int se1p_real(const double* x, const double* q, int64_t N, const double L[3], double xi,
+              double rc, double* phi_out);
+
+int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                 int64_t N, const double L[3], double xi, double rc, double* phi_out);
+
+/* Resolve the plan the k-space call with these arguments would use (no device work
+   beyond plan creation).  Returns SE1P_OK or the same errors as se1p_kspace_ex. */
+int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P,
+                    double eta, double s0, double sf, int n_local, se1p_plan_info* info);
+
+/* Per-stage device time of the last _ex call on this thread, in milliseconds, measured
+   with CUDA events when opts->reserved[0] == 1 (profiling mode).  Stages: 0 bin/sort,
+   1 gridding, 2 z-FFT, 3 mode stage, 4 inverse z-FFT, 5 gather.  Returns stages written. */
+int se1p_last_stage_times(double* ms, int max_stages);
+
+/* Number of kernels the library launched in the last call on this thread. */
+int se1p_last_launch_count(void);
+
+/* Testing hook: with opts->reserved[1] = s (1..4) a k-space call stops after stage s
+   (1 gridding, 2 z-FFT, 3 mode stage, 4 inverse z-FFT) and leaves phi_out untouched.
+   se1p_debug_copy then copies `count` elements of workspace buffer `which` (0: real grid
+   [M~][M~][M] doubles, 1: k3 planes [M/2+1][M~][M~] complex as double pairs) to host memory.
+   Returns SE1P_OK or SE1P_EINVAL if the buffer is smaller than requested. */
+int se1p_debug_copy(int which, double* host_dst, int64_t count);
+
+/* Free all plans and workspaces of the current device. */
+void se1p_release(void);
+
+const char* se1p_last_error(void);
+const char* se1p_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SE1P_H */

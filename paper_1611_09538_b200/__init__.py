@@ -1,0 +1,214 @@
+"""B200-native SE1P k-space path (arXiv:1611.09538) -- Python binding of libse1p.so.
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+``csrc/`` behind the C ABI of ``include/se1p.h``.  There is no CPU fallback: if the
+shared library is missing or fails to load, importing the functions raises.
+
+    import torch, paper_1611_09538_b200 as se1p
+    phi_k = se1p.kspace(x, q, L, xi, M, P, s0=..., sf=..., n_local=...)  # x [N,3], q [N] f64 cuda
+    phi_r = se1p.real(x, q, L, xi, rc)                                  # phi^R + phi^self
+    phi = phi_k + phi_r                                                 # Eq. (2)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = _build.OUT
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "EDOMAIN", 3: "ENONNEUTRAL", 4: "EPARAM", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
+EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query",
+           "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
+           "se1p_version", "se1p_debug_copy"]
+
+
+class SE1PError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"se1p {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("Ntilde", ctypes.c_int), ("S0", ctypes.c_int), ("SI", ctypes.c_int), ("host_io", ctypes.c_int),
+                ("skip_checks", ctypes.c_int), ("sync", ctypes.c_int), ("reserved", ctypes.c_int * 10)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_double), ("eta", ctypes.c_double), ("M", ctypes.c_int), ("Mfree", ctypes.c_int),
+                ("Mt", ctypes.c_int), ("P", ctypes.c_int), ("n_local", ctypes.c_int), ("Ntilde", ctypes.c_int),
+                ("S0", ctypes.c_int), ("SI", ctypes.c_int), ("LK", ctypes.c_int), ("n_kernel_planes", ctypes.c_int),
+                ("n_planes", ctypes.c_int), ("grid_points", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load(build_if_needed: bool = True):
+    """Load libse1p.so (building it in-tree with nvcc if missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_needed and _build.needs_build():
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libse1p.so not found at {LIB_PATH}; run paper_1611_09538_b200/build.py")
+    lib = ctypes.CDLL(LIB_PATH)
+    d, i64, i32, vp = ctypes.c_double, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    lib.se1p_kspace.argtypes = [vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
+    lib.se1p_kspace_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
+    lib.se1p_real.argtypes = [vp, vp, i64, vp, d, d, vp]
+    lib.se1p_real_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, d, vp]
+    lib.se1p_plan_query.argtypes = [ctypes.POINTER(Opts), vp, d, i32, i32, d, d, d, i32, ctypes.POINTER(PlanInfo)]
+    lib.se1p_last_stage_times.argtypes = [vp, i32]
+    lib.se1p_last_launch_count.restype = i32
+    lib.se1p_last_error.restype = ctypes.c_char_p
+    lib.se1p_version.restype = ctypes.c_char_p
+    lib.se1p_debug_copy.argtypes = [i32, vp, i64]
+    lib.se1p_debug_copy.restype = i32
+    for f in ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query", "se1p_last_stage_times"]:
+        getattr(lib, f).restype = i32
+    _lib = lib
+    return lib
+
+
+def _check(code):
+    if code != 0:
+        raise SE1PError(code, load().se1p_last_error().decode())
+
+
+def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0):
+    o = Opts()
+    o.Ntilde = int(Ntilde or 0)
+    o.S0 = int(S0 or 0)
+    o.SI = int(SI or 0)
+    o.host_io = int(bool(host_io))
+    o.skip_checks = int(bool(skip_checks))
+    o.sync = int(bool(sync))
+    o.reserved[0] = 1 if profile else 0
+    o.reserved[1] = int(stop_after)
+    return o
+
+
+def _Larr(L):
+    return (ctypes.c_double * 3)(*[float(v) for v in L])
+
+
+def _args(x, q):
+    """(x_ptr, q_ptr, N, host_io, keepalive).  torch CUDA tensors -> device pointers;
+    numpy arrays -> host pointers (the library copies them)."""
+    if isinstance(x, np.ndarray):
+        xa = np.ascontiguousarray(x, dtype=np.float64)
+        qa = np.ascontiguousarray(q, dtype=np.float64)
+        return xa.ctypes.data, qa.ctypes.data, qa.shape[0], True, (xa, qa)
+    import torch
+    if not (x.is_cuda and q.is_cuda):
+        raise TypeError("x and q must both be CUDA tensors (or both numpy arrays for host I/O)")
+    if x.dtype != torch.float64 or q.dtype != torch.float64:
+        raise TypeError("x and q must be float64")
+    xc, qc = x.contiguous(), q.contiguous()
+    if xc.dim() != 2 or xc.shape[1] != 3 or qc.shape[0] != xc.shape[0]:
+        raise ValueError("x must be [N,3] and q [N]")
+    return xc.data_ptr(), qc.data_ptr(), qc.shape[0], False, (xc, qc)
+
+
+def _stream_ptr(stream, x):
+    if isinstance(x, np.ndarray):
+        return None
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _neg(v, default=-1.0):
+    return default if v is None else float(v)
+
+
+def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
+           out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0):
+    """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1)."""
+    lib = load()
+    xp, qp, N, host, keep = _args(x, q)
+    if host:
+        out = np.zeros(N) if out is None else out
+        optr = out.ctypes.data
+    else:
+        import torch
+        out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
+        optr = out.data_ptr()
+    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after)
+    _check(lib.se1p_kspace_ex(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
+                              _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr))
+    return out
+
+
+def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False):
+    """phi^R + phi^self (Eq. (3) truncated at rc, Eq. (6))."""
+    lib = load()
+    xp, qp, N, host, keep = _args(x, q)
+    if host:
+        out = np.zeros(N) if out is None else out
+        optr = out.ctypes.data
+    else:
+        import torch
+        out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
+        optr = out.data_ptr()
+    o = _opts(host_io=host, skip_checks=skip_checks, sync=sync)
+    _check(lib.se1p_real_ex(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr))
+    return out
+
+
+def potential(x, q, L, xi, rc, M, P, **kw):
+    """Full singly periodic potential phi = phi^F + phi^R + phi^self (Eq. (2))."""
+    return kspace(x, q, L, xi, M, P, **kw) + real(x, q, L, xi, rc)
+
+
+def plan_info(L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None):
+    lib = load()
+    info = PlanInfo()
+    o = _opts(Ntilde, S0, SI)
+    _check(lib.se1p_plan_query(ctypes.byref(o), _Larr(L), float(xi), int(M), int(P), _neg(eta, 0.0), _neg(s0),
+                               _neg(sf), -1 if n_local is None else int(n_local), ctypes.byref(info)))
+    return info.as_dict()
+
+
+def stage_times():
+    """Per-stage device ms of the last profiled call: bin, spread, zfft, modes, izfft, gather."""
+    buf = (ctypes.c_double * 8)()
+    n = load().se1p_last_stage_times(buf, 8)
+    names = ["bin", "spread", "zfft", "modes", "izfft", "gather"]
+    return {names[i]: buf[i] for i in range(n)}
+
+
+def launch_count():
+    return load().se1p_last_launch_count()
+
+
+def debug_stage(x, q, L, xi, M, P, stage, **kw):
+    """Testing hook: run the k-space path up to `stage` (1 gridding, 2 z-FFT, 3 modes, 4 inverse
+    z-FFT) and return the workspace buffer (real grid [Mt,Mt,M] or planes [M/2+1,Mt,Mt] complex)."""
+    info = plan_info(L, xi, M, P, **{k: kw.get(k) for k in ("eta", "s0", "sf", "n_local", "Ntilde", "S0", "SI")})
+    kspace(x, q, L, xi, M, P, stop_after=stage, **kw)
+    Mt, Mz = info["Mt"], info["M"]
+    if stage in (1, 4):
+        buf = np.zeros(Mt * Mt * Mz)
+        _check(load().se1p_debug_copy(0, buf.ctypes.data, buf.size))
+        return buf.reshape(Mt, Mt, Mz)
+    buf = np.zeros(2 * (Mz // 2 + 1) * Mt * Mt)
+    _check(load().se1p_debug_copy(1, buf.ctypes.data, buf.size))
+    return buf.view(np.complex128).reshape(Mz // 2 + 1, Mt, Mt)
+
+
+def release():
+    load().se1p_release()
+
+
+def version():
+    return load().se1p_version().decode()

@@ -1,0 +1,407 @@
+// api.cu -- the C ABI of libse1p (include/se1p.h): argument validation, the parameter
+// planner (Alg. 1 step 1 and DESIGN.md "Parameter choices"), workspaces, stage sequencing.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/se1p.h"
+#include "kspace.cuh"
+#include "real.cuh"
+#include "sort.cuh"
+
+namespace se1p {
+
+static thread_local std::string g_err;
+static thread_local int g_launches = 0;
+static thread_local double g_stage_ms[8];
+static thread_local int g_nstages = 0;
+static std::mutex g_mu;
+
+void count_launch() { ++g_launches; }
+
+struct DevState {
+  KWork w;
+  double* dx = nullptr;   // host_io staging (device side)
+  double* dq = nullptr;
+  double* dphi = nullptr;
+  int64_t io_cap = 0;
+};
+static DevState g_dev[64];
+
+static DevState& dev_state() {
+  int d = 0;
+  SE1P_CUDA_TRY(cudaGetDevice(&d));
+  return g_dev[d & 63];
+}
+
+template <typename T>
+static void grow(T*& p, int64_t& cap, int64_t need) {
+  if (need <= cap) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  if (cudaMalloc(&p, sizeof(T) * (size_t)std::max<int64_t>(need, 1)) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{5, "cudaMalloc failed (" + std::to_string(sizeof(T) * need) + " bytes)"};
+  }
+  cap = need;
+}
+
+static void ensure_particles(KWork& w, int64_t N, int nbins) {
+  grow(w.xs, w.cap_xs, 4 * N);
+  grow(w.perm, w.cap_perm, N);
+  grow(w.keys, w.cap_keys, N);
+  grow(w.bin_start, w.cap_bs, (int64_t)nbins + 1);
+  grow(w.total, w.cap_total, (int64_t)nbins + 1);
+  grow(w.hist, w.hist_cap, sort_hist_ints(N, nbins));
+  if (!w.red) {
+    int64_t c1 = 0, c2 = 0;
+    grow(w.red, c1, 4);
+    grow(w.flag, c2, 4);
+  }
+}
+
+// ------------------------------------------------------------------ input checks
+__global__ void k_check(const double* __restrict__ x, const double* __restrict__ q, int64_t N, double L0, double L1,
+                        double* __restrict__ red, int* __restrict__ flag) {
+  // single block, fixed-order reduction: sum q, sum |q|; flag bit 0 = domain, bit 1 = non-finite
+  __shared__ double s1[1024], s2[1024];
+  __shared__ int sf[1024];
+  double a = 0.0, b = 0.0;
+  int f = 0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+    const double px = x[3 * i], py = x[3 * i + 1], pz = x[3 * i + 2], qi = q[i];
+    if (!isfinite(px) || !isfinite(py) || !isfinite(pz) || !isfinite(qi)) f |= 2;
+    if (!(px >= 0.0 && px < L0 && py >= 0.0 && py < L1)) f |= 1;
+    a += qi;
+    b += fabs(qi);
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  sf[threadIdx.x] = f;
+  __syncthreads();
+  for (int off = 512; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      s1[threadIdx.x] += s1[threadIdx.x + off];
+      s2[threadIdx.x] += s2[threadIdx.x + off];
+      sf[threadIdx.x] |= sf[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    red[0] = s1[0];
+    red[1] = s2[0];
+    flag[0] = sf[0];
+  }
+}
+
+static void check_inputs(KWork& w, const double* x, const double* q, int64_t N, const double L[3], bool neutral,
+                         cudaStream_t st) {
+  k_check<<<1, 1024, 0, st>>>(x, q, N, L[0], L[1], w.red, w.flag);
+  SE1P_LAUNCH_CHECK();
+  double red[2];
+  int flag = 0;
+  SE1P_CUDA_TRY(cudaMemcpyAsync(red, w.red, sizeof red, cudaMemcpyDeviceToHost, st));
+  SE1P_CUDA_TRY(cudaMemcpyAsync(&flag, w.flag, sizeof flag, cudaMemcpyDeviceToHost, st));
+  SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  if (flag & 2) throw Error{1, "non-finite coordinate or charge"};
+  if (flag & 1) throw Error{2, "an x or y coordinate lies outside [0,L1) x [0,L2) (free axes)"};
+  if (neutral && std::fabs(red[0]) > 1e-12 * red[1])
+    throw Error{3, "system is not charge neutral: |sum q| = " + std::to_string(std::fabs(red[0])) +
+                       " > 1e-12 sum|q| (Eq. (5) needs neutrality, P:106-110)"};
+}
+
+// ------------------------------------------------------------------ planner
+static int extent_from_factor(double s, int Mt) { return (int)std::ceil(s * Mt - 1e-9); }
+
+// Resolve defaults.  Reading of the paper's recipe for B200:
+//   eta    Eq. (comp_eta) with c = 0.95
+//   n_l    given, else ~M/16 (>= 1)
+//   S0,SI  given (opts or ceil(s M~)), else 8 M~: on this path an upsampled plane costs the
+//          same for any S, so the planner takes a generous S
+//   SJ     given, else the smallest FFT-friendly extent with Ntilde h - L >= 23 L3/(2 pi (n_l+1))
+//          (aliasing distance of the first J mode for a 1e-10 estimate, SURVEY c-6)
+static KParams resolve(const se1p_opts* o, const double L[3], double xi, int M, int P, double eta, double s0,
+                       double sf, int n_local) {
+  if (!L || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "box lengths must be positive"};
+  if (!(xi > 0)) throw Error{1, "xi must be positive"};
+  if (M < 2) throw Error{1, "M must be >= 2"};
+  KParams p{};
+  p.L[0] = L[0];
+  p.L[1] = L[1];
+  p.L[2] = L[2];
+  p.xi = xi;
+  p.M = M;
+  p.P = P;
+  const double h = L[2] / M;
+  const double m1 = L[0] / h, m2 = L[1] / h;
+  const long M1 = std::lround(m1), M2 = std::lround(m2);
+  if (std::fabs(m1 - M1) > 1e-9 * m1 || std::fabs(m2 - M2) > 1e-9 * m2)
+    throw Error{4, "L1/h and L2/h must be integers (h = L3/M)"};
+  if (M1 != M2) throw Error{4, "this build requires a square free cross-section (L1/h == L2/h)"};
+  if (M % 2) throw Error{4, "M must be even (Hermitian half along z)"};
+  if (P < 2 || P > M || P > (int)M1 + P || P > 64) throw Error{4, "P must satisfy 2 <= P <= min(M, 64)"};
+  const int Mt = (int)M1 + P;
+  p.eta = (eta > 0) ? eta : P * xi * xi * h * h / (0.95 * 0.95 * kPi);
+  if (!(p.eta > 0 && p.eta < 1)) throw Error{4, "eta must lie in (0,1) so the scaling damps (P:250)"};
+  p.n_l = (n_local >= 0) ? n_local : std::max(1, (int)std::lround(M / 16.0));
+  if (p.n_l > M / 2) throw Error{4, "n_local must be <= M/2"};
+  const int S0o = o ? o->S0 : 0, SIo = o ? o->SI : 0, SJo = o ? o->Ntilde : 0;
+  auto even = [](int v) { return v + (v & 1); };
+  p.S0 = S0o > 0 ? S0o : (s0 > 0 ? extent_from_factor(s0, Mt) : even(8 * Mt));
+  p.SI = SIo > 0 ? SIo : (sf > 0 ? extent_from_factor(sf, Mt) : even(8 * Mt));
+  if (SJo > 0) {
+    p.SJ = SJo;
+  } else {
+    const double gap = 23.0 * L[2] / (2.0 * kPi * (p.n_l + 1));
+    p.SJ = next_friendly(std::max(Mt, (int)std::ceil((L[0] + gap) / h)));
+  }
+  if (p.S0 < Mt || p.SI < Mt || p.SJ < Mt) throw Error{4, "padded FFT extents must be >= M~ = M_free + P"};
+  std::vector<int> r;
+  if (!fft_factor(p.SJ, r) || !fft_factor(M, r)) throw Error{4, "FFT extent with a prime factor > 61"};
+  return p;
+}
+
+static void fill_info(const KPlan& pl, se1p_plan_info* info) {
+  if (!info) return;
+  info->h = pl.dv.h;
+  info->eta = pl.prm.eta;
+  info->M = pl.prm.M;
+  info->Mfree = pl.dv.Mfree;
+  info->Mt = pl.dv.Mt;
+  info->P = pl.prm.P;
+  info->n_local = pl.prm.n_l;
+  info->Ntilde = pl.prm.SJ;
+  info->S0 = pl.prm.S0;
+  info->SI = pl.prm.SI;
+  info->LK = pl.LK;
+  info->n_kernel_planes = pl.n_kernel;
+  info->n_planes = pl.n_planes;
+  info->grid_points = (int64_t)pl.dv.Mt * pl.dv.Mt * pl.prm.M;
+  info->workspace_bytes = info->grid_points * 8 + (int64_t)pl.n_planes * pl.dv.Mt * pl.dv.Mt * 16 + pl.t_off_total * 16;
+}
+
+struct StageTimer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t ev[9];
+  int n = 0;
+  StageTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark() {
+    if (on && n < 9) cudaEventRecord(ev[n++], st);
+  }
+  void finish() {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    g_nstages = n - 1;
+    for (int i = 0; i + 1 < n; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      g_stage_ms[i] = ms;
+    }
+  }
+  ~StageTimer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+static void sync_and_check(cudaStream_t st) {
+  SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
+static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
+                        const double L[3], double xi, int M, int P, double eta, double s0, double sf, int n_local,
+                        double* phi_out) {
+  if (!x || !q || !phi_out) throw Error{1, "null pointer"};
+  if (N < 1) throw Error{1, "N must be >= 1"};
+  if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
+  const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  KPlan* pl = kplan_get(prm, st);
+  DevState& ds = dev_state();
+  KWork& w = ds.w;
+  const KDev& dv = pl->dv;
+  ensure_particles(w, N, dv.nbx * dv.nby * dv.nbz);
+  grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
+  grow(w.planes, w.planes_cap, (int64_t)pl->n_planes * dv.Mt * dv.Mt);
+  grow(w.T, w.T_cap, pl->t_off_total);
+  const bool host_io = o && o->host_io;
+  const double *dx = x, *dq = q;
+  double* dphi = phi_out;
+  if (host_io) {
+    grow(ds.dx, ds.io_cap, 5 * N);
+    dx = ds.dx;
+    dq = ds.dx + 3 * N;
+    dphi = ds.dx + 4 * N;
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  }
+  if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, true, st);
+  StageTimer tm(o && o->reserved[0] == 1, st);
+  const int stop = o ? o->reserved[1] : 0;
+  tm.mark();
+  k_bin_particles(*pl, w, dx, dq, N, st);
+  tm.mark();
+  k_spread(*pl, w, N, st);
+  tm.mark();
+  if (stop == 1) return sync_and_check(st);
+  k_zfft_forward(*pl, w, st);
+  tm.mark();
+  if (stop == 2) return sync_and_check(st);
+  k_mode_stage(*pl, w, st);
+  tm.mark();
+  if (stop == 3) return sync_and_check(st);
+  k_zfft_inverse(*pl, w, st);
+  tm.mark();
+  if (stop == 4) return sync_and_check(st);
+  k_gather(*pl, w, N, dphi, st);
+  tm.mark();
+  if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  tm.finish();
+  if (!o || o->sync || host_io) SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
+static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
+                      const double L[3], double xi, double rc, double* phi_out) {
+  if (!x || !q || !phi_out || !L) throw Error{1, "null pointer"};
+  if (N < 1) throw Error{1, "N must be >= 1"};
+  if (!(xi > 0) || !(rc > 0) || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "xi, rc, L must be > 0"};
+  const RDev d = real_geometry(L, xi, rc);
+  DevState& ds = dev_state();
+  KWork& w = ds.w;
+  ensure_particles(w, N, d.nc[0] * d.nc[1] * d.nc[2]);
+  const bool host_io = o && o->host_io;
+  const double *dx = x, *dq = q;
+  double* dphi = phi_out;
+  if (host_io) {
+    grow(ds.dx, ds.io_cap, 5 * N);
+    dx = ds.dx;
+    dq = ds.dx + 3 * N;
+    dphi = ds.dx + 4 * N;
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  }
+  if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, false, st);
+  real_space(d, w, dx, dq, N, dphi, st);
+  if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  if (!o || o->sync || host_io) SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
+template <typename F>
+static int guarded(F&& f) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  try {
+    f();
+    return SE1P_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SE1P_ECUDA;
+  }
+}
+
+}  // namespace se1p
+
+using namespace se1p;
+
+extern "C" {
+
+int se1p_kspace(const double* x, const double* q, int64_t N, const double L[3], double xi, int M, int P, double eta,
+                double s0, double sf, int n_local, double* phi_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    o.sync = 1;
+    kspace_impl(&o, 0, x, q, N, L, xi, M, P, eta, s0, sf, n_local, phi_out);
+  });
+}
+
+int se1p_kspace_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                   const double L[3], double xi, int M, int P, double eta, double s0, double sf, int n_local,
+                   double* phi_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    kspace_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, s0, sf, n_local, phi_out);
+  });
+}
+
+int se1p_real(const double* x, const double* q, int64_t N, const double L[3], double xi, double rc, double* phi_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    o.sync = 1;
+    real_impl(&o, 0, x, q, N, L, xi, rc, phi_out);
+  });
+}
+
+int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N, const double L[3],
+                 double xi, double rc, double* phi_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    real_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, rc, phi_out);
+  });
+}
+
+int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P, double eta, double s0,
+                    double sf, int n_local, se1p_plan_info* info) {
+  return guarded([&] {
+    const KParams prm = resolve(opts, L, xi, M, P, eta, s0, sf, n_local);
+    KPlan* pl = kplan_get(prm, 0);
+    fill_info(*pl, info);
+  });
+}
+
+int se1p_last_stage_times(double* ms, int max_stages) {
+  int n = std::min(max_stages, g_nstages);
+  for (int i = 0; i < n; ++i) ms[i] = g_stage_ms[i];
+  return n;
+}
+
+int se1p_last_launch_count(void) { return g_launches; }
+
+int se1p_debug_copy(int which, double* host_dst, int64_t count) {
+  return guarded([&] {
+    KWork& w = dev_state().w;
+    if (!host_dst || count < 0) throw Error{1, "bad arguments"};
+    if (which == 0) {
+      if (count > w.grid_cap) throw Error{1, "grid buffer smaller than requested"};
+      SE1P_CUDA_TRY(cudaMemcpy(host_dst, w.grid, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    } else if (which == 1) {
+      if (count > 2 * w.planes_cap) throw Error{1, "plane buffer smaller than requested"};
+      SE1P_CUDA_TRY(cudaMemcpy(host_dst, w.planes, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    } else {
+      throw Error{1, "unknown buffer"};
+    }
+  });
+}
+
+void se1p_release(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  kplan_release_all();
+  int d = 0;
+  cudaGetDevice(&d);
+  DevState& ds = g_dev[d & 63];
+  KWork& w = ds.w;
+  for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.hist, (void*)w.total,
+                  (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx})
+    if (p) cudaFree(p);
+  ds = DevState{};
+}
+
+const char* se1p_last_error(void) { return g_err.c_str(); }
+
+const char* se1p_version(void) { return "se1p-b200 0.1 (sm_100a, fp64)"; }
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// fft.cuh -- shared-memory mixed-radix Stockham FFT used by every transform of the SE1P
+// path (the z-FFT of AFT step 1 and the per-k3 2D transforms of Alg. 2/3).
+//
+// One FFT length n = r_0 r_1 ... r_{S-1}; stage s (radix r, Ns = r_0...r_{s-1}) reads
+// v_t = in[j + t n/r], multiplies by w^{t (j mod Ns)} with w = e^{-+2 pi i/(Ns r)}, does an
+// r-point DFT and writes out[(j/Ns) Ns r + (j mod Ns) + q Ns] (Stockham autosort, natural
+// order in and out).  Radices 4, 2, 3, 5 have dedicated butterflies; any other prime
+// factor up to 61 uses an O(r^2) butterfly with a root table.  Twiddles are tabulated on
+// the host in long double and rounded once.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace se1p {
+
+constexpr int kMaxStages = 16;
+constexpr int kMaxGenericRadix = 61;
+
+struct FftDesc {
+  int n = 0;
+  int nst = 0;
+  int rad[kMaxStages];
+  int twoff[kMaxStages];   // stage twiddles: tw[twoff + k (r-1) + t - 1] = e^{-2 pi i t k/(Ns r)}
+  int rootoff[kMaxStages]; // generic radix roots: tw[rootoff + k] = e^{-2 pi i k / r}
+  int total = 0;           // table length (complex entries)
+};
+
+// ------------------------------------------------------------------ butterflies
+// DIR = -1: forward (e^{-i...}), DIR = +1: inverse (unnormalised).
+template <int DIR>
+__device__ __forceinline__ double2 mul_i_dir(double2 a) {  // a * (DIR * i)
+  return DIR < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+template <int DIR>
+__device__ __forceinline__ void bfly2(double2* v) {
+  double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+template <int DIR>
+__device__ __forceinline__ void bfly4(double2* v) {
+  double2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+  double2 c = cadd(v[1], v[3]), d = mul_i_dir<DIR>(csub(v[1], v[3]));
+  v[0] = cadd(a, c);
+  v[2] = csub(a, c);
+  v[1] = cadd(b, d);
+  v[3] = csub(b, d);
+}
+
+template <int DIR>
+__device__ __forceinline__ void bfly3(double2* v) {
+  const double s3 = 0.866025403784438646763723170752936183;  // sqrt(3)/2
+  double2 s = cadd(v[1], v[2]);
+  double2 t = make_double2(v[0].x - 0.5 * s.x, v[0].y - 0.5 * s.y);
+  double2 d = mul_i_dir<DIR>(csub(v[1], v[2]));
+  d.x *= s3;
+  d.y *= s3;
+  v[0] = cadd(v[0], s);
+  v[1] = cadd(t, d);
+  v[2] = csub(t, d);
+}
+
+template <int DIR>
+__device__ __forceinline__ void bfly5(double2* v) {
+  // X_q = sum_t v_t w^{qt}, w = e^{DIR 2 pi i/5}
+  const double c1 = 0.309016994374947424102293417182819059;   // cos(2pi/5)
+  const double c2 = -0.809016994374947424102293417182819059;  // cos(4pi/5)
+  const double s1 = 0.951056516295153572116439333379382143;   // sin(2pi/5)
+  const double s2 = 0.587785252292473129168705954639072769;   // sin(4pi/5)
+  double2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+  double2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+  double2 r1 = make_double2(v[0].x + c1 * a1.x + c2 * a2.x, v[0].y + c1 * a1.y + c2 * a2.y);
+  double2 r2 = make_double2(v[0].x + c2 * a1.x + c1 * a2.x, v[0].y + c2 * a1.y + c1 * a2.y);
+  double2 i1 = make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
+  double2 i2 = make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
+  i1 = mul_i_dir<DIR>(i1);
+  i2 = mul_i_dir<DIR>(i2);
+  v[0] = make_double2(v[0].x + a1.x + a2.x, v[0].y + a1.y + a2.y);
+  v[1] = cadd(r1, i1);
+  v[4] = csub(r1, i1);
+  v[2] = cadd(r2, i2);
+  v[3] = csub(r2, i2);
+}
+
+// ------------------------------------------------------------------ one stage
+template <int R, int DIR>
+__device__ __forceinline__ void stage_fixed(const double2* __restrict__ in, double2* __restrict__ out,
+                                            int n, int Ns, const double2* __restrict__ tw, int nrows,
+                                            int rowstride, int tid, int nthr) {
+  const int nb = n / R;
+  const int total = nrows * nb;
+  for (int b = tid; b < total; b += nthr) {
+    const int row = b / nb, j = b - row * nb;
+    const int k = j % Ns;
+    const double2* src = in + row * rowstride;
+    double2 v[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[t] = src[j + t * nb];
+    if (k > 0) {
+#pragma unroll
+      for (int t = 1; t < R; ++t) {
+        double2 w = tw[k * (R - 1) + t - 1];
+        v[t] = DIR < 0 ? cmul(v[t], w) : cmulc(v[t], w);
+      }
+    }
+    if (R == 2) bfly2<DIR>(v);
+    if (R == 3) bfly3<DIR>(v);
+    if (R == 4) bfly4<DIR>(v);
+    if (R == 5) bfly5<DIR>(v);
+    double2* dst = out + row * rowstride + (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int q = 0; q < R; ++q) dst[q * Ns] = v[q];
+  }
+}
+
+template <int DIR>
+__device__ void stage_generic(const double2* __restrict__ in, double2* __restrict__ out, int n, int R,
+                              int Ns, const double2* __restrict__ tw, const double2* __restrict__ roots,
+                              int nrows, int rowstride, int tid, int nthr) {
+  const int nb = n / R;
+  const int total = nrows * nb;
+  for (int b = tid; b < total; b += nthr) {
+    const int row = b / nb, j = b - row * nb;
+    const int k = j % Ns;
+    const double2* src = in + row * rowstride;
+    double2 v[kMaxGenericRadix];
+    for (int t = 0; t < R; ++t) {
+      double2 x = src[j + t * nb];
+      if (k > 0 && t > 0) {
+        double2 w = tw[k * (R - 1) + t - 1];
+        x = DIR < 0 ? cmul(x, w) : cmulc(x, w);
+      }
+      v[t] = x;
+    }
+    double2* dst = out + row * rowstride + (j / Ns) * Ns * R + k;
+    for (int q = 0; q < R; ++q) {
+      double2 acc = v[0];
+      int e = 0;
+      for (int t = 1; t < R; ++t) {
+        e += q;
+        if (e >= R) e -= R;
+        double2 w = roots[e];
+        acc = cadd(acc, DIR < 0 ? cmul(v[t], w) : cmulc(v[t], w));
+      }
+      dst[q * Ns] = acc;
+    }
+  }
+}
+
+// Batched FFT of `nrows` rows (row r at buf[r*rowstride], length d.n) held in shared memory.
+// Uses `buf` and `tmp` as ping-pong buffers; returns the buffer holding the result.
+// Must be called by all `nthr` threads of the block (contains __syncthreads).
+template <int DIR>
+__device__ double2* fft_rows(double2* buf, double2* tmp, const FftDesc& d, const double2* __restrict__ tw,
+                             int nrows, int rowstride, int tid, int nthr) {
+  double2* in = buf;
+  double2* out = tmp;
+  int Ns = 1;
+  for (int s = 0; s < d.nst; ++s) {
+    const int R = d.rad[s];
+    const double2* tws = tw + d.twoff[s];
+    switch (R) {
+      case 2: stage_fixed<2, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      case 3: stage_fixed<3, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      case 4: stage_fixed<4, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      case 5: stage_fixed<5, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      default:
+        stage_generic<DIR>(in, out, d.n, R, Ns, tws, tw + d.rootoff[s], nrows, rowstride, tid, nthr);
+    }
+    __syncthreads();
+    double2* t = in;
+    in = out;
+    out = t;
+    Ns *= R;
+  }
+  return in;
+}
+
+// ------------------------------------------------------------------ host side
+// Factorise n into stage radices (4s first, then 2, 3, 5, other primes).  Returns false if a
+// prime factor exceeds kMaxGenericRadix or there are too many stages.
+bool fft_factor(int n, std::vector<int>& rad);
+// Build the descriptor and append its twiddle/root table to `table` (host), setting offsets.
+bool fft_make(int n, FftDesc& d, std::vector<double2>& table);
+// "FFT-friendly": only factors 2, 3, 5, 7.
+bool fft_friendly(int n);
+int next_friendly(int n);
+
+}  // namespace se1p

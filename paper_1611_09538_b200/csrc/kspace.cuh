@@ -1,0 +1,82 @@
+// kspace.cuh -- plan and workspace of the SE1P k-space path (Alg. 1).
+#pragma once
+#include <vector>
+
+#include "fft.cuh"
+
+namespace se1p {
+
+// Tile of the gridding / gather kernels on the extended grid (free x, free y, periodic z).
+constexpr int kTX = 8, kTY = 8, kTZ = 16;
+
+struct KParams {       // everything a k-space plan is keyed on
+  double L[3];
+  double xi;
+  int M, P;
+  double eta;          // resolved (> 0)
+  int n_l;             // resolved (>= 0)
+  int S0, SI, SJ;      // resolved padded extents
+  bool operator==(const KParams& o) const {
+    return L[0] == o.L[0] && L[1] == o.L[1] && L[2] == o.L[2] && xi == o.xi && M == o.M && P == o.P &&
+           eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ;
+  }
+};
+
+// Device view of the plan, passed by value to kernels.
+struct KDev {
+  int M, P, Mfree, Mt;          // grid: Mt x Mt (free, extended) x M (periodic)
+  double h, inv_h, alpha;       // alpha = 2 xi^2 / eta (window exponent)
+  double L3;
+  int nbx, nby, nbz;            // bins of kTX x kTY x kTZ cells
+  int ntx, nty, ntz;            // tiles over the Mt x Mt x M grid
+};
+
+struct KPlan {
+  KParams prm;
+  KDev dv;
+  int LK = 0;                   // FFT extent of the kernel (upsampled) planes
+  int n_planes = 0;             // M/2 + 1
+  int n_kernel = 0;             // planes 0..n_kernel-1 use the plan-time kernel (k3 = 0 and I)
+  FftDesc fz, fJ, fK;           // FFT lengths M, SJ, LK
+  double2* d_tw = nullptr;      // all twiddle tables
+  int twz = 0, twJ = 0, twK = 0;
+  double* d_khat = nullptr;     // [n_kernel][LK][LK] real kernel spectra (constants folded)
+  double* d_exJ = nullptr;      // [SJ] e^{-(1-eta) kappa_a^2/(4 xi^2)}, kappa_a = 2 pi a'/(SJ h)
+  double* d_k2J = nullptr;      // [SJ] kappa_a^2
+  double* d_pl = nullptr;       // [n_planes][2]: e^{-(1-eta) k3^2/(4xi^2)} * C_J, k3^2
+  int64_t t_off_total = 0;      // workspace T size (complex) for the 2D passes
+  std::vector<int64_t> t_off;   // per plane offset into T
+  double const_gather = 0;      // 4 pi h^3 (2 xi^2/(pi eta))^3 (reading R-1)
+  double plan_ms = 0;
+};
+
+struct KWork {                  // per-N workspace (grown on demand)
+  int64_t cap_xs = 0, cap_perm = 0, cap_keys = 0, cap_bs = 0, cap_total = 0;
+  double* xs = nullptr;         // sorted particles: x, y, z (folded), q  (SoA, 4 * N)
+  int* perm = nullptr;          // sorted position -> original index
+  int* keys = nullptr;
+  int* bin_start = nullptr;
+  int* hist = nullptr;
+  int64_t hist_cap = 0;
+  int* total = nullptr;
+  double* grid = nullptr;       // real grid Mt x Mt x M (H, then H~)
+  double2* planes = nullptr;    // Hk: n_planes x Mt x Mt
+  double2* T = nullptr;         // 2D pass workspace
+  int64_t grid_cap = 0, planes_cap = 0, T_cap = 0;
+  double* red = nullptr;        // reductions (neutrality check)
+  int* flag = nullptr;
+  double* host_x = nullptr;     // staging for host_io
+};
+
+KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached
+void kplan_release_all();
+
+// Stages (launch on st).
+void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
+void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);
+void k_zfft_forward(const KPlan& pl, KWork& w, cudaStream_t st);
+void k_mode_stage(const KPlan& pl, KWork& w, cudaStream_t st);
+void k_zfft_inverse(const KPlan& pl, KWork& w, cudaStream_t st);
+void k_gather(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
+
+}  // namespace se1p

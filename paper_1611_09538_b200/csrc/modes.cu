@@ -1,0 +1,291 @@
+// modes.cu -- the adaptive FFT of Alg. 2, the scaling of Alg. 1 step 4 and the inverse
+// adaptive FFT of Alg. 3, for the k3 >= 0 half of the modes.
+//
+// Layout:
+//   grid   [Mt][Mt][M]     real, z fastest           (H after gridding, H~ before gather)
+//   planes [M/2+1][Mt][Mt] complex, one plane per k3 (only the M~ x M~ content is stored;
+//                                                     padding to S is virtual)
+//   T      per plane [Mt][W] complex, W = LK (kernel planes) or SJ (J planes)
+//
+// Passes:  zfwd -> rowfwd -> colpass(FFT, multiply, IFFT) -> rowinv -> zinv.
+// J planes (s = 1): W = SJ and the multiplier is Eq. (scale_1p) sampled at kappa = 2 pi a'/(SJ h).
+// Kernel planes (k3 = 0 and the I modes): W = LK >= 2 M~ - 1 and the multiplier is the
+// plan-time spectrum of the exact aperiodic kernel equivalent to the paper's padded
+// transform of extent S.  All normalisations (1/M, 1/W^2) and the
+// gather constant are folded into the multipliers.
+#include "kspace.cuh"
+
+namespace se1p {
+
+static int zcols(int M) { return M >= 256 ? 8 : (M >= 64 ? 16 : 32); }
+static int rows_for(int W) { int r = 98304 / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
+static int cols_for(int W) { return W > 400 ? 4 : 8; }
+
+// ------------------------------------------------------------------ z-FFT (AFT step 1)
+__global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
+                       const double* __restrict__ grid, double2* __restrict__ planes) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + CB * M;
+  const int x = blockIdx.y, y0 = blockIdx.x * CB;
+  const double* src = grid + ((int64_t)x * Mt + y0) * M;
+  for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
+    const int c = idx / M;
+    buf[idx] = make_double2((y0 + c < Mt) ? src[idx] : 0.0, 0.0);
+  }
+  __syncthreads();
+  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CB, M, threadIdx.x, blockDim.x);
+  for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
+    const int n = idx / CB, c = idx - n * CB;
+    if (y0 + c < Mt) planes[((int64_t)n * Mt + x) * Mt + y0 + c] = out[c * M + n];
+  }
+}
+
+__global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
+                       const double2* __restrict__ planes, double* __restrict__ grid) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + CB * M;
+  const int x = blockIdx.y, y0 = blockIdx.x * CB;
+  for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
+    const int n = idx / CB, c = idx - n * CB;
+    double2 v = (y0 + c < Mt) ? planes[((int64_t)n * Mt + x) * Mt + y0 + c] : make_double2(0.0, 0.0);
+    buf[c * M + n] = v;
+    if (n > 0 && 2 * n < M) buf[c * M + (M - n)] = make_double2(v.x, -v.y);  // Hermitian half
+  }
+  __syncthreads();
+  double2* out = fft_rows<1>(buf, tmp, fz, tw, CB, M, threadIdx.x, blockDim.x);
+  double* dst = grid + ((int64_t)x * Mt + y0) * M;
+  for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
+    const int c = idx / M;
+    if (y0 + c < Mt) dst[idx] = out[idx].x;
+  }
+}
+
+// ------------------------------------------------------------------ 2D passes
+__global__ void k_rowfwd(int Mt, int W, int nfirst, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+                         const double2* __restrict__ planes, double2* __restrict__ T) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + RB * W;
+  const int n = nfirst + blockIdx.y, x0 = blockIdx.x * RB;
+  const int nr = min(RB, Mt - x0);
+  const double2* src = planes + ((int64_t)n * Mt + x0) * Mt;
+  for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
+    const int r = idx / W, y = idx - r * W;
+    buf[idx] = (r < nr && y < Mt) ? src[r * Mt + y] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2* out = fft_rows<-1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
+  double2* dst = T + base + (int64_t)(n - nfirst) * Mt * W + (int64_t)x0 * W;
+  for (int idx = threadIdx.x; idx < nr * W; idx += blockDim.x) dst[idx] = out[idx];
+}
+
+__global__ void k_rowinv(int Mt, int W, int nfirst, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+                         const double2* __restrict__ T, double2* __restrict__ planes) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + RB * W;
+  const int n = nfirst + blockIdx.y, x0 = blockIdx.x * RB;
+  const int nr = min(RB, Mt - x0);
+  const double2* src = T + base + (int64_t)(n - nfirst) * Mt * W + (int64_t)x0 * W;
+  for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
+    const int r = idx / W;
+    buf[idx] = (r < nr) ? src[idx] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2* out = fft_rows<1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
+  double2* dst = planes + ((int64_t)n * Mt + x0) * Mt;
+  for (int idx = threadIdx.x; idx < nr * Mt; idx += blockDim.x) {
+    const int r = idx / Mt, y = idx - r * Mt;
+    dst[r * Mt + y] = out[r * W + y];
+  }
+}
+
+// Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
+// kernel_class: multiplier = khat[(n - nfirst)][a][y]; else the J-plane scaling.
+__global__ void k_colpass(int Mt, int W, int nfirst, int64_t base, int CB, FftDesc f, const double2* __restrict__ tw,
+                          double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
+                          const double* __restrict__ exJ, const double* __restrict__ k2J,
+                          const double2* __restrict__ pl) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + CB * W;
+  const int n = nfirst + blockIdx.y, y0 = blockIdx.x * CB;
+  const int nc = min(CB, W - y0);
+  double2* Tp = T + base + (int64_t)(n - nfirst) * Mt * W;
+  for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
+    const int a = idx / CB, c = idx - a * CB;
+    buf[c * W + a] = (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, W, threadIdx.x, blockDim.x);
+  double2* oth = (out == buf) ? tmp : buf;
+  const double2 pn = pl[n];
+  for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
+    const int c = idx / W, a = idx - c * W;
+    const int y = min(y0 + c, W - 1);
+    double m;
+    if (kernel_class) {
+      m = khat[((int64_t)(n - nfirst) * W + a) * W + y];
+    } else {
+      m = pn.x * exJ[a] * exJ[y] / (k2J[a] + k2J[y] + pn.y);
+    }
+    double2 v = out[idx];
+    out[idx] = make_double2(v.x * m, v.y * m);
+  }
+  __syncthreads();
+  double2* res = fft_rows<1>(out, oth, f, tw, CB, W, threadIdx.x, blockDim.x);
+  for (int idx = threadIdx.x; idx < Mt * CB; idx += blockDim.x) {
+    const int a = idx / CB, c = idx - a * CB;
+    if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * W + a];
+  }
+}
+
+static void set_smem(const void* fn, size_t bytes) {
+  SE1P_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+void k_zfft_forward(const KPlan& pl, KWork& w, cudaStream_t st) {
+  const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
+  const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
+  set_smem((const void*)k_zfwd, smem);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)Mt);
+  k_zfwd<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, w.planes);
+  SE1P_LAUNCH_CHECK();
+}
+
+void k_zfft_inverse(const KPlan& pl, KWork& w, cudaStream_t st) {
+  const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
+  const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
+  set_smem((const void*)k_zinv, smem);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)Mt);
+  k_zinv<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.planes, w.grid);
+  SE1P_LAUNCH_CHECK();
+}
+
+static void mode_class(const KPlan& pl, KWork& w, int nfirst, int nplanes, int W, const FftDesc& f, int twoff,
+                       int64_t base, int kernel_class, cudaStream_t st) {
+  if (nplanes <= 0) return;
+  const int Mt = pl.dv.Mt;
+  const int RB = rows_for(W), CB = cols_for(W);
+  const size_t smr = 2 * (size_t)RB * W * sizeof(double2), smc = 2 * (size_t)CB * W * sizeof(double2);
+  set_smem((const void*)k_rowfwd, smr);
+  set_smem((const void*)k_rowinv, smr);
+  set_smem((const void*)k_colpass, smc);
+  const double2* tw = pl.d_tw + twoff;
+  k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, nfirst, base, RB, f, tw, w.planes, w.T);
+  SE1P_LAUNCH_CHECK();
+  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), 256, smc, st>>>(Mt, W, nfirst, base, CB, f, tw, w.T, kernel_class,
+                                                                        pl.d_khat, pl.d_exJ, pl.d_k2J,
+                                                                        (const double2*)pl.d_pl);
+  SE1P_LAUNCH_CHECK();
+  k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, nfirst, base, RB, f, tw, w.T, w.planes);
+  SE1P_LAUNCH_CHECK();
+}
+
+void k_mode_stage(const KPlan& pl, KWork& w, cudaStream_t st) {
+  const int Mt = pl.dv.Mt;
+  // kernel planes 0 .. n_kernel-1 (k3 = 0 and the I modes), then J planes
+  mode_class(pl, w, 0, pl.n_kernel, pl.LK, pl.fK, pl.twK, 0, 1, st);
+  const int64_t baseJ = (int64_t)pl.n_kernel * Mt * pl.LK;
+  mode_class(pl, w, pl.n_kernel, pl.n_planes - pl.n_kernel, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
+}
+
+// ------------------------------------------------------------------ plan-time kernel spectra
+// sig: (S/2+1)^2 table of the scaling function over |a'|,|b'| (host computed).
+// Step A: tmp[d][m2] = sum_{m1} mult(m1) sig[m1][m2] cos(2 pi m1 d/S), d < Mt, m2 <= S/2.
+__global__ void k_kern_a(int S, int Mt, const double* __restrict__ sig, double* __restrict__ tmp) {
+  const int H = S / 2 + 1;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)Mt * H) return;
+  const int d = (int)(id / H), m2 = (int)(id - (int64_t)d * H);
+  double acc = 0.0;
+  for (int m1 = 0; m1 < H; ++m1) {
+    const double mult = (m1 == 0 || 2 * m1 == S) ? 1.0 : 2.0;
+    const long long r = ((long long)m1 * d) % S;
+    acc = fma(mult * sig[(int64_t)m1 * H + m2], cospi(2.0 * (double)r / (double)S), acc);
+  }
+  tmp[id] = acc;
+}
+
+// Step B: K[d1][d2] = (1/S^2) sum_{m2} mult(m2) tmp[d1][m2] cos(2 pi m2 d2/S), written into the
+// LK x LK complex array at (+-d1 mod LK, +-d2 mod LK).
+__global__ void k_kern_b(int S, int Mt, int LK, const double* __restrict__ tmp, double2* __restrict__ KL) {
+  const int H = S / 2 + 1;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)Mt * Mt) return;
+  const int d1 = (int)(id / Mt), d2 = (int)(id - (int64_t)d1 * Mt);
+  double acc = 0.0;
+  for (int m2 = 0; m2 < H; ++m2) {
+    const double mult = (m2 == 0 || 2 * m2 == S) ? 1.0 : 2.0;
+    const long long r = ((long long)m2 * d2) % S;
+    acc = fma(mult * tmp[(int64_t)d1 * H + m2], cospi(2.0 * (double)r / (double)S), acc);
+  }
+  acc /= (double)S * (double)S;
+  const int i1[2] = {d1, (LK - d1) % LK}, i2[2] = {d2, (LK - d2) % LK};
+  for (int s1 = 0; s1 < 2; ++s1)
+    for (int s2 = 0; s2 < 2; ++s2) KL[(int64_t)i1[s1] * LK + i2[s2]] = make_double2(acc, 0.0);
+}
+
+// In-place FFT of the rows of an n x n complex matrix (plan-time helper).
+__global__ void k_fft_rows_inplace(int n, int RB, FftDesc f, const double2* __restrict__ tw, double2* __restrict__ A) {
+  extern __shared__ double2 sm[];
+  double2* buf = sm;
+  double2* tmp = sm + RB * n;
+  const int r0 = blockIdx.x * RB, nr = min(RB, n - r0);
+  for (int idx = threadIdx.x; idx < RB * n; idx += blockDim.x)
+    buf[idx] = (idx / n < nr) ? A[(int64_t)r0 * n + idx] : make_double2(0.0, 0.0);
+  __syncthreads();
+  double2* out = fft_rows<-1>(buf, tmp, f, tw, RB, n, threadIdx.x, blockDim.x);
+  for (int idx = threadIdx.x; idx < nr * n; idx += blockDim.x) A[(int64_t)r0 * n + idx] = out[idx];
+}
+
+__global__ void k_transpose_scale_real(int n, double scale, const double2* __restrict__ A, double* __restrict__ out) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)n * n) return;
+  const int i = (int)(id / n), j = (int)(id - (int64_t)i * n);
+  out[id] = A[(int64_t)j * n + i].x * scale;
+}
+
+__global__ void k_transpose(int n, const double2* __restrict__ A, double2* __restrict__ B) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)n * n) return;
+  const int i = (int)(id / n), j = (int)(id - (int64_t)i * n);
+  B[id] = A[(int64_t)j * n + i];
+}
+
+// Device part of the kernel spectrum: sig (host table, device copy) -> khat_out [LK][LK].
+void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* khat_out, double scale,
+                           cudaStream_t st) {
+  const int Mt = pl.dv.Mt, LK = pl.LK, H = S / 2 + 1;
+  double* tmp = nullptr;
+  double2 *A = nullptr, *B = nullptr;
+  SE1P_CUDA_TRY(cudaMalloc(&tmp, sizeof(double) * (size_t)Mt * H));
+  SE1P_CUDA_TRY(cudaMalloc(&A, sizeof(double2) * (size_t)LK * LK));
+  SE1P_CUDA_TRY(cudaMalloc(&B, sizeof(double2) * (size_t)LK * LK));
+  SE1P_CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * (size_t)LK * LK, st));
+  k_kern_a<<<(unsigned)ceil_div((int64_t)Mt * H, 128), 128, 0, st>>>(S, Mt, d_sig, tmp);
+  SE1P_LAUNCH_CHECK();
+  k_kern_b<<<(unsigned)ceil_div((int64_t)Mt * Mt, 128), 128, 0, st>>>(S, Mt, LK, tmp, A);
+  SE1P_LAUNCH_CHECK();
+  const int RB = rows_for(LK);
+  const size_t sm = 2 * (size_t)RB * LK * sizeof(double2);
+  set_smem((const void*)k_fft_rows_inplace, sm);
+  const double2* tw = pl.d_tw + pl.twK;
+  k_fft_rows_inplace<<<(unsigned)ceil_div(LK, RB), 256, sm, st>>>(LK, RB, pl.fK, tw, A);
+  SE1P_LAUNCH_CHECK();
+  k_transpose<<<(unsigned)ceil_div((int64_t)LK * LK, 256), 256, 0, st>>>(LK, A, B);
+  SE1P_LAUNCH_CHECK();
+  k_fft_rows_inplace<<<(unsigned)ceil_div(LK, RB), 256, sm, st>>>(LK, RB, pl.fK, tw, B);
+  SE1P_LAUNCH_CHECK();
+  // B = transpose of the 2D spectrum; transpose back while taking the (real) value
+  k_transpose_scale_real<<<(unsigned)ceil_div((int64_t)LK * LK, 256), 256, 0, st>>>(LK, scale, B, khat_out);
+  SE1P_LAUNCH_CHECK();
+  SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  cudaFree(A);
+  cudaFree(B);
+}
+
+}  // namespace se1p

@@ -1,0 +1,100 @@
+// real.cu -- real-space sum phi^R (Eq. (3)) truncated at rc with linked cells
+// and the self term (Eq. (6)).
+//
+// Cells: nc_d = max(1, floor(L_d/rc)) per axis, so a cell is at least rc wide; free axes
+// scan the 3 neighbouring cells (no images), the periodic axis scans the unwrapped cells
+// cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell (u mod nc_z)
+// shifted by floor(u/nc_z) L3.  Every image within rc is visited exactly once, for any rc.
+#include "kspace.cuh"
+#include "real.cuh"
+#include "sort.cuh"
+
+namespace se1p {
+
+__device__ __forceinline__ int rfloordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+__global__ void k_real_keys(RDev d, const double* __restrict__ x, int64_t N, int* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double pz = x[3 * i + 2];
+  pz -= d.L[2] * floor(pz / d.L[2]);
+  if (pz >= d.L[2]) pz -= d.L[2];
+  int cx = min(max((int)floor(x[3 * i] / d.cs[0]), 0), d.nc[0] - 1);
+  int cy = min(max((int)floor(x[3 * i + 1] / d.cs[1]), 0), d.nc[1] - 1);
+  int cz = min(max((int)floor(pz / d.cs[2]), 0), d.nc[2] - 1);
+  keys[i] = (cx * d.nc[1] + cy) * d.nc[2] + cz;
+}
+
+__global__ void k_real_permute(RDev d, const double* __restrict__ x, const double* __restrict__ q,
+                               const int* __restrict__ perm, int64_t N, double4* __restrict__ out) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  const int64_t i = perm[s];
+  double pz = x[3 * i + 2];
+  pz -= d.L[2] * floor(pz / d.L[2]);
+  if (pz >= d.L[2]) pz -= d.L[2];
+  out[s] = make_double4(x[3 * i], x[3 * i + 1], pz, q[i]);
+}
+
+// One thread per target (sorted order, so neighbouring threads share cells).
+__global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restrict__ P4, const int* __restrict__ perm,
+                                                  const int* __restrict__ cell_start, int64_t N,
+                                                  double* __restrict__ phi_out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N) return;
+  const double4 pt = P4[t];
+  const int cx = min(max((int)floor(pt.x / d.cs[0]), 0), d.nc[0] - 1);
+  const int cy = min(max((int)floor(pt.y / d.cs[1]), 0), d.nc[1] - 1);
+  const int cz = min(max((int)floor(pt.z / d.cs[2]), 0), d.nc[2] - 1);
+  const double rc2 = d.rc * d.rc;
+  double acc = 0.0;
+  for (int ax = max(0, cx - 1); ax <= min(d.nc[0] - 1, cx + 1); ++ax)
+    for (int ay = max(0, cy - 1); ay <= min(d.nc[1] - 1, cy + 1); ++ay)
+      for (int u = cz - d.K; u <= cz + d.K; ++u) {
+        const int w = rfloordiv(u, d.nc[2]);
+        const int az = u - w * d.nc[2];
+        const double shift = w * d.L[2];
+        const int c = (ax * d.nc[1] + ay) * d.nc[2] + az;
+        const int s = cell_start[c], e = cell_start[c + 1];
+        for (int j = s; j < e; ++j) {
+          if (w == 0 && j == t) continue;   // the prime in Eq. (3): n = m only at p = 0
+          const double4 ps = P4[j];
+          const double dx = pt.x - ps.x, dy = pt.y - ps.y, dz = pt.z - (ps.z + shift);
+          const double r2 = dx * dx + dy * dy + dz * dz;
+          if (r2 <= rc2) {
+            const double r = sqrt(r2);
+            acc = fma(ps.w, erfc(d.xi * r) / r, acc);
+          }
+        }
+      }
+  phi_out[perm[t]] = acc - 2.0 * d.xi * pt.w * 0.564189583547756286948079451560772586;  // 1/sqrt(pi)
+}
+
+RDev real_geometry(const double L[3], double xi, double rc) {
+  RDev d;
+  for (int a = 0; a < 3; ++a) {
+    d.L[a] = L[a];
+    d.nc[a] = std::max(1, (int)std::floor(L[a] / rc));
+    d.nc[a] = std::min(d.nc[a], 256);
+    d.cs[a] = L[a] / d.nc[a];
+  }
+  d.K = (int)std::ceil(rc / d.cs[2]);
+  d.xi = xi;
+  d.rc = rc;
+  return d;
+}
+
+void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
+                cudaStream_t st) {
+  const int ncell = d.nc[0] * d.nc[1] * d.nc[2];
+  const unsigned nb = (unsigned)ceil_div(N, 256);
+  k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
+  SE1P_LAUNCH_CHECK();
+  stable_bin_sort(w.keys, N, ncell, w.perm, w.bin_start, w.hist, w.total, st);
+  k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
+  SE1P_LAUNCH_CHECK();
+  k_real_sum<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out);
+  SE1P_LAUNCH_CHECK();
+}
+
+}  // namespace se1p

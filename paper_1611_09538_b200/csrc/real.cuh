@@ -1,0 +1,22 @@
+// real.cuh -- real-space geometry (see real.cu).
+#pragma once
+#include <algorithm>
+#include <cmath>
+
+#include "kspace.cuh"
+
+namespace se1p {
+
+struct RDev {
+  double L[3];
+  double cs[3];   // cell sizes
+  int nc[3];      // cells per axis
+  int K;          // periodic-axis cell reach
+  double xi, rc;
+};
+
+RDev real_geometry(const double L[3], double xi, double rc);
+void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
+                cudaStream_t st);
+
+}  // namespace se1p

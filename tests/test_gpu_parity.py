@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances:
+  * element-wise vs the step-by-step Alg. 1 oracle (same discretisation): |d| <= 1e-11 max|phi|.
+    Both evaluate the same discrete sums in fp64; the GPU applies the upsampled planes as an
+    exact aperiodic convolution and sums in another order, so they differ by rounding only
+    (~ eps * log2(FFT size) * dynamic range of the spectra).
+  * full potential vs the exact Ewald1P oracle: relative rms <= 1e-9 (BASELINE north_star).
+  * real space vs the oracle's direct sum: |d| <= 1e-12 max|phi|.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import se1p_discrete as sd
+from se1p_synth import CONFIGS, make_system
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1611_09538_b200 as se1p  # noqa: E402
+
+
+def _dev(x, q):
+    return (torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+
+
+def _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, **kw):
+    xd, qd = _dev(x, q)
+    return se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=S0, SI=SI, Ntilde=SJ, **kw).cpu().numpy()
+
+
+CASES = [
+    # name, N, L, xi, M, P, n_l, S0, SI, SJ, seed
+    ("C1", 100, (1, 1, 1), 4.0, 16, 16, 2, 110, 64, 32, 1),
+    ("C1-wide", 100, (1, 1, 1), 4.0, 16, 16, 2, 256, 256, 40, 1),
+    ("C2", 2000, (1, 1, 1), 8.0, 32, 20, 3, 416, 416, 64, 2),
+    ("tiny-odd", 37, (1, 1, 1), 3.0, 8, 6, 1, 40, 36, 15, 5),
+    ("ragged-tiles", 333, (1, 1, 1), 5.0, 20, 10, 3, 90, 75, 35, 6),
+    ("longz", 150, (1, 1, 2), 4.0, 24, 8, 4, 60, 72, 21, 7),
+    ("plain-upsampled", 80, (1, 1, 1), 4.0, 12, 8, 6, 60, 60, 60, 8),
+    ("prime-extent", 60, (1, 1, 1), 4.0, 12, 8, 2, 53, 47, 23, 9),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_kspace_matches_alg1_oracle(case):
+    name, N, L, xi, M, P, n_l, S0, SI, SJ, seed = case
+    x, q = make_system(N, L, seed)
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    err = np.max(np.abs(got - ref))
+    assert err <= 1e-11 * np.max(np.abs(ref)), (name, err, np.max(np.abs(ref)))
+
+
+def test_kspace_single_particle_and_pair():
+    """Degenerate cases: N = 2 coaxial pair (rho = 0 in the zero mode) and a lone particle
+    (non-neutral -> refused unless checks are skipped; then it is still well defined)."""
+    L = (1.0, 1.0, 1.0)
+    x = np.array([[0.45, 0.55, 0.1], [0.45, 0.55, 0.4]])
+    q = np.array([1.0, -1.0])
+    ref = sd.se1p_kspace(x, q, L, 5.0, 16, 12, 8, 112, 112, 56)
+    got = _gpu_kspace(x, q, L, 5.0, 16, 12, 8, 112, 112, 56)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+    x1, q1 = x[:1], np.array([1.0])
+    with pytest.raises(se1p.SE1PError) as ei:
+        _gpu_kspace(x1, q1, L, 5.0, 16, 12, 2, 112, 84, 28)
+    assert ei.value.code == 3
+    ref1 = sd.se1p_kspace(x1, q1, L, 5.0, 16, 12, 2, 112, 84, 28)
+    got1 = _gpu_kspace(x1, q1, L, 5.0, 16, 12, 2, 112, 84, 28, skip_checks=True)
+    assert abs(got1[0] - ref1[0]) <= 1e-11 * abs(ref1[0])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_potential_vs_exact_oracle(cfg):
+    c = CONFIGS[cfg]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    phi = (se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, s0=c.s0, sf=c.sf, n_local=c.n_local, Ntilde=c.Ntilde)
+           + se1p.real(xd, qd, c.L, c.xi, c.rc)).cpu().numpy()
+    ref = oracle.phi_exact(x, q, c.L)
+    assert oracle.rel_rms(phi, ref) <= 1e-9
+
+
+def test_real_space_vs_oracle():
+    for L, xi, rc, N, seed in [((1, 1, 1), 4.0, 1.158, 100, 1), ((1, 1, 1), 8.0, 0.594, 500, 2),
+                               ((1, 1, 2), 12.0, 0.401, 800, 3), ((2, 2, 2), 30.0, 0.1, 3000, 5),
+                               ((1, 1, 1), 3.0, 2.7, 40, 4)]:
+        x, q = make_system(N, L, seed)
+        xd, qd = _dev(x, q)
+        got = se1p.real(xd, qd, L, xi, rc).cpu().numpy()
+        ref = oracle.phi_real(x, q, L, xi, rc) + oracle.phi_self(q, xi)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)), (L, xi, rc)
+
+
+def test_bitwise_determinism_and_host_io():
+    c = CONFIGS["C2"]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    kw = dict(n_local=3, S0=416, SI=416, Ntilde=64)
+    a = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw).cpu().numpy()
+    b = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw).cpu().numpy()
+    h = se1p.kspace(x, q, c.L, c.xi, c.M, c.P, **kw)          # numpy in -> host I/O path
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, h)
+    r1 = se1p.real(xd, qd, c.L, c.xi, c.rc).cpu().numpy()
+    r2 = se1p.real(x, q, c.L, c.xi, c.rc)
+    assert np.array_equal(r1, r2)
+
+
+def test_invariances():
+    """z-translation by one grid step is exact on the grid; permuting particles permutes phi;
+    phi is linear in q."""
+    L, xi, M, P = (1.0, 1.0, 1.0), 6.0, 24, 14
+    x, q = make_system(300, L, 11)
+    kw = dict(n_local=3, S0=300, SI=300, Ntilde=48)
+    base = _gpu_kspace(x, q, L, xi, M, P, **{"n_l": 3, "S0": 300, "SI": 300, "SJ": 48})
+    xs = x.copy()
+    xs[:, 2] = (xs[:, 2] + 1.0 / M) % 1.0
+    shifted = _gpu_kspace(xs, q, L, xi, M, P, 3, 300, 300, 48)
+    assert np.max(np.abs(shifted - base)) <= 1e-12 * np.max(np.abs(base))
+    p = np.random.default_rng(0).permutation(300)
+    perm = _gpu_kspace(x[p], q[p], L, xi, M, P, 3, 300, 300, 48)
+    assert np.max(np.abs(perm - base[p])) <= 1e-12 * np.max(np.abs(base))
+    neg = _gpu_kspace(x, -2.5 * q, L, xi, M, P, 3, 300, 300, 48)
+    assert np.max(np.abs(neg + 2.5 * base)) <= 1e-12 * np.max(np.abs(base))
+    del kw
+
+
+def test_errors():
+    L = (1.0, 1.0, 1.0)
+    x, q = make_system(50, L, 12)
+    xd, qd = _dev(x, q)
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(xd, qd + 0.1, L, 4.0, 16, 8)
+    assert e.value.code == 3
+    xb = x.copy()
+    xb[3, 0] = 1.2
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(torch.from_numpy(xb).cuda(), qd, L, 4.0, 16, 8)
+    assert e.value.code == 2
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(xd, qd, (1.0, 1.0, 1.0), 4.0, 15, 8)      # odd M
+    assert e.value.code == 4
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(xd, qd, (1.0, 1.3, 1.0), 4.0, 16, 8)      # L2/h not an integer
+    assert e.value.code == 4
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(xd, qd, L, 4.0, 16, 8, n_local=20)
+    assert e.value.code == 4
+    # z outside [0, L3) is folded, not an error
+    xz = x.copy()
+    xz[:, 2] += 3.0
+    a = se1p.kspace(torch.from_numpy(xz).cuda(), qd, L, 4.0, 16, 8, n_local=2, S0=96, SI=72, Ntilde=24).cpu().numpy()
+    b = se1p.kspace(xd, qd, L, 4.0, 16, 8, n_local=2, S0=96, SI=72, Ntilde=24).cpu().numpy()
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+
+
+def test_plan_info_defaults():
+    info = se1p.plan_info((1.0, 1.0, 1.0), 4.0, 16, 16, s0=2 + math.sqrt(2), sf=2.0, n_local=2)
+    assert info["Mt"] == 32 and info["S0"] == 110 and info["SI"] == 64
+    assert info["LK"] >= 2 * 32 - 1 and info["n_kernel_planes"] == 3 and info["n_planes"] == 9
+    assert abs(info["eta"] - 16 * 16.0 / 256 / (0.95 ** 2 * math.pi)) < 1e-15
