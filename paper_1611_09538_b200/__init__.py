@@ -84,7 +84,8 @@ def _check(code):
         raise SE1PError(code, load().se1p_last_error().decode())
 
 
-def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0):
+def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0,
+          reference_kernels=False):
     o = Opts()
     o.Ntilde = int(Ntilde or 0)
     o.S0 = int(S0 or 0)
@@ -94,7 +95,24 @@ def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=
     o.sync = int(bool(sync))
     o.reserved[0] = 1 if profile else 0
     o.reserved[1] = int(stop_after)
+    o.reserved[2] = 1 if reference_kernels else 0
+    o.reserved[3] = 1 if os.environ.get("SE1P_PHASE_COUNTERS") == "1" else 0
     return o
+
+
+def phase_counters():
+    """Debug: clock64 phase counters of the last gridding (first 16) and gather (last 16) tile
+    kernels, recorded when SE1P_PHASE_COUNTERS=1."""
+    buf = np.zeros(32)
+    _check(load().se1p_debug_copy(2, buf.ctypes.data, 32))
+    names = ["prod_total", "prod_wait_empty", "prod_stage", "prod_candidates", "batches", "", "", "",
+             "cons_total", "cons_wait_full", "cons_list", "cons_kstep", "mma_issued"]
+    out = {}
+    for base, tag in ((0, "spread"), (16, "gather")):
+        for i, nm in enumerate(names):
+            if nm:
+                out[f"{tag}.{nm}"] = buf[base + i]
+    return out
 
 
 def _Larr(L):
@@ -132,8 +150,10 @@ def _neg(v, default=-1.0):
 
 
 def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
-           out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0):
-    """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1)."""
+           out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0,
+           reference_kernels=False):
+    """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1).
+    reference_kernels=True selects the simple v1 gridding/gather kernels (A/B testing)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
     if host:
@@ -143,7 +163,7 @@ def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=N
         import torch
         out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
         optr = out.data_ptr()
-    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after)
+    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels)
     _check(lib.se1p_kspace_ex(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
                               _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr))
     return out

@@ -52,6 +52,8 @@ static void grow(T*& p, int64_t& cap, int64_t need) {
 
 static void ensure_particles(KWork& w, int64_t N, int nbins) {
   grow(w.xs, w.cap_xs, 4 * N);
+  grow(w.s4, w.cap_s4, 4 * N);
+  grow(w.f6, w.cap_f6, 6 * N);
   grow(w.perm, w.cap_perm, N);
   grow(w.keys, w.cap_keys, N);
   grow(w.bin_start, w.cap_bs, (int64_t)nbins + 1);
@@ -228,7 +230,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   DevState& ds = dev_state();
   KWork& w = ds.w;
   const KDev& dv = pl->dv;
-  ensure_particles(w, N, dv.nbx * dv.nby * dv.nbz);
+  ensure_particles(w, N, dv.nbx * dv.nby * dv.M);
   grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
   grow(w.planes, w.planes_cap, (int64_t)pl->n_planes * dv.Mt * dv.Mt);
   grow(w.T, w.T_cap, pl->t_off_total);
@@ -246,10 +248,18 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, true, st);
   StageTimer tm(o && o->reserved[0] == 1, st);
   const int stop = o ? o->reserved[1] : 0;
+  const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
+  if (!v1) grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+  w.prof_on = o && o->reserved[3] == 1;       // phase counters of the tile kernels
+  if (w.prof_on) {
+    if (!w.prof) SE1P_CUDA_TRY(cudaMalloc(&w.prof, 32 * sizeof(unsigned long long)));
+    SE1P_CUDA_TRY(cudaMemsetAsync(w.prof, 0, 32 * sizeof(unsigned long long), st));
+  }
   tm.mark();
   k_bin_particles(*pl, w, dx, dq, N, st);
   tm.mark();
-  k_spread(*pl, w, N, st);
+  if (v1) k_spread(*pl, w, N, st);
+  else k_spread_mma(*pl, w, N, st);
   tm.mark();
   if (stop == 1) return sync_and_check(st);
   k_zfft_forward(*pl, w, st);
@@ -261,7 +271,8 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   k_zfft_inverse(*pl, w, st);
   tm.mark();
   if (stop == 4) return sync_and_check(st);
-  k_gather(*pl, w, N, dphi, st);
+  if (v1) k_gather(*pl, w, N, dphi, st);
+  else k_gather_mma(*pl, w, N, dphi, st);
   tm.mark();
   if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   tm.finish();
@@ -381,6 +392,11 @@ int se1p_debug_copy(int which, double* host_dst, int64_t count) {
     } else if (which == 1) {
       if (count > 2 * w.planes_cap) throw Error{1, "plane buffer smaller than requested"};
       SE1P_CUDA_TRY(cudaMemcpy(host_dst, w.planes, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    } else if (which == 2) {
+      if (count > 32 || !w.prof) throw Error{1, "no phase counters (run with profiling counters on)"};
+      unsigned long long h[32];
+      SE1P_CUDA_TRY(cudaMemcpy(h, w.prof, sizeof h, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < count; ++i) host_dst[i] = (double)h[i];
     } else {
       throw Error{1, "unknown buffer"};
     }
@@ -395,7 +411,8 @@ void se1p_release(void) {
   DevState& ds = g_dev[d & 63];
   KWork& w = ds.w;
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.hist, (void*)w.total,
-                  (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx})
+                  (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
+                  (void*)w.gpart})
     if (p) cudaFree(p);
   ds = DevState{};
 }

@@ -28,7 +28,11 @@ struct KDev {
   double h, inv_h, alpha;       // alpha = 2 xi^2 / eta (window exponent)
   double L3;
   int nbx, nby, nbz;            // bins of kTX x kTY x kTZ cells
-  int ntx, nty, ntz;            // tiles over the Mt x Mt x M grid
+  int ntx, nty, ntz;            // tiles over the Mt x Mt x M grid (v1 kernels)
+  int nty2;                     // 16-wide tiles of the DMMA kernels
+  int nsxy, nsz, nslot;         // gather partial slots per particle
+  unsigned long long* prof;     // optional phase counters of the tile kernels (nullptr = off)
+  int dbg;                      // debug experiment bits of the tile kernels (0 = normal)
 };
 
 struct KPlan {
@@ -52,7 +56,10 @@ struct KPlan {
 
 struct KWork {                  // per-N workspace (grown on demand)
   int64_t cap_xs = 0, cap_perm = 0, cap_keys = 0, cap_bs = 0, cap_total = 0;
-  double* xs = nullptr;         // sorted particles: x, y, z (folded), q  (SoA, 4 * N)
+  double* xs = nullptr;         // sorted particles: x, y, z (folded), q  (double4 per particle)
+  int* s4 = nullptr;            // sorted stencil starts: jx0, jy0, lz0, lz0 mod M (int4)
+  double* f6 = nullptr;         // sorted FGG factors A_x, E_x, A_y, E_y, A_z, E_z
+  int64_t cap_s4 = 0, cap_f6 = 0;
   int* perm = nullptr;          // sorted position -> original index
   int* keys = nullptr;
   int* bin_start = nullptr;
@@ -63,6 +70,10 @@ struct KWork {                  // per-N workspace (grown on demand)
   double2* planes = nullptr;    // Hk: n_planes x Mt x Mt
   double2* T = nullptr;         // 2D pass workspace
   int64_t grid_cap = 0, planes_cap = 0, T_cap = 0;
+  unsigned long long* prof = nullptr;   // 32 phase counters of the tile kernels (debug)
+  bool prof_on = false;
+  double* gpart = nullptr;      // gather partials [N][nslot]
+  int64_t gpart_cap = 0;
   double* red = nullptr;        // reductions (neutrality check)
   int* flag = nullptr;
   double* host_x = nullptr;     // staging for host_io
@@ -73,7 +84,12 @@ void kplan_release_all();
 
 // Stages (launch on st).
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
-void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);
+void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
+void k_spread_mma(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);      // DMMA tiles
+void k_gather_mma(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
+int64_t gather_slots(const KDev& dv);
+void slot_geometry(KDev& dv);
+int tile_tz(int M);
 void k_zfft_forward(const KPlan& pl, KWork& w, cudaStream_t st);
 void k_mode_stage(const KPlan& pl, KWork& w, cudaStream_t st);
 void k_zfft_inverse(const KPlan& pl, KWork& w, cudaStream_t st);

@@ -25,28 +25,53 @@ __global__ void k_keys(KDev dv, const double* __restrict__ x, int64_t N, int* __
   cx = min(max(cx, 0), dv.Mfree - 1);
   cy = min(max(cy, 0), dv.Mfree - 1);
   cz = min(max(cz, 0), dv.M - 1);
-  keys[i] = ((cx / kTX) * dv.nby + (cy / kTY)) * dv.nbz + cz / kTZ;
+  // bins: xy columns of kTX x kTY cells, z-sorted by cell inside a column
+  keys[i] = ((cx / kTX) * dv.nby + (cy / kTY)) * dv.M + cz;
 }
 
+// Sorted particle records: position/charge, stencil starts (reading R-3) and the per-particle
+// Fast Gaussian Gridding factors of each axis: with d0 the signed distance from the
+// particle to the first stencil node, the window weight at stencil offset t is
+//   e^{-alpha (d0 + t h)^2} = A E^t f1(t),  A = e^{-alpha d0^2},  E = e^{-2 alpha h d0},
+//   f1(t) = e^{-alpha h^2 t^2} (particle independent).
 __global__ void k_permute(KDev dv, const double* __restrict__ x, const double* __restrict__ q,
-                          const int* __restrict__ perm, int64_t N, double4* __restrict__ out) {
+                          const int* __restrict__ perm, int64_t N, double4* __restrict__ out,
+                          int4* __restrict__ s4, double* __restrict__ f6) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= N) return;
   const int64_t i = perm[s];
   double pz = x[3 * i + 2];
   pz -= dv.L3 * floor(pz / dv.L3);
   if (pz >= dv.L3) pz -= dv.L3;
-  out[s] = make_double4(x[3 * i], x[3 * i + 1], pz, q[i]);
+  const double px = x[3 * i], py = x[3 * i + 1];
+  out[s] = make_double4(px, py, pz, q[i]);
+  int cx = (int)floor(px * dv.inv_h), cy = (int)floor(py * dv.inv_h);
+  cx = min(max(cx, 0), dv.Mfree - 1);
+  cy = min(max(cy, 0), dv.Mfree - 1);
+  const int jx0 = cx + 1, jy0 = cy + 1, lz0 = (int)floor(pz * dv.inv_h - 0.5 * dv.P) + 1;
+  int a = lz0 % dv.M;
+  if (a < 0) a += dv.M;
+  s4[s] = make_int4(jx0, jy0, lz0, a);
+  const double dx = ((double)jx0 - 0.5 * dv.P) * dv.h - px;
+  const double dy = ((double)jy0 - 0.5 * dv.P) * dv.h - py;
+  const double dz = (double)lz0 * dv.h - pz;
+  double* f = f6 + 6 * s;
+  f[0] = exp(-dv.alpha * dx * dx);
+  f[1] = exp(-2.0 * dv.alpha * dv.h * dx);
+  f[2] = exp(-dv.alpha * dy * dy);
+  f[3] = exp(-2.0 * dv.alpha * dv.h * dy);
+  f[4] = exp(-dv.alpha * dz * dz);
+  f[5] = exp(-2.0 * dv.alpha * dv.h * dz);
 }
 
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st) {
   const KDev& dv = pl.dv;
-  const int nbins = dv.nbx * dv.nby * dv.nbz;
+  const int nbins = dv.nbx * dv.nby * dv.M;
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_keys<<<nb, 256, 0, st>>>(dv, x, N, w.keys);
   SE1P_LAUNCH_CHECK();
   stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.hist, w.total, st);
-  k_permute<<<nb, 256, 0, st>>>(dv, x, q, w.perm, N, (double4*)w.xs);
+  k_permute<<<nb, 256, 0, st>>>(dv, x, q, w.perm, N, (double4*)w.xs, (int4*)w.s4, w.f6);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -109,8 +134,8 @@ __global__ void __launch_bounds__(128) k_spread_v1(KDev dv, const double4* __res
     for (int by = by0; by <= by1; ++by)
       for (int bzu = bz0; bzu <= bz1; ++bzu) {
         const int bz = imod(bzu, dv.nbz);
-        const int b = (bx * dv.nby + by) * dv.nbz + bz;
-        const int s = bin_start[b], e = bin_start[b + 1];
+        const int col = (bx * dv.nby + by) * dv.M;
+        const int s = bin_start[col + bz * kTZ], e = bin_start[col + min(bz * kTZ + kTZ, dv.M)];
         for (int base = s; base < e; base += kBatch) {
           const int cnt = min(kBatch, e - base);
           for (int task = tid; task < cnt * 4; task += blockDim.x) {

@@ -58,10 +58,12 @@ class Config:
     xi: float
     M: int            # grid points on the periodic axis (h = L3/M)
     P: int            # Gaussian support points per dimension
-    s0: float         # k3 = 0 upsampling factor (paper's s0, relative to M~ = M_free + P)
-    sf: float         # upsampling factor s_l of the I modes
-    n_local: int      # n_l: number of upsampled |k3| modes
+    n_local: int      # n_l: number of upsampled |k3| modes (Eq. (I))
     Ntilde: int       # FFT extent of the free axes for the J modes (>= M_free + P)
+    S0: int           # padded extent of the k3 = 0 plane (0 -> from s0)
+    SI: int           # padded extent of the I planes (0 -> from sf)
+    s0: float         # paper's factors when the config fixes them (BASELINE config 1)
+    sf: float
     rc: float         # real-space cutoff
     seed: int
     oracle_targets: int   # seeded target subset for the exact oracle (all N if >= N)
@@ -69,10 +71,21 @@ class Config:
 
 
 # Parameters: BASELINE.json configs + the readings in DESIGN.md ("Parameter choices").
+# C1 keeps the config's own s0 = 2+sqrt(2), s_l = 2 on |k3| <= 2 and the paper's M~ extent.
 CONFIGS = {
-    "C1": Config("C1", 100, (1.0, 1.0, 1.0), 4.0, 16, 16, 2.0 + 2.0 ** 0.5, 2.0, 2, 40, 1.158, 1, 100, 0),
-    "C2": Config("C2", 2000, (1.0, 1.0, 1.0), 8.0, 32, 20, 3.0, 3.0, 3, 64, 0.594, 2, 2000, 0),
-    "C3": Config("C3", 20000, (1.0, 1.0, 2.0), 12.0, 96, 24, 2.0, 5.0, 7, 96, 0.401, 3, 1024, 128),
-    "C4": Config("C4", 200000, (1.0, 1.0, 1.0), 20.0, 128, 24, 2.0, 3.0, 4, 224, 0.247, 4, 512, 128),
-    "C5": Config("C5", 2000000, (2.0, 2.0, 2.0), 30.0, 256, 24, 2.0, 3.0, 5, 420, 0.1, 5, 256, 64),
+    "C1": Config("C1", 100, (1.0, 1.0, 1.0), 4.0, 16, 16, 2, 32, 0, 0, 2.0 + 2.0 ** 0.5, 2.0, 1.158, 1, 100, 0),
+    "C2": Config("C2", 2000, (1.0, 1.0, 1.0), 8.0, 32, 20, 3, 64, 416, 416, 0.0, 0.0, 0.594, 2, 2000, 0),
+    "C3": Config("C3", 20000, (1.0, 1.0, 2.0), 12.0, 96, 24, 7, 96, 576, 576, 0.0, 0.0, 0.401, 3, 1024, 128),
+    "C4": Config("C4", 200000, (1.0, 1.0, 1.0), 20.0, 128, 24, 4, 224, 1216, 1216, 0.0, 0.0, 0.247, 4, 512, 128),
+    "C5": Config("C5", 2000000, (2.0, 2.0, 2.0), 30.0, 256, 24, 16, 320, 2240, 2240, 0.0, 0.0, 0.1, 5, 256, 64),
 }
+
+
+def kspace_kwargs(c: Config) -> dict:
+    """Keyword arguments of paper_1611_09538_b200.kspace for a config (data only)."""
+    kw = dict(n_local=c.n_local, Ntilde=c.Ntilde)
+    if c.S0:
+        kw.update(S0=c.S0, SI=c.SI)
+    else:
+        kw.update(s0=c.s0, sf=c.sf)
+    return kw

@@ -15,7 +15,7 @@ import pytest
 
 import oracle
 from oracle import se1p_discrete as sd
-from se1p_synth import CONFIGS, make_system
+from se1p_synth import CONFIGS, kspace_kwargs, make_system
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -81,7 +81,7 @@ def test_full_potential_vs_exact_oracle(cfg):
     c = CONFIGS[cfg]
     x, q = make_system(c.N, c.L, c.seed)
     xd, qd = _dev(x, q)
-    phi = (se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, s0=c.s0, sf=c.sf, n_local=c.n_local, Ntilde=c.Ntilde)
+    phi = (se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kspace_kwargs(c))
            + se1p.real(xd, qd, c.L, c.xi, c.rc)).cpu().numpy()
     ref = oracle.phi_exact(x, q, c.L)
     assert oracle.rel_rms(phi, ref) <= 1e-9
@@ -166,3 +166,13 @@ def test_plan_info_defaults():
     assert info["Mt"] == 32 and info["S0"] == 110 and info["SI"] == 64
     assert info["LK"] >= 2 * 32 - 1 and info["n_kernel_planes"] == 3 and info["n_planes"] == 9
     assert abs(info["eta"] - 16 * 16.0 / 256 / (0.95 ** 2 * math.pi)) < 1e-15
+
+
+@pytest.mark.parametrize("case", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_reference_kernels_match_oracle(case):
+    """The simple v1 gridding/gather kernels (kept for A/B checks) against the same oracle."""
+    name, N, L, xi, M, P, n_l, S0, SI, SJ, seed = case
+    x, q = make_system(N, L, seed)
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, reference_kernels=True)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), name
