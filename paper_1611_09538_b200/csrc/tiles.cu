@@ -5,21 +5,24 @@
 // One CTA per tile X0..X0+15 x Y0..Y0+15 x Z0..Z0+TZ-1 (periodic in z):
 //   producer warps (kPW): stream the candidate particles of the tile (bins are xy columns of
 //     8 x 8 cells, z-sorted inside), keep those whose P^3 stencil meets the tile (order-
-//     preserving compaction) and hand lists of kStage particles to the consumers through a
-//     ring of kNL shared-memory lists (named barriers lfull/lempty);
-//   consumer warps (kCW = 16): each owns a 4 x 4 column block over all TZ nodes.  Per batch
-//     they (a) stage the NEXT batch's tile-restricted Fast Gaussian Gridding weights into the
-//     other half of a double buffer -- w = A E^t f1(t) with A, E per particle and axis from
-//     k_permute and f1 a table, no exps here -- and (b) run DMMA on the CURRENT
-//     batch for the staged particles meeting their block:
+//     preserving compaction) and append a record per kept particle to a shared-memory ring:
+//     stencil starts and, per axis, the Fast Gaussian Gridding factors A and E (from k_permute;
+//     P:813-817).  Every kStage records form a batch,
+//     published into one of kNBuf weight buffers;
+//   staging: a batch's tile-restricted weights w = A E^t f1(t) (one warp unit per particle,
+//     lanes = window nodes) are claimed unit by unit through an atomic counter by ANY warp that
+//     is free -- producers after publishing, consumers when they reach the batch -- so no warp
+//     waits for the slowest one;
+//   consumer warps (kCW = 16): each owns a 4 x 4 column block over all TZ nodes, waits until
+//     its next batch is fully staged, compacts the staged particles meeting its block and runs
 //       gridding  C[16 cols x 8 z]        += A[16 cols x 4 particles] B[4 particles x 8 z]
 //       gather    T[16 cols x 8 particles] = A[16 cols x 4 z] (H~, registers) B[4 z x 8 particles]
 //                 phi_p += sum_cols wx wy T
-//     skipping the 8-node z blocks no particle of the k-step reaches; one consumer barrier
-//     per batch.  Staging by all 16 warps interleaves with other warps' DMMA issue.
-// Gridding writes its tile once (no atomics); the gather writes one partial per (particle,
-// tile) into a fixed slot and k_gather_finish sums the slots in a fixed order: results are
-// bitwise reproducible.
+//     skipping the 8-node z blocks no particle of the k-step reaches.
+// Buffer reuse: consumers arrive on a named "empty" barrier after a batch; producers sync on it
+// before publishing into that buffer again.  Gridding writes its tile once (no atomics on
+// floating point data); the gather writes one partial per (particle, tile) into a fixed slot
+// and k_gather_finish sums the slots in a fixed order: results are bitwise reproducible.
 #include <cstdlib>
 
 #include "tiles.cuh"
@@ -30,10 +33,12 @@ constexpr int kCW = 16, kPW = 4;
 constexpr int kPT = kPW * 32;                 // producer threads
 constexpr int kCT = kCW * 32;                 // consumer threads
 constexpr int kThreads = kCT + kPT;           // 640
-constexpr int kNL = 4;                        // candidate-list ring
-constexpr int kBarProd = 1, kBarCons = 2;
-__host__ __device__ constexpr int bar_lfull(int b) { return 3 + b; }
-__host__ __device__ constexpr int bar_lempty(int b) { return 3 + kNL + b; }
+constexpr int kNBuf = 3;
+constexpr int kRing = 512;                    // candidate records (>= (kNBuf + 2) kStage + kPre kPT)
+constexpr int kPre = 2;                       // candidates per producer thread per round
+constexpr int kBarProd = 1;                   // producer-internal barrier id
+__host__ __device__ constexpr int bar_full(int b) { return 2 + b; }
+__host__ __device__ constexpr int bar_empty(int b) { return 2 + kNBuf + b; }
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -54,7 +59,7 @@ __device__ __forceinline__ int zcount(int a, int P, int M, int TZ) {
   return n;
 }
 
-// Does the stencil (jx0, jy0, lz0 mod M = a) meet tile (tx,ty,tz)?  Agrees with the slot
+// Does the stencil (jx0, jy0, lz0, a = lz0 mod M) meet tile (tx,ty,tz)?  Agrees with the slot
 // ranges of k_gather_finish: x tiles fdiv(jx0,16)..fdiv(jx0+P-1,16) (no wrap), z per zslot.
 template <int TZ>
 __device__ __forceinline__ bool tile_hit(const KDev& dv, const int4& s, int tx, int ty, int tz) {
@@ -64,32 +69,37 @@ __device__ __forceinline__ bool tile_hit(const KDev& dv, const int4& s, int tx, 
   return zslot(s.w, P, dv.M, TZ, tz) >= 0;
 }
 
+// A E^t f1[t] for 0 <= t < 64 from the binary powers of E (depth-3 product tree).
+__device__ __forceinline__ double fgg_w(double A, double E, int t, const double* f1) {
+  const double e2 = E * E, e4 = e2 * e2, e8 = e4 * e4, e16 = e8 * e8, e32 = e16 * e16;
+  const double p01 = ((t & 1) ? E : 1.0) * ((t & 2) ? e2 : 1.0);
+  const double p23 = ((t & 4) ? e4 : 1.0) * ((t & 8) ? e8 : 1.0);
+  const double p45 = ((t & 16) ? e16 : 1.0) * ((t & 32) ? e32 : 1.0);
+  return (A * f1[t]) * ((p01 * p23) * p45);
+}
+
 template <int TZ>
-struct WBuf {   // staged weights of one batch
+struct Buf {   // one staged batch
   static constexpr int SZ = TZ + 4;
   double wx[(kStage + 1) * kSX];
   double wy[(kStage + 1) * kSX];
   double wz[(kStage + 1) * SZ];
+  double acc[kStage * (kCW + 1)];
+  int64_t slot[kStage];   // gather: destination of each particle's partial in gpart
   int xr[kStage + 1], yr[kStage + 1], zm[kStage + 1];
-  int pad;
-};
-
-struct LBuf {   // a candidate list (sorted particle indices)
-  int idx[kStage];
-  int cnt;      // < 0: end of stream
-  int pad[3];
+  int cnt;       // particles (< 0: end of stream)
+  int rec;       // ring position of the first record
+  int claim;     // staging units claimed
+  int done;      // staging units finished
 };
 
 template <int TZ>
 struct Smem {
-  WBuf<TZ> wb[2];
-  double acc[3][kStage * (kCW + 1)];   // gather: partial per (particle, warp), ring of 3 batches
-  int sidx[3][kStage];
-  int scnt[3];
-  int pad0;
-  LBuf lb[kNL];
+  Buf<TZ> buf[kNBuf];
   double f1[64];
-  int pend[kPT + kStage];
+  double pf[kRing][6];      // A_x, E_x, A_y, E_y, A_z (x q when gridding), E_z
+  int4 ps[kRing];           // stencil starts
+  int pi[kRing];            // sorted particle index
   int pcnt[kPW];
   int wl[kCW][kStage + 8];
 };
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_tile_mma(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, const double* __restrict__ F6,
                const int* __restrict__ bin_start, double* __restrict__ grid, double* __restrict__ gpart, int ntz) {
   constexpr int NZB = TZ / 8;
-  constexpr int SZ = WBuf<TZ>::SZ;
+  constexpr int SZ = Buf<TZ>::SZ;
   constexpr int NK = TZ / 4;
   extern __shared__ __align__(16) char smem_raw[];
   Smem<TZ>& S = *reinterpret_cast<Smem<TZ>*>(smem_raw);
@@ -113,24 +123,113 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int X0 = tx * kTXY, Y0 = ty * kTXY, Z0 = tz * TZ;
   const int M = dv.M, P = dv.P;
 
-  if (w >= kCW) {
-    // ================================================================ producers: candidate lists
-    const int ptid = tid - kCT, pw = w - kCW;
-    unsigned long long t_wait = 0, t_all0 = clock64();
-    int nlist = 0, npend = 0;
-    auto emit = [&](int cnt) {   // hand S.pend[0..cnt) to the consumers (cnt < 0: end marker)
-      const int b = nlist % kNL;
-      if (nlist >= kNL) {
-        const unsigned long long t0 = clock64();
-        bar_sync(bar_lempty(b), kThreads);
-        if (*(volatile int*)&S.lb[b].cnt == -12345) S.pcnt[0] = 0;   // charge the lazy wait here
-        t_wait += clock64() - t0;
+  // ---- setup (all threads)
+  for (int t = tid; t < 64; t += kThreads) S.f1[t] = (t < P) ? exp(-dv.alpha * dv.h * dv.h * (double)t * (double)t) : 0.0;
+  for (int b = 0; b < kNBuf; ++b) {   // dummy all-zero row (index kStage) of every buffer
+    Buf<TZ>& B = S.buf[b];
+    for (int k = tid; k < kSX; k += kThreads) {
+      B.wx[kStage * kSX + k] = 0.0;
+      B.wy[kStage * kSX + k] = 0.0;
+    }
+    for (int k = tid; k < SZ; k += kThreads) B.wz[kStage * SZ + k] = 0.0;
+    if (tid == 0) B.xr[kStage] = B.yr[kStage] = B.zm[kStage] = 0;
+  }
+  __syncthreads();
+
+  // ---- staging unit: warp-wide, one particle p of buffer B
+  auto stage_unit = [&](Buf<TZ>& B, int p) {
+    const int rr = (B.rec + p) & (kRing - 1);
+    const int4 s = S.ps[rr];
+    {   // x (lanes 0-15) and y (lanes 16-31)
+      const int ax = lane >> 4, k = lane & 15;
+      const int t = (ax == 0 ? X0 - s.x : Y0 - s.y) + k;
+      const double v = (t >= 0 && t < P) ? fgg_w(S.pf[rr][2 * ax], S.pf[rr][2 * ax + 1], t, S.f1) : 0.0;
+      (ax == 0 ? B.wx : B.wy)[p * kSX + k] = v;
+    }
+    bool in = false;
+    if (lane < TZ) {   // z: lane = window node
+      const int g = Z0 + lane;
+      int t = g - s.w;
+      if (t < 0) t += M;
+      in = (g < M) && (t < P);
+      B.wz[p * SZ + lane] = in ? fgg_w(S.pf[rr][4], S.pf[rr][5], t, S.f1) : 0.0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) {
+      int mask = 0;
+#pragma unroll
+      for (int zb = 0; zb < NZB; ++zb) mask |= ((bal >> (8 * zb)) & 0xffu) ? (1 << zb) : 0;
+      B.zm[p] = mask;
+      B.xr[p] = (max(s.x, X0) - X0) | ((min(s.x + P, X0 + kTXY) - X0) << 8);
+      B.yr[p] = (max(s.y, Y0) - Y0) | ((min(s.y + P, Y0 + kTXY) - Y0) << 8);
+      if (GATHER) {
+        const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
+        const int sz = zslot(s.w, P, M, TZ, tz);
+        B.slot[p] = (int64_t)S.pi[rr] * dv.nslot + (sx * dv.nsxy + sy) * dv.nsz + sz;
       }
-      for (int k = ptid; k < cnt; k += kPT) S.lb[b].idx[k] = S.pend[k];
-      if (ptid == 0) S.lb[b].cnt = cnt;
-      bar_arrive(bar_lfull(b), kThreads);
-      ++nlist;
+    }
+    if (GATHER && lane < kCW + 1) B.acc[p * (kCW + 1) + lane] = 0.0;
+  };
+  // claim and process units of B until none is left (warp-uniform)
+  auto help_stage = [&](Buf<TZ>& B, int cnt) {
+    for (;;) {
+      int u = 0;
+      if (lane == 0) u = atomicAdd(&B.claim, 1);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= cnt) break;
+      stage_unit(B, u);
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&B.done, 1);
+    }
+  };
+
+  if (w >= kCW) {
+    // ================================================================ producers
+    const int ptid = tid - kCT, pw = w - kCW;
+    unsigned long long t_wait = 0, t_stage = 0, t_all0 = clock64();
+    int nbatch = 0, npend = 0, nwaited = 0, head = 0, tail = 0;
+
+    auto reduce = [&](int b) {   // sum the per-warp partials of a finished gather batch
+      if (!GATHER) return;
+      Buf<TZ>& B = S.buf[b];
+      const int cnt = B.cnt;
+      for (int p = ptid; p < cnt; p += kPT) {
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < kCW; ++v) s += B.acc[p * (kCW + 1) + v];
+        gpart[B.slot[p]] = s;
+      }
     };
+    auto wait_empty = [&](int batch) {   // buffer of `batch` is free again (consumers done)
+      const int b = batch % kNBuf;
+      const unsigned long long t0 = clock64();
+      bar_sync(bar_empty(b), kThreads);
+      if (*(volatile int*)&S.buf[b].cnt == -12345) S.pcnt[0] = 0;   // charge the lazy wait here
+      t_wait += clock64() - t0;
+      reduce(b);
+      ++nwaited;
+    };
+    auto publish = [&](int cnt) {   // records head .. head+cnt-1 form the next batch (cnt < 0: end)
+      const int b = nbatch % kNBuf;
+      if (nbatch >= kNBuf) wait_empty(nbatch - kNBuf);
+      Buf<TZ>& B = S.buf[b];
+      bar_sync(kBarProd, kPT);   // every producer finished reading the old batch (reduce)
+      if (ptid == 0) {
+        B.cnt = cnt;
+        B.rec = head & (kRing - 1);
+        B.claim = 0;
+        B.done = 0;
+      }
+      bar_arrive(bar_full(b), kThreads);
+      const unsigned long long ts = clock64();
+      if (cnt > 0) help_stage(B, cnt);
+      t_stage += clock64() - ts;
+      ++nbatch;
+      if (cnt > 0) head += cnt;
+    };
+
+    // candidate stream: bins are xy columns of 8x8 cells, z-sorted by cell inside
     const int bx0 = max(0, fdiv(X0 - P, kTX)), bx1 = min(dv.nbx - 1, fdiv(X0 + kTXY - 1, kTX));
     const int by0 = max(0, fdiv(Y0 - P, kTY)), by1 = min(dv.nby - 1, fdiv(Y0 + kTXY - 1, kTY));
     // cells whose stencil may reach the tile: nodes lz0..lz0+P-1 with lz0 = floor(z/h - P/2)+1,
@@ -143,60 +242,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (a <= c) { r0s[0] = a; r1s[0] = c; nr = 1; }
       else { r0s[0] = a; r1s[0] = M - 1; r0s[1] = 0; r1s[1] = c; nr = 2; }
     }
-    constexpr int kPre = 4;   // candidate records loaded ahead per thread
     for (int bx = bx0; bx <= bx1; ++bx)
       for (int by = by0; by <= by1; ++by) {
         const int base = (bx * dv.nby + by) * M;
         for (int r = 0; r < nr; ++r) {
           const int s = bin_start[base + r0s[r]], e = bin_start[base + r1s[r] + 1];
           for (int c00 = s; c00 < e; c00 += kPre * kPT) {
+            int4 sv[kPre];
             bool relv[kPre];
 #pragma unroll
             for (int u = 0; u < kPre; ++u) {
               const int idx = c00 + u * kPT + ptid;
-              relv[u] = (idx < e) && tile_hit<TZ>(dv, S4[idx], tx, ty, tz);
+              relv[u] = false;
+              if (idx < e) {
+                sv[u] = S4[idx];
+                relv[u] = tile_hit<TZ>(dv, sv[u], tx, ty, tz);
+              }
+            }
+            double fv[kPre][6];
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+              if (relv[u]) {
+                const int idx = c00 + u * kPT + ptid;
+                const double2* f2 = reinterpret_cast<const double2*>(F6 + 6 * (int64_t)idx);
+                const double2 a = f2[0], bb = f2[1], cc = f2[2];
+                fv[u][0] = a.x; fv[u][1] = a.y; fv[u][2] = bb.x; fv[u][3] = bb.y; fv[u][4] = cc.x; fv[u][5] = cc.y;
+                if (!GATHER) fv[u][4] *= P4[idx].w;
+              }
+            }
+            // ordered compaction of the kPre rounds: per-warp counts packed in one int
+            unsigned bals[kPre];
+            int packed = 0;
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+              bals[u] = __ballot_sync(0xffffffffu, relv[u]);
+              packed |= __popc(bals[u]) << (8 * u);
+            }
+            if (lane == 0) S.pcnt[pw] = packed;
+            bar_sync(kBarProd, kPT);
+            int off[kPre], total = 0;
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+              int o = total, t = 0;
+#pragma unroll
+              for (int v = 0; v < kPW; ++v) {
+                const int cv = (S.pcnt[v] >> (8 * u)) & 255;
+                if (v < pw) o += cv;
+                t += cv;
+              }
+              off[u] = o;
+              total += t;
             }
 #pragma unroll
             for (int u = 0; u < kPre; ++u) {
-              if (c00 + u * kPT >= e) break;
-              const int idx = c00 + u * kPT + ptid;
-              const bool rel = relv[u];
-              const unsigned bal = __ballot_sync(0xffffffffu, rel);
-              if (lane == 0) S.pcnt[pw] = __popc(bal);
-              bar_sync(kBarProd, kPT);
-              int off = npend, tot = 0;
+              if (relv[u]) {
+                const int rr = (tail + off[u] + __popc(bals[u] & ((1u << lane) - 1u))) & (kRing - 1);
+                S.pi[rr] = c00 + u * kPT + ptid;
+                S.ps[rr] = sv[u];
 #pragma unroll
-              for (int v = 0; v < kPW; ++v) {
-                const int cv = S.pcnt[v];
-                if (v < pw) off += cv;
-                tot += cv;
+                for (int k = 0; k < 6; ++k) S.pf[rr][k] = fv[u][k];
               }
-              if (rel) S.pend[off + __popc(bal & ((1u << lane) - 1u))] = idx;
-              bar_sync(kBarProd, kPT);
-              npend += tot;
-              while (npend >= kStage) {
-                emit(kStage);
-                const int rem = npend - kStage;
-                const int v = (ptid < rem) ? S.pend[kStage + ptid] : 0;
-                bar_sync(kBarProd, kPT);
-                if (ptid < rem) S.pend[ptid] = v;
-                bar_sync(kBarProd, kPT);
-                npend = rem;
-              }
+            }
+            bar_sync(kBarProd, kPT);
+            tail += total;
+            npend += total;
+            while (npend >= kStage) {
+              publish(kStage);
+              npend -= kStage;
             }
           }
         }
       }
-    if (npend > 0) emit(npend);
-    emit(-1);   // end marker
-    // match the consumers' lempty arrivals of the lists still outstanding
-    for (int j = max(0, nlist - kNL); j < nlist; ++j) bar_sync(bar_lempty(j % kNL), kThreads);
+    if (npend > 0) publish(npend);
+    const int nreal = nbatch;
+    publish(-1);   // end marker
+    for (int j = nwaited; j < nreal; ++j) wait_empty(j);
     if (dv.prof && lane == 0) {
       const unsigned long long tall = clock64() - t_all0;
-      atomicAdd(dv.prof + 0, tall);          // producer warp total
-      atomicAdd(dv.prof + 1, t_wait);        // waiting for free list slots
-      atomicAdd(dv.prof + 3, tall - t_wait); // candidate filtering
-      if (pw == 0) atomicAdd(dv.prof + 4, (unsigned long long)(nlist - 1));
+      atomicAdd(dv.prof + 0, tall);                     // producer warp total
+      atomicAdd(dv.prof + 1, t_wait);                   // waiting for free buffers
+      atomicAdd(dv.prof + 2, t_stage);                  // helping to stage
+      atomicAdd(dv.prof + 3, tall - t_wait - t_stage);  // candidate filtering
+      if (pw == 0) atomicAdd(dv.prof + 4, (unsigned long long)nreal);
     }
     return;
   }
@@ -205,18 +332,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int gid = lane >> 2, tig = lane & 3;
   const int bxw = w & 3, byw = w >> 2;
   const int colx = X0 + 4 * bxw + (gid & 3), coly = Y0 + 4 * byw + (gid >> 2);
-  for (int t = tid; t < P; t += kCT) S.f1[t] = exp(-dv.alpha * dv.h * dv.h * (double)t * (double)t);
-  for (int b = 0; b < 2; ++b) {   // dummy all-zero row (index kStage)
-    WBuf<TZ>& B = S.wb[b];
-    if (tid < kSX) {
-      B.wx[kStage * kSX + tid] = 0.0;
-      B.wy[kStage * kSX + tid] = 0.0;
-    }
-    if (tid < SZ) B.wz[kStage * SZ + tid] = 0.0;
-    if (tid == 0) B.xr[kStage] = B.yr[kStage] = B.zm[kStage] = 0;
-  }
-  bar_sync(kBarCons, kCT);
-
   double c[NZB][4];
   double hA[GATHER ? NK : 1][2];
 #pragma unroll
@@ -234,83 +349,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       hA[s][1] = a1;
     }
   }
-
-  // Stage list `L` (cnt particles) into weight buffer B; acc/sidx ring slot `slot`.
-  // Task = (particle, axis): 3 cnt tasks spread over all warps (lane-major).
-  auto stage = [&](const LBuf& L, int cnt, WBuf<TZ>& B, int slot) {
-    const int task = lane * kCW + w;
-    if (task < 3 * cnt) {
-      const int p = task / 3, ax = task - 3 * p;
-      const int i = L.idx[p];
-      const int4 s = S4[i];
-      double A = F6[6 * (int64_t)i + 2 * ax];
-      const double E = F6[6 * (int64_t)i + 2 * ax + 1];
-      if (!GATHER && ax == 2) A *= P4[i].w;
-      // A E^t for t = 4k + j as four independent chains in k
-      const double E2 = E * E, E4 = E2 * E2;
-      double Ej[4] = {A, A * E, A * E2, A * E2 * E};
-      if (ax < 2) {
-        double* row = (ax == 0 ? B.wx : B.wy) + p * kSX;
-        const int j0 = ax == 0 ? s.x : s.y;
-        const int T0 = ax == 0 ? X0 : Y0;
-#pragma unroll
-        for (int k = 0; k < kTXY; ++k) row[k] = 0.0;
-        for (int t0 = 0; t0 < P; t0 += 4) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int t = t0 + j, k = j0 + t - T0;
-            if (t < P && k >= 0 && k < kTXY) row[k] = Ej[j] * S.f1[t];
-            Ej[j] *= E4;
-          }
-        }
-        (ax == 0 ? B.xr : B.yr)[p] = (max(j0, T0) - T0) | ((min(j0 + P, T0 + kTXY) - T0) << 8);
-      } else {
-        double* row = B.wz + p * SZ;
-#pragma unroll
-        for (int k = 0; k < TZ; ++k) row[k] = 0.0;
-        int mask = 0;
-        for (int t0 = 0; t0 < P; t0 += 4) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int t = t0 + j;
-            int g = s.w + t;
-            if (g >= M) g -= M;
-            const int gl = g - Z0;
-            if (t < P && gl >= 0 && gl < TZ) {
-              row[gl] = Ej[j] * S.f1[t];
-              mask |= 1 << (gl >> 3);
-            }
-            Ej[j] *= E4;
-          }
-        }
-        B.zm[p] = mask;
-        S.sidx[slot][p] = i;
-      }
-    }
-    if (GATHER)
-      for (int k = tid; k < cnt * (kCW + 1); k += kCT) S.acc[slot][k] = 0.0;
-    if (tid == 0) S.scnt[slot] = cnt;
-  };
-
-  // Sum the per-warp partials of a finished gather batch into the fixed slots.
-  auto reduce = [&](int slot) {
-    const int cnt = S.scnt[slot];
-    for (int p = tid; p < cnt; p += kCT) {
-      double s = 0.0;
-#pragma unroll
-      for (int v = 0; v < kCW; ++v) s += S.acc[slot][p * (kCW + 1) + v];
-      const int i = S.sidx[slot][p];
-      const int4 st = S4[i];
-      const int sx = tx - fdiv(st.x, kTXY), sy = ty - fdiv(st.y, kTXY);
-      const int sz = zslot(st.w, P, M, TZ, tz);
-      gpart[(int64_t)i * dv.nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = s;
-    }
-  };
-
-  // Contract the staged batch B (cnt particles) into this warp's accumulators.
   int* wl = S.wl[w];
-  unsigned long long c_dmma = 0;
-  auto compute = [&](const WBuf<TZ>& B, int cnt, int slot) {
+  unsigned long long c_wait = 0, c_stage = 0, c_all0 = clock64(), c_dmma = 0;
+  for (int batch = 0;; ++batch) {
+    const int b = batch % kNBuf;
+    Buf<TZ>& B = S.buf[b];
+    unsigned long long t0 = clock64();
+    bar_sync(bar_full(b), kThreads);
+    const int cnt = *(volatile int*)&B.cnt;
+    unsigned long long t1 = clock64();
+    c_wait += t1 - t0;
+    if (cnt < 0) break;
+    help_stage(B, cnt);
+    while (*(volatile int*)&B.done < cnt) __nanosleep(32);
+    __threadfence_block();
+    t0 = clock64();
+    c_stage += t0 - t1;
+    // staged particles meeting this warp's 4x4 column block (order preserving)
     int n = 0;
     for (int p0 = 0; p0 < cnt; p0 += 32) {
       const int p = p0 + lane;
@@ -327,8 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int npad = (n + KS - 1) / KS * KS;
     if (lane < npad - n) wl[n + lane] = kStage;
     __syncwarp();
-    if (dv.dbg & 1) return;
-    if (!GATHER) {
+    if (dv.dbg & 1) {
+      // experiment: no consumer compute
+    } else if (!GATHER) {
       for (int k = 0; k < npad; k += 4) {
         const int p = wl[k + tig];
         const double wxv = B.wx[p * kSX + 4 * bxw + (gid & 3)];
@@ -351,65 +407,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         zm |= __shfl_xor_sync(0xffffffffu, zm, 8);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 16);
         c_dmma += 2 * __popc(zm);
-        double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
+        double t0v[4] = {0.0, 0.0, 0.0, 0.0}, t1v[4] = {0.0, 0.0, 0.0, 0.0};
         const double* wzr = B.wz + pB * SZ + tig;
 #pragma unroll
         for (int s = 0; s < NK; s += 2) {      // two accumulators halve the DMMA dependency chain
           if ((zm >> (s >> 1)) & 1) {
-            dmma_16x8x4(t0, hA[s][0], hA[s][1], wzr[4 * s]);
-            dmma_16x8x4(t1, hA[s + 1][0], hA[s + 1][1], wzr[4 * s + 4]);
+            dmma_16x8x4(t0v, hA[s][0], hA[s][1], wzr[4 * s]);
+            dmma_16x8x4(t1v, hA[s + 1][0], hA[s + 1][1], wzr[4 * s + 4]);
           }
         }
         const int pa = wl[k + 2 * tig], pb = wl[k + 2 * tig + 1];
         const int ix = 4 * bxw + (gid & 3), iy = 4 * byw + (gid >> 2);
-        double va = B.wx[pa * kSX + ix] * fma(B.wy[pa * kSX + iy], t0[0] + t1[0], B.wy[pa * kSX + iy + 2] * (t0[2] + t1[2]));
-        double vb = B.wx[pb * kSX + ix] * fma(B.wy[pb * kSX + iy], t0[1] + t1[1], B.wy[pb * kSX + iy + 2] * (t0[3] + t1[3]));
+        double va = B.wx[pa * kSX + ix] * fma(B.wy[pa * kSX + iy], t0v[0] + t1v[0], B.wy[pa * kSX + iy + 2] * (t0v[2] + t1v[2]));
+        double vb = B.wx[pb * kSX + ix] * fma(B.wy[pb * kSX + iy], t0v[1] + t1v[1], B.wy[pb * kSX + iy + 2] * (t0v[3] + t1v[3]));
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) {
           va += __shfl_xor_sync(0xffffffffu, va, off);
           vb += __shfl_xor_sync(0xffffffffu, vb, off);
         }
         if (gid == 0) {
-          if (pa < kStage) S.acc[slot][pa * (kCW + 1) + w] = va;
-          if (pb < kStage) S.acc[slot][pb * (kCW + 1) + w] = vb;
+          if (pa < kStage) B.acc[pa * (kCW + 1) + w] = va;
+          if (pb < kStage) B.acc[pb * (kCW + 1) + w] = vb;
         }
       }
     }
-  };
-
-  unsigned long long c_wait = 0, c_all0 = clock64(), c_stage = 0;
-  auto take_list = [&](int k) -> int {   // wait for list k; returns its count
-    const unsigned long long t0 = clock64();
-    bar_sync(bar_lfull(k % kNL), kThreads);
-    const int cnt = *(volatile int*)&S.lb[k % kNL].cnt;
-    c_wait += clock64() - t0;
-    return cnt;
-  };
-  int cur = take_list(0);
-  if (cur >= 0) stage(S.lb[0], cur, S.wb[0], 0);
-  bar_arrive(bar_lempty(0), kThreads);
-  bar_sync(kBarCons, kCT);
-  int k = 0;
-  while (cur >= 0) {
-    if (GATHER && k >= 1) reduce((k - 1) % 3);
-    const int nxt = take_list(k + 1);
-    const unsigned long long ts = clock64();
-    if (nxt >= 0) stage(S.lb[(k + 1) % kNL], nxt, S.wb[(k + 1) & 1], (k + 1) % 3);
-    c_stage += clock64() - ts;
-    bar_arrive(bar_lempty((k + 1) % kNL), kThreads);
-    compute(S.wb[k & 1], cur, k % 3);
-    bar_sync(kBarCons, kCT);
-    cur = nxt;
-    ++k;
+    bar_arrive(bar_empty(b), kThreads);
   }
-  if (GATHER && k >= 1) reduce((k - 1) % 3);
   if (dv.prof && lane == 0) {
     const unsigned long long tall = clock64() - c_all0;
-    atomicAdd(dv.prof + 8, tall);       // consumer warp total
-    atomicAdd(dv.prof + 9, c_wait);     // waiting for candidate lists
-    atomicAdd(dv.prof + 10, c_stage);   // staging
-    atomicAdd(dv.prof + 11, tall - c_wait - c_stage);   // DMMA k-steps + barriers
-    atomicAdd(dv.prof + 12, c_dmma);    // m16n8k4 issued
+    atomicAdd(dv.prof + 8, tall);                      // consumer warp total
+    atomicAdd(dv.prof + 9, c_wait);                    // waiting for published batches
+    atomicAdd(dv.prof + 10, c_stage);                  // staging + waiting for staging
+    atomicAdd(dv.prof + 11, tall - c_wait - c_stage);  // lists + DMMA k-steps
+    atomicAdd(dv.prof + 12, c_dmma);                   // m16n8k4 issued
   }
   if (!GATHER) {
 #pragma unroll

@@ -18,7 +18,7 @@ c = se1p.phase_counters()
 for tag in ("spread", "gather"):
     pt, ct, nb = c[f"{tag}.prod_total"], c[f"{tag}.cons_total"], max(c[f"{tag}.batches"], 1)
     print(f"{tag}: batches {nb:.0f}  mma {c[f'{tag}.mma_issued']:.3e}")
-    print(f"  producers: wait_list_slot {c[f'{tag}.prod_wait_empty']/pt:.2f} candidates {c[f'{tag}.prod_candidates']/pt:.2f}"
-          f"  (cycles/batch/warp {pt / 4 / nb:.0f})")
-    print(f"  consumers: wait_list {c[f'{tag}.cons_wait_full']/ct:.2f} stage {c[f'{tag}.cons_list']/ct:.2f} "
-          f"compute+barrier {c[f'{tag}.cons_kstep']/ct:.2f}  (cycles/batch/warp {ct / 16 / nb:.0f})")
+    print(f"  producers: wait_empty {c[f'{tag}.prod_wait_empty']/pt:.2f} stage {c[f'{tag}.prod_stage']/pt:.2f} "
+          f"candidates {c[f'{tag}.prod_candidates']/pt:.2f}  (cycles/batch/warp {pt / 4 / nb:.0f})")
+    print(f"  consumers: wait_full {c[f'{tag}.cons_wait_full']/ct:.2f} list {c[f'{tag}.cons_list']/ct:.2f} "
+          f"kstep {c[f'{tag}.cons_kstep']/ct:.2f}  (cycles/batch/warp {ct / 16 / nb:.0f})")
