@@ -247,9 +247,13 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   }
   if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, true, st);
   StageTimer tm(o && o->reserved[0] == 1, st);
+  SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   const int stop = o ? o->reserved[1] : 0;
   const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
-  if (!v1) grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+  if (!v1) {
+    grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+    grow(w.wts, w.cap_wts, N * 3 * dv.P);
+  }
   w.prof_on = o && o->reserved[3] == 1;       // phase counters of the tile kernels
   if (w.prof_on) {
     if (!w.prof) SE1P_CUDA_TRY(cudaMalloc(&w.prof, 32 * sizeof(unsigned long long)));
@@ -276,7 +280,12 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   tm.mark();
   if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   tm.finish();
-  if (!o || o->sync || host_io) SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  if (!o || o->sync || host_io) {
+    SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+    int kerr = 0;
+    SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+  }
   SE1P_CUDA_TRY(cudaGetLastError());
 }
 

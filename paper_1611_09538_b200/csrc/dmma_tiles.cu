@@ -1,28 +1,30 @@
-// tiles.cu -- gridding (Alg. 1 step 2, Eq. (spread_1p)) and gather (Alg. 1 step 6,
-// Eq. (se1p_complete_discretized)) as output-stationary tile contractions on the
-// FP64 tensor pipe (mma.sync m16n8k4 f64 -> SASS DMMA).  See tiles.cuh for the decomposition.
+// dmma_tiles.cu -- gridding (Alg. 1 step 2, Eq. (spread_1p)) and gather (Alg. 1
+// step 6, Eq. (se1p_complete_discretized)) as output-stationary tile contractions on
+// the FP64 tensor pipe (mma.sync m16n8k4 f64 -> SASS DMMA).  See tiles.cuh.
+//
+// Weights: k_stencil_weights evaluates every particle's 3 x P one-dimensional window weights
+// e^{-alpha d^2} once per call (W[i][axis][t], t = stencil offset).  A tile then only COPIES
+// the parts of those rows that fall inside it.
 //
 // One CTA per tile X0..X0+15 x Y0..Y0+15 x Z0..Z0+TZ-1 (periodic in z):
 //   producer warps (kPW): stream the candidate particles of the tile (bins are xy columns of
 //     8 x 8 cells, z-sorted inside), keep those whose P^3 stencil meets the tile (order-
-//     preserving compaction) and append a record per kept particle to a shared-memory ring:
-//     stencil starts and, per axis, the Fast Gaussian Gridding factors A and E (from k_permute;
-//     P:813-817).  Every kStage records form a batch,
-//     published into one of kNBuf weight buffers;
-//   staging: a batch's tile-restricted weights w = A E^t f1(t) (one warp unit per particle,
-//     lanes = window nodes) are claimed unit by unit through an atomic counter by ANY warp that
-//     is free -- producers after publishing, consumers when they reach the batch -- so no warp
-//     waits for the slowest one;
-//   consumer warps (kCW = 16): each owns a 4 x 4 column block over all TZ nodes, waits until
-//     its next batch is fully staged, compacts the staged particles meeting its block and runs
+//     preserving compaction) into a ring of records; every kStage records form a batch,
+//     published into one of kNBuf shared-memory weight buffers;
+//   staging: per particle one warp unit copies the tile windows of its rows with cp.async
+//     (zero-fill outside the stencil); units are claimed through an atomic counter by any free
+//     warp (producers after publishing, consumers when they reach the batch);
+//   consumer warps (kCW = 16): each owns a 4 x 4 column block over all TZ nodes and runs
 //       gridding  C[16 cols x 8 z]        += A[16 cols x 4 particles] B[4 particles x 8 z]
+//                 A = q wx wy, B = wz
 //       gather    T[16 cols x 8 particles] = A[16 cols x 4 z] (H~, registers) B[4 z x 8 particles]
 //                 phi_p += sum_cols wx wy T
-//     skipping the 8-node z blocks no particle of the k-step reaches.
-// Buffer reuse: consumers arrive on a named "empty" barrier after a batch; producers sync on it
-// before publishing into that buffer again.  Gridding writes its tile once (no atomics on
-// floating point data); the gather writes one partial per (particle, tile) into a fixed slot
-// and k_gather_finish sums the slots in a fixed order: results are bitwise reproducible.
+//     on the staged particles meeting its block, skipping 8-node z blocks no particle of the
+//     k-step reaches.
+// Consumers arrive on a named "empty" barrier after a batch; producers sync on it before
+// reusing that buffer.  Gridding writes its tile once (no floating-point atomics); the gather
+// writes one partial per (particle, tile) into a fixed slot and k_gather_finish sums the slots
+// in a fixed order: results are bitwise reproducible.
 #include <cstdlib>
 
 #include "tiles.cuh"
@@ -34,14 +36,22 @@ constexpr int kPT = kPW * 32;                 // producer threads
 constexpr int kCT = kCW * 32;                 // consumer threads
 constexpr int kThreads = kCT + kPT;           // 640
 constexpr int kNBuf = 3;
-constexpr int kRing = 512;                    // candidate records (>= (kNBuf + 2) kStage + kPre kPT)
-constexpr int kPre = 2;                       // candidates per producer thread per round
+constexpr int kRing = 1024;                   // candidate records (>= (kNBuf + 2) kStage + kPre kPT)
+constexpr int kPre = 4;                       // candidates per producer thread per round
+constexpr int kWin = 4;                       // z cells per candidate window
 constexpr int kBarProd = 1;                   // producer-internal barrier id
 __host__ __device__ constexpr int bar_full(int b) { return 2 + b; }
 __host__ __device__ constexpr int bar_empty(int b) { return 2 + kNBuf + b; }
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 8-byte global -> shared async copy; src_bytes = 0 writes zeros (cp.async zero-fill)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // z tiles (extent TZ, the last one ragged) hit by the stencil nodes a, a+1, ..., a+P-1 (mod M),
 // a in [0,M): first the tiles of [a, min(a+P,M)), then those of the wrapped part [0, a+P-M)
@@ -69,15 +79,6 @@ __device__ __forceinline__ bool tile_hit(const KDev& dv, const int4& s, int tx, 
   return zslot(s.w, P, dv.M, TZ, tz) >= 0;
 }
 
-// A E^t f1[t] for 0 <= t < 64 from the binary powers of E (depth-3 product tree).
-__device__ __forceinline__ double fgg_w(double A, double E, int t, const double* f1) {
-  const double e2 = E * E, e4 = e2 * e2, e8 = e4 * e4, e16 = e8 * e8, e32 = e16 * e16;
-  const double p01 = ((t & 1) ? E : 1.0) * ((t & 2) ? e2 : 1.0);
-  const double p23 = ((t & 4) ? e4 : 1.0) * ((t & 8) ? e8 : 1.0);
-  const double p45 = ((t & 16) ? e16 : 1.0) * ((t & 32) ? e32 : 1.0);
-  return (A * f1[t]) * ((p01 * p23) * p45);
-}
-
 template <int TZ>
 struct Buf {   // one staged batch
   static constexpr int SZ = TZ + 4;
@@ -85,6 +86,7 @@ struct Buf {   // one staged batch
   double wy[(kStage + 1) * kSX];
   double wz[(kStage + 1) * SZ];
   double acc[kStage * (kCW + 1)];
+  double q[kStage + 1];
   int64_t slot[kStage];   // gather: destination of each particle's partial in gpart
   int xr[kStage + 1], yr[kStage + 1], zm[kStage + 1];
   int cnt;       // particles (< 0: end of stream)
@@ -96,11 +98,11 @@ struct Buf {   // one staged batch
 template <int TZ>
 struct Smem {
   Buf<TZ> buf[kNBuf];
-  double f1[64];
-  double pf[kRing][6];      // A_x, E_x, A_y, E_y, A_z (x q when gridding), E_z
+  double pq[kRing];         // charge
   int4 ps[kRing];           // stencil starts
   int pi[kRing];            // sorted particle index
   int pcnt[kPW];
+  int cs[64], csz[64], cpre[65];   // candidate window: per-column start, size, exclusive prefix
   int wl[kCW][kStage + 8];
 };
 
@@ -109,7 +111,7 @@ __host__ __device__ constexpr size_t tile_smem_bytes() { return sizeof(Smem<TZ>)
 
 template <int TZ, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_tile_mma(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, const double* __restrict__ F6,
+    k_tile_mma(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, const double* __restrict__ W,
                const int* __restrict__ bin_start, double* __restrict__ grid, double* __restrict__ gpart, int ntz) {
   constexpr int NZB = TZ / 8;
   constexpr int SZ = Buf<TZ>::SZ;
@@ -123,8 +125,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int X0 = tx * kTXY, Y0 = ty * kTXY, Z0 = tz * TZ;
   const int M = dv.M, P = dv.P;
 
-  // ---- setup (all threads)
-  for (int t = tid; t < 64; t += kThreads) S.f1[t] = (t < P) ? exp(-dv.alpha * dv.h * dv.h * (double)t * (double)t) : 0.0;
   for (int b = 0; b < kNBuf; ++b) {   // dummy all-zero row (index kStage) of every buffer
     Buf<TZ>& B = S.buf[b];
     for (int k = tid; k < kSX; k += kThreads) {
@@ -132,19 +132,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       B.wy[kStage * kSX + k] = 0.0;
     }
     for (int k = tid; k < SZ; k += kThreads) B.wz[kStage * SZ + k] = 0.0;
-    if (tid == 0) B.xr[kStage] = B.yr[kStage] = B.zm[kStage] = 0;
+    if (tid == 0) {
+      B.xr[kStage] = B.yr[kStage] = B.zm[kStage] = 0;
+      B.q[kStage] = 0.0;
+    }
   }
   __syncthreads();
 
-  // ---- staging unit: warp-wide, one particle p of buffer B
+  // ---- staging unit: warp-wide, one particle p of buffer B (async copies, no wait here)
   auto stage_unit = [&](Buf<TZ>& B, int p) {
     const int rr = (B.rec + p) & (kRing - 1);
     const int4 s = S.ps[rr];
+    int i = S.pi[rr];
+    if ((unsigned)i >= (unsigned)dv.N || (unsigned)p >= (unsigned)kStage) {   // never expected
+      atomicOr(dv.err, 1 | (p >= kStage ? 2 : 0));
+      i = 0;
+    }
+    const double* row = W + (int64_t)i * 3 * P;
     {   // x (lanes 0-15) and y (lanes 16-31)
       const int ax = lane >> 4, k = lane & 15;
       const int t = (ax == 0 ? X0 - s.x : Y0 - s.y) + k;
-      const double v = (t >= 0 && t < P) ? fgg_w(S.pf[rr][2 * ax], S.pf[rr][2 * ax + 1], t, S.f1) : 0.0;
-      (ax == 0 ? B.wx : B.wy)[p * kSX + k] = v;
+      const bool v = t >= 0 && t < P;
+      cp_async8((ax == 0 ? B.wx : B.wy) + p * kSX + k, row + ax * P + (v ? t : 0), v ? 8 : 0);
     }
     bool in = false;
     if (lane < TZ) {   // z: lane = window node
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int t = g - s.w;
       if (t < 0) t += M;
       in = (g < M) && (t < P);
-      B.wz[p * SZ + lane] = in ? fgg_w(S.pf[rr][4], S.pf[rr][5], t, S.f1) : 0.0;
+      cp_async8(B.wz + p * SZ + lane, row + 2 * P + (in ? t : 0), in ? 8 : 0);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, in);
     if (lane == 0) {
@@ -165,22 +174,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (GATHER) {
         const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
         const int sz = zslot(s.w, P, M, TZ, tz);
-        B.slot[p] = (int64_t)S.pi[rr] * dv.nslot + (sx * dv.nsxy + sy) * dv.nsz + sz;
+        B.slot[p] = (int64_t)i * dv.nslot + (sx * dv.nsxy + sy) * dv.nsz + sz;
+      } else {
+        B.q[p] = S.pq[rr];
       }
     }
     if (GATHER && lane < kCW + 1) B.acc[p * (kCW + 1) + lane] = 0.0;
   };
-  // claim and process units of B until none is left (warp-uniform)
+  // claim and process units of B until none is left (warp-uniform), then publish completion
   auto help_stage = [&](Buf<TZ>& B, int cnt) {
+    int mine = 0;
     for (;;) {
       int u = 0;
       if (lane == 0) u = atomicAdd(&B.claim, 1);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= cnt) break;
       stage_unit(B, u);
+      ++mine;
+    }
+    if (mine) {
+      cp_async_wait_all();
       __threadfence_block();
       __syncwarp();
-      if (lane == 0) atomicAdd(&B.done, 1);
+      if (lane == 0) atomicAdd(&B.done, mine);
     }
   };
 
@@ -198,7 +214,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         double s = 0.0;
 #pragma unroll
         for (int v = 0; v < kCW; ++v) s += B.acc[p * (kCW + 1) + v];
-        gpart[B.slot[p]] = s;
+        const int64_t sl = B.slot[p];
+        if (sl < 0 || sl >= dv.N * dv.nslot) atomicOr(dv.err, 4);   // never expected
+        else gpart[sl] = s;
       }
     };
     auto wait_empty = [&](int batch) {   // buffer of `batch` is free again (consumers done)
@@ -223,96 +241,113 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       bar_arrive(bar_full(b), kThreads);
       const unsigned long long ts = clock64();
-      if (cnt > 0) help_stage(B, cnt);
+      if (cnt > 0 && !(dv.dbg & 2)) help_stage(B, cnt);
       t_stage += clock64() - ts;
       ++nbatch;
       if (cnt > 0) head += cnt;
     };
 
-    // candidate stream: bins are xy columns of 8x8 cells, z-sorted by cell inside
+    // candidate stream, interleaved over the xy bin columns (8x8 cells, z-sorted by cell inside):
+    // z windows of kWin cells, and inside a window the columns' ranges concatenated, so every
+    // batch spreads over the whole tile (balanced consumer warps) and stays z-coherent.
     const int bx0 = max(0, fdiv(X0 - P, kTX)), bx1 = min(dv.nbx - 1, fdiv(X0 + kTXY - 1, kTX));
     const int by0 = max(0, fdiv(Y0 - P, kTY)), by1 = min(dv.nby - 1, fdiv(Y0 + kTXY - 1, kTY));
+    const int nbyc = by1 - by0 + 1, ncol = max(0, (bx1 - bx0 + 1) * nbyc);
     // cells whose stencil may reach the tile: nodes lz0..lz0+P-1 with lz0 = floor(z/h - P/2)+1,
     // i.e. cz - (P+1)/2 <= lz0 <= cz - P/2 + 1 (exact test: tile_hit)
-    const int cz0 = Z0 - P / 2 - 1, cz1 = Z0 + TZ + (P + 1) / 2;
-    int r0s[2], r1s[2], nr;
-    if (cz1 - cz0 + 1 >= M) { r0s[0] = 0; r1s[0] = M - 1; nr = 1; }
-    else {
-      const int a = pmod(cz0, M), c = pmod(cz1, M);
-      if (a <= c) { r0s[0] = a; r1s[0] = c; nr = 1; }
-      else { r0s[0] = a; r1s[0] = M - 1; r0s[1] = 0; r1s[1] = c; nr = 2; }
-    }
-    for (int bx = bx0; bx <= bx1; ++bx)
-      for (int by = by0; by <= by1; ++by) {
-        const int base = (bx * dv.nby + by) * M;
-        for (int r = 0; r < nr; ++r) {
-          const int s = bin_start[base + r0s[r]], e = bin_start[base + r1s[r] + 1];
-          for (int c00 = s; c00 < e; c00 += kPre * kPT) {
-            int4 sv[kPre];
-            bool relv[kPre];
+    int czs = Z0 - P / 2 - 1, span = TZ + P + 2;
+    if (span >= M) { czs = 0; span = M; }
+    for (int w0 = 0; w0 < span;) {
+      const int a = pmod(czs + w0, M);
+      const int len = min(min(kWin, span - w0), M - a);   // a window never crosses the periodic seam
+      w0 += len;
+      if (ptid < ncol) {
+        const int c = ptid, bx = bx0 + c / nbyc, by = by0 + c - (c / nbyc) * nbyc;
+        const int base = (bx * dv.nby + by) * M + a;
+        const int s = bin_start[base];
+        S.cs[c] = s;
+        S.csz[c] = bin_start[base + len] - s;
+      }
+      bar_sync(kBarProd, kPT);
+      if (pw == 0) {   // exclusive prefix of the column sizes (<= 64 columns, 2 per lane)
+        const int v0 = (2 * lane < ncol) ? S.csz[2 * lane] : 0, v1 = (2 * lane + 1 < ncol) ? S.csz[2 * lane + 1] : 0;
+        int x = v0 + v1;
 #pragma unroll
-            for (int u = 0; u < kPre; ++u) {
-              const int idx = c00 + u * kPT + ptid;
-              relv[u] = false;
-              if (idx < e) {
-                sv[u] = S4[idx];
-                relv[u] = tile_hit<TZ>(dv, sv[u], tx, ty, tz);
-              }
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const int ex = x - v0 - v1;
+        S.cpre[2 * lane] = ex;
+        S.cpre[2 * lane + 1] = ex + v0;
+        if (lane == 31) S.cpre[64] = x;
+      }
+      bar_sync(kBarProd, kPT);
+      const int total_w = S.cpre[64];
+      for (int c00 = 0; c00 < total_w; c00 += kPre * kPT) {
+        int4 sv[kPre];
+        bool relv[kPre];
+        double qv[kPre];
+        int idxv[kPre];
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          const int vi = c00 + u * kPT + ptid;
+          relv[u] = false;
+          idxv[u] = 0;
+          if (vi < total_w) {
+            int lo = 0, hi = ncol - 1;   // last column with cpre[c] <= vi
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (S.cpre[mid] <= vi) lo = mid; else hi = mid - 1;
             }
-            double fv[kPre][6];
-#pragma unroll
-            for (int u = 0; u < kPre; ++u) {
-              if (relv[u]) {
-                const int idx = c00 + u * kPT + ptid;
-                const double2* f2 = reinterpret_cast<const double2*>(F6 + 6 * (int64_t)idx);
-                const double2 a = f2[0], bb = f2[1], cc = f2[2];
-                fv[u][0] = a.x; fv[u][1] = a.y; fv[u][2] = bb.x; fv[u][3] = bb.y; fv[u][4] = cc.x; fv[u][5] = cc.y;
-                if (!GATHER) fv[u][4] *= P4[idx].w;
-              }
-            }
-            // ordered compaction of the kPre rounds: per-warp counts packed in one int
-            unsigned bals[kPre];
-            int packed = 0;
-#pragma unroll
-            for (int u = 0; u < kPre; ++u) {
-              bals[u] = __ballot_sync(0xffffffffu, relv[u]);
-              packed |= __popc(bals[u]) << (8 * u);
-            }
-            if (lane == 0) S.pcnt[pw] = packed;
-            bar_sync(kBarProd, kPT);
-            int off[kPre], total = 0;
-#pragma unroll
-            for (int u = 0; u < kPre; ++u) {
-              int o = total, t = 0;
-#pragma unroll
-              for (int v = 0; v < kPW; ++v) {
-                const int cv = (S.pcnt[v] >> (8 * u)) & 255;
-                if (v < pw) o += cv;
-                t += cv;
-              }
-              off[u] = o;
-              total += t;
-            }
-#pragma unroll
-            for (int u = 0; u < kPre; ++u) {
-              if (relv[u]) {
-                const int rr = (tail + off[u] + __popc(bals[u] & ((1u << lane) - 1u))) & (kRing - 1);
-                S.pi[rr] = c00 + u * kPT + ptid;
-                S.ps[rr] = sv[u];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) S.pf[rr][k] = fv[u][k];
-              }
-            }
-            bar_sync(kBarProd, kPT);
-            tail += total;
-            npend += total;
-            while (npend >= kStage) {
-              publish(kStage);
-              npend -= kStage;
-            }
+            const int idx = S.cs[lo] + (vi - S.cpre[lo]);
+            idxv[u] = idx;
+            sv[u] = S4[idx];
+            if (!GATHER) qv[u] = P4[idx].w;
+            relv[u] = tile_hit<TZ>(dv, sv[u], tx, ty, tz);
           }
         }
+        // ordered compaction of the kPre rounds: per-warp counts packed in one int
+        unsigned bals[kPre];
+        int packed = 0;
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          bals[u] = __ballot_sync(0xffffffffu, relv[u]);
+          packed |= __popc(bals[u]) << (8 * u);
+        }
+        if (lane == 0) S.pcnt[pw] = packed;
+        bar_sync(kBarProd, kPT);
+        int off[kPre], total = 0;
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          int o = total, t = 0;
+#pragma unroll
+          for (int v = 0; v < kPW; ++v) {
+            const int cv = (S.pcnt[v] >> (8 * u)) & 255;
+            if (v < pw) o += cv;
+            t += cv;
+          }
+          off[u] = o;
+          total += t;
+        }
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          if (relv[u]) {
+            const int rr = (tail + off[u] + __popc(bals[u] & ((1u << lane) - 1u))) & (kRing - 1);
+            S.pi[rr] = idxv[u];
+            S.ps[rr] = sv[u];
+            if (!GATHER) S.pq[rr] = qv[u];
+          }
+        }
+        bar_sync(kBarProd, kPT);
+        tail += total;
+        npend += total;
+        while (npend >= kStage) {
+          publish(kStage);
+          npend -= kStage;
+        }
       }
+    }
     if (npend > 0) publish(npend);
     const int nreal = nbatch;
     publish(-1);   // end marker
@@ -387,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (!GATHER) {
       for (int k = 0; k < npad; k += 4) {
         const int p = wl[k + tig];
-        const double wxv = B.wx[p * kSX + 4 * bxw + (gid & 3)];
+        const double wxv = B.wx[p * kSX + 4 * bxw + (gid & 3)] * B.q[p];
         const double a0 = wxv * B.wy[p * kSX + 4 * byw + (gid >> 2)];
         const double a1 = wxv * B.wy[p * kSX + 4 * byw + (gid >> 2) + 2];
         int zm = B.zm[p];
@@ -471,6 +506,24 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   phi[perm[p]] = s;
 }
 
+// One-dimensional window weights of every sorted particle: W[i][axis][t] = e^{-alpha d_t^2},
+// d_t the signed distance to stencil node t (Eq. (spread_1p) factorised per axis, reading R-3).
+__global__ void k_stencil_weights(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, int64_t N,
+                                  double* __restrict__ W) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int P = dv.P;
+  if (id >= N * 3 * P) return;
+  const int64_t i = id / (3 * P);
+  const int r = (int)(id - i * 3 * P), ax = r / P, t = r - ax * P;
+  const double4 pp = P4[i];
+  const int4 s = S4[i];
+  double d;
+  if (ax == 0) d = ((double)(s.x + t) - 0.5 * P) * dv.h - pp.x;
+  else if (ax == 1) d = ((double)(s.y + t) - 0.5 * P) * dv.h - pp.y;
+  else d = (double)(s.z + t) * dv.h - pp.z;
+  W[id] = exp(-dv.alpha * d * d);
+}
+
 int tile_tz(int M) { return M >= 64 ? 32 : 16; }
 
 // Slots of the gather partials: x and y tiles per stencil, then z tiles (<= ceil(P/TZ)+2 once
@@ -488,6 +541,13 @@ int64_t gather_slots(const KDev& dv) {
   return d.nslot;
 }
 
+void k_weights(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
+  const int64_t n = N * 3 * pl.dv.P;
+  k_stencil_weights<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N,
+                                                                 w.wts);
+  SE1P_LAUNCH_CHECK();
+}
+
 template <int TZ, bool GATHER>
 static void launch_tile(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st) {
   KDev dv = pl.dv;
@@ -496,6 +556,8 @@ static void launch_tile(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaS
   const int ntx2 = (int)ceil_div(dv.Mt, kTXY);
   slot_geometry(dv);
   dv.prof = w.prof_on ? w.prof + (GATHER ? 16 : 0) : nullptr;
+  dv.err = w.flag + 1;
+  dv.N = N;
   {
     const char* e = getenv("SE1P_TILE_DBG");
     dv.dbg = e ? atoi(e) : 0;
@@ -504,7 +566,7 @@ static void launch_tile(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaS
   SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tile_mma<TZ, GATHER>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned nblk = (unsigned)(ntx2 * dv.nty2 * ntz);
-  k_tile_mma<TZ, GATHER><<<nblk, kThreads, smem, st>>>(dv, (const double4*)w.xs, (const int4*)w.s4, w.f6,
+  k_tile_mma<TZ, GATHER><<<nblk, kThreads, smem, st>>>(dv, (const double4*)w.xs, (const int4*)w.s4, w.wts,
                                                        w.bin_start, w.grid, GATHER ? w.gpart : nullptr, ntz);
   SE1P_LAUNCH_CHECK();
   if (GATHER) {
@@ -514,6 +576,7 @@ static void launch_tile(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaS
 }
 
 void k_spread_mma(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
+  k_weights(pl, w, N, st);
   if (tile_tz(pl.dv.M) == 32) launch_tile<32, false>(pl, w, N, nullptr, st);
   else launch_tile<16, false>(pl, w, N, nullptr, st);
 }

@@ -33,6 +33,8 @@ struct KDev {
   int nsxy, nsz, nslot;         // gather partial slots per particle
   unsigned long long* prof;     // optional phase counters of the tile kernels (nullptr = off)
   int dbg;                      // debug experiment bits of the tile kernels (0 = normal)
+  int* err;                     // device error word of the tile kernels (bounds checks)
+  int64_t N;
 };
 
 struct KPlan {
@@ -60,6 +62,8 @@ struct KWork {                  // per-N workspace (grown on demand)
   int* s4 = nullptr;            // sorted stencil starts: jx0, jy0, lz0, lz0 mod M (int4)
   double* f6 = nullptr;         // sorted FGG factors A_x, E_x, A_y, E_y, A_z, E_z
   int64_t cap_s4 = 0, cap_f6 = 0;
+  double* wts = nullptr;        // sorted stencil weights W[i][axis][t] (k_stencil_weights)
+  int64_t cap_wts = 0;
   int* perm = nullptr;          // sorted position -> original index
   int* keys = nullptr;
   int* bin_start = nullptr;
