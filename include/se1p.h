@@ -114,8 +114,9 @@ int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, 
                     double eta, double s0, double sf, int n_local, se1p_plan_info* info);
 
 /* Per-stage device time of the last _ex call on this thread, in milliseconds, measured
-   with CUDA events when opts->reserved[0] == 1 (profiling mode).  Stages: 0 bin/sort,
-   1 gridding, 2 z-FFT, 3 mode stage, 4 inverse z-FFT, 5 gather.  Returns stages written. */
+   with CUDA events on the call's stream when opts->reserved[0] == 1 (profiling mode).
+   Stages: 0 bin/sort, 1 particle records (window weights), 2 gridding tiles, 3 z-FFT,
+   4 mode stage, 5 inverse z-FFT, 6 gather tiles, 7 gather slot sum.  Returns stages written. */
 int se1p_last_stage_times(double* ms, int max_stages);
 
 /* Number of kernels the library launched in the last call on this thread. */

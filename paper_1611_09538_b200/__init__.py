@@ -96,23 +96,7 @@ def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=
     o.reserved[0] = 1 if profile else 0
     o.reserved[1] = int(stop_after)
     o.reserved[2] = 1 if reference_kernels else 0
-    o.reserved[3] = 1 if os.environ.get("SE1P_PHASE_COUNTERS") == "1" else 0
     return o
-
-
-def phase_counters():
-    """Debug: clock64 phase counters of the last gridding (first 16) and gather (last 16) tile
-    kernels, recorded when SE1P_PHASE_COUNTERS=1."""
-    buf = np.zeros(32)
-    _check(load().se1p_debug_copy(2, buf.ctypes.data, 32))
-    names = ["prod_total", "prod_wait_empty", "prod_stage", "prod_candidates", "batches", "", "", "",
-             "cons_total", "cons_wait_full", "cons_list", "cons_kstep", "mma_issued"]
-    out = {}
-    for base, tag in ((0, "spread"), (16, "gather")):
-        for i, nm in enumerate(names):
-            if nm:
-                out[f"{tag}.{nm}"] = buf[base + i]
-    return out
 
 
 def _Larr(L):
@@ -200,10 +184,11 @@ def plan_info(L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None
 
 
 def stage_times():
-    """Per-stage device ms of the last profiled call: bin, spread, zfft, modes, izfft, gather."""
-    buf = (ctypes.c_double * 8)()
-    n = load().se1p_last_stage_times(buf, 8)
-    names = ["bin", "spread", "zfft", "modes", "izfft", "gather"]
+    """Per-stage device ms of the last profiled call (CUDA events on the call's stream):
+    bin, records, spread, zfft, modes, izfft, gather, finish."""
+    buf = (ctypes.c_double * 10)()
+    n = load().se1p_last_stage_times(buf, 10)
+    names = ["bin", "records", "spread", "zfft", "modes", "izfft", "gather", "finish"]
     return {names[i]: buf[i] for i in range(n)}
 
 

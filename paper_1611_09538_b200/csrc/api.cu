@@ -11,12 +11,13 @@
 #include "kspace.cuh"
 #include "real.cuh"
 #include "sort.cuh"
+#include "tiles.cuh"
 
 namespace se1p {
 
 static thread_local std::string g_err;
 static thread_local int g_launches = 0;
-static thread_local double g_stage_ms[8];
+static thread_local double g_stage_ms[10];
 static thread_local int g_nstages = 0;
 static std::mutex g_mu;
 
@@ -53,12 +54,10 @@ static void grow(T*& p, int64_t& cap, int64_t need) {
 static void ensure_particles(KWork& w, int64_t N, int nbins) {
   grow(w.xs, w.cap_xs, 4 * N);
   grow(w.s4, w.cap_s4, 4 * N);
-  grow(w.f6, w.cap_f6, 6 * N);
   grow(w.perm, w.cap_perm, N);
   grow(w.keys, w.cap_keys, N);
   grow(w.bin_start, w.cap_bs, (int64_t)nbins + 1);
-  grow(w.total, w.cap_total, (int64_t)nbins + 1);
-  grow(w.hist, w.hist_cap, sort_hist_ints(N, nbins));
+  grow(w.scratch, w.scratch_cap, sort_scratch_ints(N, nbins));
   if (!w.red) {
     int64_t c1 = 0, c2 = 0;
     grow(w.red, c1, 4);
@@ -189,14 +188,14 @@ static void fill_info(const KPlan& pl, se1p_plan_info* info) {
 struct StageTimer {
   bool on;
   cudaStream_t st;
-  cudaEvent_t ev[9];
+  cudaEvent_t ev[10];
   int n = 0;
   StageTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
     if (on)
       for (auto& e : ev) cudaEventCreate(&e);
   }
   void mark() {
-    if (on && n < 9) cudaEventRecord(ev[n++], st);
+    if (on && n < 10) cudaEventRecord(ev[n++], st);
   }
   void finish() {
     if (!on) return;
@@ -252,18 +251,21 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
   if (!v1) {
     grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
-    grow(w.wts, w.cap_wts, N * 3 * dv.P);
+    grow(w.rec, w.cap_rec, N * (int64_t)rec_stride(dv.P));
   }
   w.prof_on = o && o->reserved[3] == 1;       // phase counters of the tile kernels
   if (w.prof_on) {
     if (!w.prof) SE1P_CUDA_TRY(cudaMalloc(&w.prof, 32 * sizeof(unsigned long long)));
     SE1P_CUDA_TRY(cudaMemsetAsync(w.prof, 0, 32 * sizeof(unsigned long long), st));
   }
+  // stages (se1p_last_stage_times): bin, records, spread, zfft, modes, izfft, gather, finish
   tm.mark();
   k_bin_particles(*pl, w, dx, dq, N, st);
   tm.mark();
+  if (!v1) k_records_stage(*pl, w, N, st);
+  tm.mark();
   if (v1) k_spread(*pl, w, N, st);
-  else k_spread_mma(*pl, w, N, st);
+  else k_spread_tiles(*pl, w, N, st);
   tm.mark();
   if (stop == 1) return sync_and_check(st);
   k_zfft_forward(*pl, w, st);
@@ -276,7 +278,9 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   tm.mark();
   if (stop == 4) return sync_and_check(st);
   if (v1) k_gather(*pl, w, N, dphi, st);
-  else k_gather_mma(*pl, w, N, dphi, st);
+  else k_gather_tiles(*pl, w, N, st);
+  tm.mark();
+  if (!v1) k_gather_finish_stage(*pl, w, N, dphi, st);
   tm.mark();
   if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   tm.finish();
@@ -419,7 +423,7 @@ void se1p_release(void) {
   cudaGetDevice(&d);
   DevState& ds = g_dev[d & 63];
   KWork& w = ds.w;
-  for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.hist, (void*)w.total,
+  for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
                   (void*)w.gpart})
     if (p) cudaFree(p);

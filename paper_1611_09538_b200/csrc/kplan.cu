@@ -52,8 +52,8 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   dv.Mt = dv.Mfree + p.P;
   dv.alpha = 2.0 * p.xi * p.xi / p.eta;
   dv.L3 = p.L[2];
-  dv.nbx = (int)ceil_div(dv.Mfree, kTX);
-  dv.nby = (int)ceil_div(dv.Mfree, kTY);
+  dv.nbx = (int)ceil_div(dv.Mfree, kBin);
+  dv.nby = (int)ceil_div(dv.Mfree, kBin);
   dv.nbz = (int)ceil_div(p.M, kTZ);
   dv.ntx = (int)ceil_div(dv.Mt, kTX);
   dv.nty = (int)ceil_div(dv.Mt, kTY);

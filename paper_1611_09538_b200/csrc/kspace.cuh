@@ -6,8 +6,10 @@
 
 namespace se1p {
 
-// Tile of the gridding / gather kernels on the extended grid (free x, free y, periodic z).
+// Tile of the v1 (reference) gridding kernel on the extended grid (free x, free y, periodic z).
 constexpr int kTX = 8, kTY = 8, kTZ = 16;
+// Particle bins: xy columns of kBin x kBin cells, z-sorted by cell inside a column.
+constexpr int kBin = 4;
 
 struct KParams {       // everything a k-space plan is keyed on
   double L[3];
@@ -27,7 +29,7 @@ struct KDev {
   int M, P, Mfree, Mt;          // grid: Mt x Mt (free, extended) x M (periodic)
   double h, inv_h, alpha;       // alpha = 2 xi^2 / eta (window exponent)
   double L3;
-  int nbx, nby, nbz;            // bins of kTX x kTY x kTZ cells
+  int nbx, nby, nbz;            // bins: xy columns of kBin x kBin cells (nbz: v1 z-chunks of kTZ)
   int ntx, nty, ntz;            // tiles over the Mt x Mt x M grid (v1 kernels)
   int nty2;                     // 16-wide tiles of the DMMA kernels
   int nsxy, nsz, nslot;         // gather partial slots per particle
@@ -57,19 +59,17 @@ struct KPlan {
 };
 
 struct KWork {                  // per-N workspace (grown on demand)
-  int64_t cap_xs = 0, cap_perm = 0, cap_keys = 0, cap_bs = 0, cap_total = 0;
+  int64_t cap_xs = 0, cap_perm = 0, cap_keys = 0, cap_bs = 0;
   double* xs = nullptr;         // sorted particles: x, y, z (folded), q  (double4 per particle)
   int* s4 = nullptr;            // sorted stencil starts: jx0, jy0, lz0, lz0 mod M (int4)
-  double* f6 = nullptr;         // sorted FGG factors A_x, E_x, A_y, E_y, A_z, E_z
-  int64_t cap_s4 = 0, cap_f6 = 0;
-  double* wts = nullptr;        // sorted stencil weights W[i][axis][t] (k_stencil_weights)
-  int64_t cap_wts = 0;
+  int64_t cap_s4 = 0;
+  double* rec = nullptr;        // sorted particle records (tiles.cuh, k_records)
+  int64_t cap_rec = 0;
   int* perm = nullptr;          // sorted position -> original index
   int* keys = nullptr;
   int* bin_start = nullptr;
-  int* hist = nullptr;
-  int64_t hist_cap = 0;
-  int* total = nullptr;
+  int* scratch = nullptr;       // sort scratch (sort_scratch_ints)
+  int64_t scratch_cap = 0;
   double* grid = nullptr;       // real grid Mt x Mt x M (H, then H~)
   double2* planes = nullptr;    // Hk: n_planes x Mt x Mt
   double2* T = nullptr;         // 2D pass workspace
@@ -89,8 +89,10 @@ void kplan_release_all();
 // Stages (launch on st).
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
 void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
-void k_spread_mma(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);      // DMMA tiles
-void k_gather_mma(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
+void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);   // tiles.cu
+void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);    // DMMA tiles
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);
+void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
 int64_t gather_slots(const KDev& dv);
 void slot_geometry(KDev& dv);
 int tile_tz(int M);

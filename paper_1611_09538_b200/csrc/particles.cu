@@ -25,18 +25,14 @@ __global__ void k_keys(KDev dv, const double* __restrict__ x, int64_t N, int* __
   cx = min(max(cx, 0), dv.Mfree - 1);
   cy = min(max(cy, 0), dv.Mfree - 1);
   cz = min(max(cz, 0), dv.M - 1);
-  // bins: xy columns of kTX x kTY cells, z-sorted by cell inside a column
-  keys[i] = ((cx / kTX) * dv.nby + (cy / kTY)) * dv.M + cz;
+  // bins: xy columns of kBin x kBin cells, z-sorted by cell inside a column
+  keys[i] = ((cx / kBin) * dv.nby + (cy / kBin)) * dv.M + cz;
 }
 
-// Sorted particle records: position/charge, stencil starts (reading R-3) and the per-particle
-// Fast Gaussian Gridding factors of each axis: with d0 the signed distance from the
-// particle to the first stencil node, the window weight at stencil offset t is
-//   e^{-alpha (d0 + t h)^2} = A E^t f1(t),  A = e^{-alpha d0^2},  E = e^{-2 alpha h d0},
-//   f1(t) = e^{-alpha h^2 t^2} (particle independent).
+// Sorted particles: position/charge and stencil starts (reading R-3).
 __global__ void k_permute(KDev dv, const double* __restrict__ x, const double* __restrict__ q,
                           const int* __restrict__ perm, int64_t N, double4* __restrict__ out,
-                          int4* __restrict__ s4, double* __restrict__ f6) {
+                          int4* __restrict__ s4) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= N) return;
   const int64_t i = perm[s];
@@ -52,16 +48,6 @@ __global__ void k_permute(KDev dv, const double* __restrict__ x, const double* _
   int a = lz0 % dv.M;
   if (a < 0) a += dv.M;
   s4[s] = make_int4(jx0, jy0, lz0, a);
-  const double dx = ((double)jx0 - 0.5 * dv.P) * dv.h - px;
-  const double dy = ((double)jy0 - 0.5 * dv.P) * dv.h - py;
-  const double dz = (double)lz0 * dv.h - pz;
-  double* f = f6 + 6 * s;
-  f[0] = exp(-dv.alpha * dx * dx);
-  f[1] = exp(-2.0 * dv.alpha * dv.h * dx);
-  f[2] = exp(-dv.alpha * dy * dy);
-  f[3] = exp(-2.0 * dv.alpha * dv.h * dy);
-  f[4] = exp(-dv.alpha * dz * dz);
-  f[5] = exp(-2.0 * dv.alpha * dv.h * dz);
 }
 
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st) {
@@ -70,8 +56,8 @@ void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_keys<<<nb, 256, 0, st>>>(dv, x, N, w.keys);
   SE1P_LAUNCH_CHECK();
-  stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.hist, w.total, st);
-  k_permute<<<nb, 256, 0, st>>>(dv, x, q, w.perm, N, (double4*)w.xs, (int4*)w.s4, w.f6);
+  stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.scratch, st);
+  k_permute<<<nb, 256, 0, st>>>(dv, x, q, w.perm, N, (double4*)w.xs, (int4*)w.s4);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -125,8 +111,8 @@ __global__ void __launch_bounds__(128) k_spread_v1(KDev dv, const double4* __res
   for (int k = 0; k < 8; ++k) acc[k] = 0.0;
 
   // bins whose cells can touch the tile: cx in [X0-P, X0+kTX-2] etc. (stencil j0 = cx+1)
-  const int bx0 = max(0, floordiv(X0 - dv.P, kTX)), bx1 = min(dv.nbx - 1, floordiv(X0 + kTX - 2, kTX));
-  const int by0 = max(0, floordiv(Y0 - dv.P, kTY)), by1 = min(dv.nby - 1, floordiv(Y0 + kTY - 2, kTY));
+  const int bx0 = max(0, floordiv(X0 - dv.P, kBin)), bx1 = min(dv.nbx - 1, floordiv(X0 + kTX - 2, kBin));
+  const int by0 = max(0, floordiv(Y0 - dv.P, kBin)), by1 = min(dv.nby - 1, floordiv(Y0 + kTY - 2, kBin));
   int bz0 = floordiv(Z0 - dv.P - 1, kTZ), bz1 = floordiv(Z0 + kTZ + dv.P + 1, kTZ);
   if (bz1 - bz0 + 1 >= dv.nbz) { bz0 = 0; bz1 = dv.nbz - 1; }
 

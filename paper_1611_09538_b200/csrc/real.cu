@@ -90,7 +90,7 @@ void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
   SE1P_LAUNCH_CHECK();
-  stable_bin_sort(w.keys, N, ncell, w.perm, w.bin_start, w.hist, w.total, st);
+  stable_bin_sort(w.keys, N, ncell, w.perm, w.bin_start, w.scratch, st);
   k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
   SE1P_LAUNCH_CHECK();
   k_real_sum<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out);

@@ -4,13 +4,11 @@
 
 namespace se1p {
 
-constexpr int kChunk = 4096;
-
 // keys[i] in [0, nbins).  perm[pos] = original index of the particle at sorted position pos;
 // bin_start[b] .. bin_start[b+1] is bin b (bin_start has nbins+1 entries).
-// hist: sort_hist_ints(N, nbins) ints of scratch; total: nbins ints of scratch.
-void stable_bin_sort(const int* keys, int64_t N, int nbins, int* perm, int* bin_start, int* hist,
-                     int* total, cudaStream_t st);
-int64_t sort_hist_ints(int64_t N, int nbins);
+// scratch: sort_scratch_ints(N, nbins) ints.
+void stable_bin_sort(const int* keys, int64_t N, int nbins, int* perm, int* bin_start, int* scratch,
+                     cudaStream_t st);
+int64_t sort_scratch_ints(int64_t N, int nbins);
 
 }  // namespace se1p

@@ -1,26 +1,46 @@
-// tiles.cuh -- shared machinery of the DMMA gridding and gather kernels (tiles.cu).
+// tiles.cuh -- shared machinery of the gridding and gather tile kernels (tiles.cu).
 //
-// CTA tile: 16 (x) x 16 (y) columns of the extended grid x TZ (z) nodes, 16 warps; warp w owns
-// the 4 x 4 column block (4 (w&3), 4 (w>>2)) over all TZ nodes.  Gridding is the contraction
-//   H[(x,y), z] += sum_p (wx_p[x] wy_p[y]) (q_p wz_p[z])                 (Eq. (spread_1p))
-// and the gather the contraction T[(x,y), p] = sum_z H~[(x,y), z] wz_p[z] followed by
-// phi_p += sum_(x,y) wx_p[x] wy_p[y] T[(x,y), p]                          (Eq. (se1p_complete_
-// discretized)); both run on the FP64 tensor pipe (mma.sync m16n8k4 f64, SASS DMMA).
+// Gridding (Alg. 1 step 2, Eq. (spread_1p)) is, per output tile, the contraction
+//   H[(x,y), z] += sum_p (q_p wx_p[x] wy_p[y]) wz_p[z]
+// and the gather (Alg. 1 step 6, Eq. (se1p_complete_discretized)) the contraction
+//   T[(x,y), p] = sum_z H~[(x,y), z] wz_p[z],   phi_p += sum_(x,y) wx_p[x] wy_p[y] T[(x,y), p].
+// Both run on the FP64 tensor pipe with mma.sync m16n8k8 f64 (SASS DMMA): tcgen05.mma has no
+// f64 kind, so DMMA is the sm_100a fp64 matrix path (same 37 TFLOP/s as DFMA, 4-16x fewer
+// instructions per FMA).
 #pragma once
 #include "kspace.cuh"
 
 namespace se1p {
 
-constexpr int kTXY = 16;        // CTA x and y extent (grid nodes)
-constexpr int kWarps = 16;      // 4 x 4 column blocks of 4 x 4
-constexpr int kStage = 64;      // particles staged per batch
-constexpr int kSX = 20;         // smem row stride of x/y weights (doubles, = 4 mod 16: no bank conflicts)
+constexpr int kTXY = 16;        // CTA tile extent in x and y (grid nodes)
+constexpr int kBXY = 4;         // particle bins: xy columns of kBXY x kBXY cells, z-sorted inside
 
-__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b) {
+// Particle record (one row per sorted particle, RS doubles, built by k_records):
+//   [0,1] int4 {jx0, jy0, lz0, lz0 mod M}   stencil starts (reading R-3)
+//   [2]   q
+//   [3]   0                          guard (index -1 of wx)
+//   [4, 4+P)        wx[t]            window weights e^{-alpha d_t^2} per axis
+//   [4+P]           0                guard
+//   [5+P, 5+2P)     wy[t]
+//   [5+2P]          0
+//   [6+2P, 6+3P)    wz[t]
+//   [6+3P]          0
+// RS = smallest value >= 7+3P with RS = 4 (mod 16): rows are 16-byte aligned for the bulk copy
+// and consecutive rows start 4 doubles (8 banks) apart in shared memory.
+__host__ __device__ inline int rec_stride(int P) {
+  int r = 7 + 3 * P;
+  while (r % 16 != 4) ++r;
+  return r;
+}
+__host__ __device__ inline int rec_wx() { return 4; }
+__host__ __device__ inline int rec_wy(int P) { return 5 + P; }
+__host__ __device__ inline int rec_wz(int P) { return 6 + 2 * P; }
+
+__device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], double b0, double b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a0), "d"(a1), "d"(b));
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b0), "d"(b1));
 }
 
 __device__ __forceinline__ int fdiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }

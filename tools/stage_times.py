@@ -19,4 +19,4 @@ for r in range(6):
     if r >= 2:
         for k, v in se1p.stage_times().items():
             acc[k] = acc.get(k, 0.0) + v / 4
-print(cfg.name, "v1" if v1 else "tiles", " ".join(f"{k}={v:.3f}" for k, v in acc.items()), f"total={sum(acc.values()):.3f} ms")
+print(cfg.name, "v1" if v1 else "tiles", " ".join(f"{k}={v:.3f}" for k, v in acc.items()), f"total={sum(acc.values()):.3f} ms", flush=True)
