@@ -229,7 +229,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   DevState& ds = dev_state();
   KWork& w = ds.w;
   const KDev& dv = pl->dv;
-  ensure_particles(w, N, dv.nbx * dv.nby * dv.M);
+  ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
   grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
   grow(w.planes, w.planes_cap, (int64_t)pl->n_planes * dv.Mt * dv.Mt);
   grow(w.T, w.T_cap, pl->t_off_total);

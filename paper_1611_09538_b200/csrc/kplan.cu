@@ -102,6 +102,14 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_pl, plv.data(), sizeof(double2) * pl->n_planes, cudaMemcpyHostToDevice));
   }
 
+  // Fast Gaussian Gridding table f1[t] = e^{-alpha h^2 t^2}
+  {
+    std::vector<double> f1(p.P);
+    for (int t = 0; t < p.P; ++t) f1[t] = std::exp(-dv.alpha * h * h * (double)t * (double)t);
+    SE1P_CUDA_TRY(cudaMalloc(&pl->d_f1, sizeof(double) * p.P));
+    SE1P_CUDA_TRY(cudaMemcpy(pl->d_f1, f1.data(), sizeof(double) * p.P, cudaMemcpyHostToDevice));
+  }
+
   // kernel planes: k3 = 0 (extent S0) and 0 < k3 <= 2 pi n_l/L3 (extent SI)
   {
     const int LK = pl->LK;
@@ -144,6 +152,7 @@ KPlan* kplan_get(const KParams& p, cudaStream_t st) {
     cudaFree(old->d_exJ);
     cudaFree(old->d_k2J);
     cudaFree(old->d_pl);
+    cudaFree(old->d_f1);
     g_plans.erase(g_plans.begin());
   }
   return build(p, st);
@@ -156,6 +165,7 @@ void kplan_release_all() {
     cudaFree(q->d_exJ);
     cudaFree(q->d_k2J);
     cudaFree(q->d_pl);
+    cudaFree(q->d_f1);
   }
   g_plans.clear();
 }

@@ -52,6 +52,7 @@ struct KPlan {
   double* d_exJ = nullptr;      // [SJ] e^{-(1-eta) kappa_a^2/(4 xi^2)}, kappa_a = 2 pi a'/(SJ h)
   double* d_k2J = nullptr;      // [SJ] kappa_a^2
   double* d_pl = nullptr;       // [n_planes][2]: e^{-(1-eta) k3^2/(4xi^2)} * C_J, k3^2
+  double* d_f1 = nullptr;       // [P] e^{-alpha h^2 t^2}, the particle-independent FGG factor
   int64_t t_off_total = 0;      // workspace T size (complex) for the 2D passes
   std::vector<int64_t> t_off;   // per plane offset into T
   double const_gather = 0;      // 4 pi h^3 (2 xi^2/(pi eta))^3 (reading R-1)

@@ -25,8 +25,9 @@ __global__ void k_keys(KDev dv, const double* __restrict__ x, int64_t N, int* __
   cx = min(max(cx, 0), dv.Mfree - 1);
   cy = min(max(cy, 0), dv.Mfree - 1);
   cz = min(max(cz, 0), dv.M - 1);
-  // bins: xy columns of kBin x kBin cells, z-sorted by cell inside a column
-  keys[i] = ((cx / kBin) * dv.nby + (cy / kBin)) * dv.M + cz;
+  // bins: (x band of kBin cells, z cell, y cell), y fastest -- a tile's candidates in one x band
+  // and z cell are one contiguous run of the sorted order
+  keys[i] = ((cx / kBin) * dv.M + cz) * dv.Mfree + cy;
 }
 
 // Sorted particles: position/charge and stencil starts (reading R-3).
@@ -52,7 +53,7 @@ __global__ void k_permute(KDev dv, const double* __restrict__ x, const double* _
 
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st) {
   const KDev& dv = pl.dv;
-  const int nbins = dv.nbx * dv.nby * dv.M;
+  const int nbins = dv.nbx * dv.M * dv.Mfree;
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_keys<<<nb, 256, 0, st>>>(dv, x, N, w.keys);
   SE1P_LAUNCH_CHECK();
@@ -110,18 +111,18 @@ __global__ void __launch_bounds__(128) k_spread_v1(KDev dv, const double4* __res
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.0;
 
-  // bins whose cells can touch the tile: cx in [X0-P, X0+kTX-2] etc. (stencil j0 = cx+1)
+  // cells whose particles can touch the tile: cx in [X0-P, X0+kTX-2] etc. (stencil j0 = cx+1)
   const int bx0 = max(0, floordiv(X0 - dv.P, kBin)), bx1 = min(dv.nbx - 1, floordiv(X0 + kTX - 2, kBin));
-  const int by0 = max(0, floordiv(Y0 - dv.P, kBin)), by1 = min(dv.nby - 1, floordiv(Y0 + kTY - 2, kBin));
-  int bz0 = floordiv(Z0 - dv.P - 1, kTZ), bz1 = floordiv(Z0 + kTZ + dv.P + 1, kTZ);
-  if (bz1 - bz0 + 1 >= dv.nbz) { bz0 = 0; bz1 = dv.nbz - 1; }
+  const int cy0 = max(0, Y0 - dv.P), cy1 = min(dv.Mfree - 1, Y0 + kTY - 2);
+  int cz0 = Z0 - dv.P - 1, nz = kTZ + 2 * dv.P + 3;
+  if (nz >= dv.M) { cz0 = 0; nz = dv.M; }
 
   for (int bx = bx0; bx <= bx1; ++bx)
-    for (int by = by0; by <= by1; ++by)
-      for (int bzu = bz0; bzu <= bz1; ++bzu) {
-        const int bz = imod(bzu, dv.nbz);
-        const int col = (bx * dv.nby + by) * dv.M;
-        const int s = bin_start[col + bz * kTZ], e = bin_start[col + min(bz * kTZ + kTZ, dv.M)];
+    for (int zz = 0; zz < nz; ++zz) {
+      if (cy1 < cy0) break;
+      {
+        const int row = (bx * dv.M + imod(cz0 + zz, dv.M)) * dv.Mfree;
+        const int s = bin_start[row + cy0], e = bin_start[row + cy1 + 1];
         for (int base = s; base < e; base += kBatch) {
           const int cnt = min(kBatch, e - base);
           for (int task = tid; task < cnt * 4; task += blockDim.x) {
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(128) k_spread_v1(KDev dv, const double4* __res
           __syncthreads();
         }
       }
+    }
   const int gx = X0 + ix, gy = Y0 + iy;
   if (gx < dv.Mt && gy < dv.Mt) {
     double* col = grid + ((int64_t)gx * dv.Mt + gy) * dv.M;

@@ -32,8 +32,6 @@ namespace se1p {
 constexpr int kCW = 16;                      // consumer warps
 constexpr int kThreads = (kCW + 1) * 32;     // + 1 producer warp
 constexpr int kMaxNB = 4;
-constexpr int kWinCells = 4;                 // z cells per candidate window
-constexpr int kMaxCols = 512;                // candidate bin columns per tile (host-checked)
 
 struct TileArgs {
   KDev dv;
@@ -51,7 +49,7 @@ struct TileSmem {
 
 __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int RS, bool gather) {
   TileSmem s;
-  int o = 2 * kMaxNB * 8 + kMaxNB * 4 + 2 * kMaxCols * 4;   // barriers, counts, column tables
+  int o = 2 * kMaxNB * 8 + kMaxNB * 4;   // barriers, counts
   s.off_pidx = o;
   o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
@@ -139,8 +137,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxNB;
   int* cnt = reinterpret_cast<int*>(empty + kMaxNB);
-  int* colS = cnt + kMaxNB;
-  int* colN = colS + kMaxCols;
   int* pidx = reinterpret_cast<int*>(smem + L.off_pidx);
   int2* lists = reinterpret_cast<int2*>(smem + L.off_lists);
   double* acc = reinterpret_cast<double*>(smem + L.off_acc);
@@ -217,29 +213,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
       have = false;
     };
 
+    // Candidate runs: z cells czs .. czs+span-1 (unwrapped, z-major), x bands bx0..bx1, and in
+    // each the contiguous y-cell range cy0..cy1 of the sorted order (bins: x band, z, y).
     const int bx0 = max(0, fdiv(X0 - P, kBin)), bx1 = min(dv.nbx - 1, fdiv(X0 + kTXY - 2, kBin));
-    const int by0 = max(0, fdiv(Y0 - P, kBin)), by1 = min(dv.nby - 1, fdiv(Y0 + kTXY - 2, kBin));
-    const int nbyc = by1 - by0 + 1, ncol = max(0, (bx1 - bx0 + 1) * nbyc);
-    // cells whose stencil may reach the tile: lz0 = floor(z/h - P/2) + 1 within P-1 of the tile
-    int czs = Z0 - P / 2 - 1, span = TZ + P + 2;
+    const int cy0 = max(0, Y0 - P), cy1 = min(dv.Mfree - 1, Y0 + kTXY - 2);
+    const int nbx = bx1 - bx0 + 1;
+    int czs = Z0 - P / 2 - 1, span = TZ + P + 2;   // cells whose stencils may reach the tile
     if (span >= M) {
       czs = 0;
       span = M;
     }
-    for (int w0 = 0; w0 < span;) {
-      const int a = pmod(czs + w0, M);
-      const int len = min(min(kWinCells, span - w0), M - a);   // a window never crosses the seam
-      w0 += len;
-      for (int c = lane; c < ncol; c += 32) {
-        const int bx = bx0 + c / nbyc, by = by0 + c % nbyc;
-        const int base = (bx * dv.nby + by) * M + a;
-        const int s = A.bin_start[base];
-        colS[c] = s;
-        colN[c] = A.bin_start[base + len] - s;
+    const int npc = (cy1 >= cy0 && nbx > 0) ? span * nbx : 0;
+    auto load_run = [&](int q, int& s, int& e) {
+      s = e = 0;
+      if (q < npc) {
+        const int zz = q / nbx, bx = bx0 + (q - zz * nbx);
+        const int row = (bx * M + pmod(czs + zz, M)) * dv.Mfree;
+        s = A.bin_start[row + cy0];
+        e = A.bin_start[row + cy1 + 1];
       }
-      __syncwarp();
-      for (int c = 0; c < ncol; ++c) {
-        int s = colS[c], n = colN[c];
+    };
+    int sN, eN;
+    load_run(lane, sN, eN);
+    for (int q0 = 0; q0 < npc; q0 += 32) {
+      const int sC = sN, eC = eN;
+      load_run(q0 + 32 + lane, sN, eN);   // prefetch the next 32 runs
+      const int nq = min(32, npc - q0);
+      for (int i = 0; i < nq; ++i) {
+        int s = __shfl_sync(0xffffffffu, sC, i);
+        int n = __shfl_sync(0xffffffffu, eC, i) - s;
         while (n > 0) {
           if (!have) acquire();
           const int take = min(n, BM - fill);
@@ -256,7 +258,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
           if (fill == BM) publish(BM);
         }
       }
-      __syncwarp();
     }
     if (fill > 0) publish(fill);
     acquire();
@@ -298,9 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   }
   const int2 dummy = make_int2(BM | (8 << 16) | (8 << 24), 0);
 
-  for (int j = 0;; ++j) {
-    const int b = j % NB;
-    mbar_wait(&full[b], (unsigned)((j / NB) & 1));
+  for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
+    mbar_wait(&full[b], (unsigned)ph);
     const int cn = cnt[b];
     if (cn < 0) break;
     const double* bb = bufs + b * BS;
@@ -442,36 +442,54 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   phi[perm[p]] = s;
 }
 
-// Record rows of the sorted particles (layout in tiles.cuh): one thread per row element.
-// Window weight of stencil node t: e^{-alpha d_t^2}, d_t the signed node-particle distance
-// (Eq. (spread_1p) factorised per axis, reading R-3).
-__global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, int64_t N, int RS,
-                          double* __restrict__ rec) {
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= N * RS) return;
-  const int64_t i = id / RS;
-  const int e = (int)(id - i * RS);
+// Record rows of the sorted particles (layout in tiles.cuh).  Window weights by Fast Gaussian
+// Gridding: with d0 the signed distance from the particle to the first stencil node,
+//   e^{-alpha (d0 + t h)^2} = e^{-alpha d0^2} (e^{-2 alpha h d0})^t e^{-alpha h^2 t^2},
+// i.e. two exponentials per particle and axis plus the particle-independent table f1[t]
+// (reading R-3 for the node positions).  kRecPB particles per block are assembled in shared
+// memory and written out as one coalesced run.
+constexpr int kRecPB = 16;
+
+__global__ void __launch_bounds__(128) k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4,
+                                                 int64_t N, int RS, const double* __restrict__ f1,
+                                                 double* __restrict__ rec) {
+  extern __shared__ __align__(16) double srow[];
   const int P = dv.P;
-  const int4 s = S4[i];
-  if (e < 2) {
-    reinterpret_cast<int2*>(rec + i * RS)[e] = (e == 0) ? make_int2(s.x, s.y) : make_int2(s.z, s.w);
-    return;
+  const int64_t i0 = (int64_t)blockIdx.x * kRecPB;
+  const int np = (int)((N - i0 < kRecPB) ? (N - i0) : kRecPB);
+  for (int k = threadIdx.x; k < kRecPB * RS; k += blockDim.x) srow[k] = 0.0;
+  __syncthreads();
+  if (threadIdx.x < 3 * np) {
+    const int p = threadIdx.x / 3, ax = threadIdx.x - 3 * p;
+    const int64_t i = i0 + p;
+    const double4 pp = P4[i];
+    const int4 s = S4[i];
+    double* row = srow + p * RS;
+    double d0;
+    int off;
+    if (ax == 0) {
+      d0 = ((double)s.x - 0.5 * P) * dv.h - pp.x;
+      off = rec_wx();
+      reinterpret_cast<int4*>(row)[0] = s;
+      row[2] = pp.w;
+    } else if (ax == 1) {
+      d0 = ((double)s.y - 0.5 * P) * dv.h - pp.y;
+      off = rec_wy(P);
+    } else {
+      d0 = (double)s.z * dv.h - pp.z;
+      off = rec_wz(P);
+    }
+    double g = exp(-dv.alpha * d0 * d0);
+    const double E = exp(-2.0 * dv.alpha * dv.h * d0);
+    for (int t = 0; t < P; ++t) {
+      row[off + t] = g * f1[t];
+      g *= E;
+    }
   }
-  const double4 pp = P4[i];
-  double v = 0.0;
-  if (e == 2) {
-    v = pp.w;
-  } else if (e >= rec_wx() && e < rec_wx() + P) {
-    const double d = ((double)(s.x + e - rec_wx()) - 0.5 * P) * dv.h - pp.x;
-    v = exp(-dv.alpha * d * d);
-  } else if (e >= rec_wy(P) && e < rec_wy(P) + P) {
-    const double d = ((double)(s.y + e - rec_wy(P)) - 0.5 * P) * dv.h - pp.y;
-    v = exp(-dv.alpha * d * d);
-  } else if (e >= rec_wz(P) && e < rec_wz(P) + P) {
-    const double d = (double)(s.z + e - rec_wz(P)) * dv.h - pp.z;
-    v = exp(-dv.alpha * d * d);
-  }
-  rec[id] = v;
+  __syncthreads();
+  const double2* src = reinterpret_cast<const double2*>(srow);
+  double2* dst = reinterpret_cast<double2*>(rec + i0 * RS);
+  for (int k = threadIdx.x; k < np * RS / 2; k += blockDim.x) dst[k] = src[k];
 }
 
 int tile_tz(int M) { return M >= 64 ? 32 : 16; }
@@ -493,8 +511,11 @@ int64_t gather_slots(const KDev& dv) {
 
 void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
   const int RS = rec_stride(pl.dv.P);
-  const int64_t n = N * RS;
-  k_records<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, RS, w.rec);
+  const size_t smem = sizeof(double) * kRecPB * RS;
+  if (smem > 48 * 1024)
+    SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_records, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_records<<<(unsigned)ceil_div(N, kRecPB), 128, smem, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, RS,
+                                                               pl.d_f1, w.rec);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -514,8 +535,6 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) 
   a.bin_start = w.bin_start;
   a.grid = w.grid;
   a.gpart = GATHER ? w.gpart : nullptr;
-  const int ncol_max = ((kTXY + dv.P - 1) / kBin + 2) * ((kTXY + dv.P - 1) / kBin + 2);
-  if (ncol_max > kMaxCols) throw Error{4, "P too large for the tile kernels"};
   int BM = 0, NB = 0;
   const int limit = 227 * 1024 - 1024;
   for (int bm : {64, 32, 16}) {
