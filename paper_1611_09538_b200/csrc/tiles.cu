@@ -54,7 +54,7 @@ __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int RS, bool gathe
   o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
   s.off_lists = o;
-  o += kCW * (BM + 8) * 8;
+  o += kCW * (BM + 16) * 8;
   o = (o + 15) & ~15;
   s.off_acc = o;
   if (gather) o += NB * BM * (kCW + 1) * 8;
@@ -126,7 +126,7 @@ __device__ __forceinline__ int zmask_of(int d, int P, int M, int jmax) {
   return zm;
 }
 
-template <int TZ, bool GATHER>
+template <int TZ, bool GATHER, bool WRAP2>
 __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   constexpr int NZB = TZ / 8;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -273,31 +273,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   }
 
   // ================================================================ consumers
+  // List entry per relevant particle: x = p | zmask << 8 | (ox + 8) << 16 | (oy + 8) << 24 with
+  // ox = X0b - jx0, oy = Y0b - jy0 (window offsets of the warp block), y = the z offset:
+  //   WRAP2:  d = (Z0 - a) mod M, stencil index of tile node j is (d + j) mod M
+  //   else:   e = signed tile offset of the stencil start, stencil index of node j is j - e
   const int gid = lane >> 2, tig = lane & 3;
-  const int cx = gid & 3, cy = gid >> 2;
   const int X0b = X0 + 4 * (w & 3), Y0b = Y0 + 4 * (w >> 2);
-  int2* wl = lists + w * (BM + 8);
-  double c[NZB][4];
-  double hA[GATHER ? NZB : 1][4];
+  int2* wl = lists + w * (BM + 16);
+  const int2 dummy = make_int2(BM | (8 << 16) | (8 << 24), WRAP2 ? 0 : -P);
+  auto zidx = [&](int y, int j) -> int {   // stencil index of tile node j, clamped onto a guard
+    if (WRAP2) {
+      int t = y + j;
+      t -= (t >= M) ? M : 0;
+      return min(t, P);
+    }
+    return clampw(j - y, P);
+  };
+
+  // gridding accumulators: C[16 cols x 8 z] per 8-node block; col r -> (r & 3, r >> 2) of the block
+  double c[GATHER ? 1 : NZB][4];
+  // gather operands: H~[8 z x 8 cols] per (z block, col half); col n of half h -> (n & 3, (n >> 2) + 2h)
+  double hB[GATHER ? NZB : 1][2][2];
+  if (!GATHER) {
 #pragma unroll
-  for (int zb = 0; zb < NZB; ++zb) c[zb][0] = c[zb][1] = c[zb][2] = c[zb][3] = 0.0;
-  if (GATHER) {
-    const int x = X0b + cx, y0 = Y0b + cy, y1 = y0 + 2;
+    for (int zb = 0; zb < NZB; ++zb) c[zb][0] = c[zb][1] = c[zb][2] = c[zb][3] = 0.0;
+  } else {
+    const int x = X0b + (gid & 3);
 #pragma unroll
     for (int zb = 0; zb < NZB; ++zb)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int z = Z0 + 8 * zb + tig + 4 * h;
-        double v0 = 0.0, v1 = 0.0;
-        if (z < M && x < Mt) {
-          if (y0 < Mt) v0 = A.grid[((int64_t)x * Mt + y0) * M + z];
-          if (y1 < Mt) v1 = A.grid[((int64_t)x * Mt + y1) * M + z];
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int y = Y0b + (gid >> 2) + 2 * h, z = Z0 + 8 * zb + tig + 4 * kk;
+          hB[zb][h][kk] = (z < M && x < Mt && y < Mt) ? A.grid[((int64_t)x * Mt + y) * M + z] : 0.0;
         }
-        hA[zb][2 * h] = v0;
-        hA[zb][2 * h + 1] = v1;
-      }
   }
-  const int2 dummy = make_int2(BM | (8 << 16) | (8 << 24), 0);
 
   for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
     mbar_wait(&full[b], (unsigned)ph);
@@ -318,92 +329,94 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
           if (d < 0) d += M;
           const int zm = zmask_of(d, P, M, jmax);
           rel = zm != 0;
-          e = make_int2(p | (zm << 8) | ((ox + 8) << 16) | ((oy + 8) << 24), d);
+          e = make_int2(p | (zm << 8) | ((ox + 8) << 16) | ((oy + 8) << 24), WRAP2 ? d : (d < P ? -d : M - d));
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
       if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
       n += __popc(bal);
     }
-    const int npad = (n + 7) & ~7;
+    const int npad = (n + 15) & ~15;
     if (lane < npad - n) wl[n + lane] = dummy;
     __syncwarp();
 
     if (!GATHER) {
-      for (int k = 0; k < npad; k += 8) {
-        const int2 e0 = wl[k + tig], e1 = wl[k + tig + 4];
-        int zm = ((e0.x | e1.x) >> 8) & 0xff;
+      // C[16 cols x 8 z] += A[16 cols x 16 particles] B[16 particles x 8 z]; particle of k-slot
+      // tig + 4j is list entry k + tig + 4j (A and B agree on it)
+      const int cx = gid & 3, cy = gid >> 2;
+      for (int k = 0; k < npad; k += 16) {
+        int2 e[4];
+        int zm = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          e[j] = wl[k + tig + 4 * j];
+          zm |= e[j].x;
+        }
+        zm = (zm >> 8) & 0xff;
         zm |= __shfl_xor_sync(0xffffffffu, zm, 1);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 2);
-        const double* r0 = bb + (e0.x & 0xff) * RS;
-        const double* r1 = bb + (e1.x & 0xff) * RS;
-        double a[4];
-        {
-          const int ox = ((e0.x >> 16) & 0xff) - 8, oy = ((unsigned)e0.x >> 24) - 8;
-          const double wq = r0[2] * r0[WXo + clampw(ox + cx, P)];
-          a[0] = wq * r0[WYo + clampw(oy + cy, P)];
-          a[1] = wq * r0[WYo + clampw(oy + cy + 2, P)];
+        double a[8];
+        const double* rz[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double* r = bb + (e[j].x & 0xff) * RS;
+          const int ox = ((e[j].x >> 16) & 0xff) - 8, oy = ((unsigned)e[j].x >> 24) - 8;
+          const double wq = r[2] * r[WXo + clampw(ox + cx, P)];
+          a[2 * j] = wq * r[WYo + clampw(oy + cy, P)];
+          a[2 * j + 1] = wq * r[WYo + clampw(oy + cy + 2, P)];
+          rz[j] = r + WZo;
         }
-        {
-          const int ox = ((e1.x >> 16) & 0xff) - 8, oy = ((unsigned)e1.x >> 24) - 8;
-          const double wq = r1[2] * r1[WXo + clampw(ox + cx, P)];
-          a[2] = wq * r1[WYo + clampw(oy + cy, P)];
-          a[3] = wq * r1[WYo + clampw(oy + cy + 2, P)];
-        }
-        const double* z0 = r0 + WZo;
-        const double* z1 = r1 + WZo;
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
           if ((zm >> zb) & 1) {
-            int t0 = e0.y + 8 * zb + gid, t1 = e1.y + 8 * zb + gid;
-            t0 -= (t0 >= M) ? M : 0;
-            t1 -= (t1 >= M) ? M : 0;
-            dmma_16x8x8(c[zb], a, z0[min(t0, P)], z1[min(t1, P)]);
+            const int jz = 8 * zb + gid;
+            dmma_16x8x16(c[zb], a, rz[0][zidx(e[0].y, jz)], rz[1][zidx(e[1].y, jz)], rz[2][zidx(e[2].y, jz)],
+                         rz[3][zidx(e[3].y, jz)]);
           }
         }
       }
     } else {
-      for (int k = 0; k < npad; k += 8) {
-        const int2 e = wl[k + gid];
-        int zm = (e.x >> 8) & 0xff;
+      // T[16 particles x 8 cols] = A[16 particles x 8 z] (wz) B[8 z x 8 cols] (H~), per col half;
+      // particle of row gid (gid + 8) is list entry k + gid (k + gid + 8)
+      for (int k = 0; k < npad; k += 16) {
+        const int2 e0 = wl[k + gid], e1 = wl[k + gid + 8];
+        int zm = ((e0.x | e1.x) >> 8) & 0xff;
         zm |= __shfl_xor_sync(0xffffffffu, zm, 4);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 8);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 16);
-        const double* rz = bb + (e.x & 0xff) * RS + WZo;
-        double t0v[4] = {0.0, 0.0, 0.0, 0.0}, t1v[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* r0 = bb + (e0.x & 0xff) * RS;
+        const double* r1 = bb + (e1.x & 0xff) * RS;
+        double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
           if ((zm >> zb) & 1) {
-            int u0 = e.y + 8 * zb + tig, u1 = u0 + 4;
-            u0 -= (u0 >= M) ? M : 0;
-            u1 -= (u1 >= M) ? M : 0;
-            if (zb & 1) dmma_16x8x8(t1v, hA[zb], rz[min(u0, P)], rz[min(u1, P)]);
-            else dmma_16x8x8(t0v, hA[zb], rz[min(u0, P)], rz[min(u1, P)]);
+            const int j0 = 8 * zb + tig, j1 = j0 + 4;
+            const double a[4] = {r0[WZo + zidx(e0.y, j0)], r1[WZo + zidx(e1.y, j0)], r0[WZo + zidx(e0.y, j1)],
+                                 r1[WZo + zidx(e1.y, j1)]};
+            dmma_16x8x8(t0, a, hB[zb][0][0], hB[zb][0][1]);
+            dmma_16x8x8(t1, a, hB[zb][1][0], hB[zb][1][1]);
           }
         }
-        const int2 ea = wl[k + 2 * tig], eb = wl[k + 2 * tig + 1];
-        double va, vb;
-        {
-          const double* r = bb + (ea.x & 0xff) * RS;
-          const int ox = ((ea.x >> 16) & 0xff) - 8, oy = ((unsigned)ea.x >> 24) - 8;
-          va = r[WXo + clampw(ox + cx, P)] *
-               fma(r[WYo + clampw(oy + cy, P)], t0v[0] + t1v[0], r[WYo + clampw(oy + cy + 2, P)] * (t0v[2] + t1v[2]));
-        }
-        {
-          const double* r = bb + (eb.x & 0xff) * RS;
-          const int ox = ((eb.x >> 16) & 0xff) - 8, oy = ((unsigned)eb.x >> 24) - 8;
-          vb = r[WXo + clampw(ox + cx, P)] *
-               fma(r[WYo + clampw(oy + cy, P)], t0v[1] + t1v[1], r[WYo + clampw(oy + cy + 2, P)] * (t0v[3] + t1v[3]));
-        }
+        // this thread's cols: x = 2 (tig & 1) + {0, 1}, y = (tig >> 1) + {0 (half 0), 2 (half 1)}
+        const int cx0 = 2 * (tig & 1), cy0 = tig >> 1;
+        double v[2];
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          va += __shfl_xor_sync(0xffffffffu, va, off);
-          vb += __shfl_xor_sync(0xffffffffu, vb, off);
+        for (int h = 0; h < 2; ++h) {
+          const int2 eh = h ? e1 : e0;
+          const double* r = h ? r1 : r0;
+          const int ox = ((eh.x >> 16) & 0xff) - 8, oy = ((unsigned)eh.x >> 24) - 8;
+          const double wx0 = r[WXo + clampw(ox + cx0, P)], wx1 = r[WXo + clampw(ox + cx0 + 1, P)];
+          const double wy0 = r[WYo + clampw(oy + cy0, P)], wy2 = r[WYo + clampw(oy + cy0 + 2, P)];
+          v[h] = wy0 * fma(wx0, t0[2 * h], wx1 * t0[2 * h + 1]) + wy2 * fma(wx0, t1[2 * h], wx1 * t1[2 * h + 1]);
         }
-        if (gid == 0) {
-          const int pa = ea.x & 0xff, pb = eb.x & 0xff;
-          if (pa < BM) acc[(b * BM + pa) * (kCW + 1) + w] = va;
-          if (pb < BM) acc[(b * BM + pb) * (kCW + 1) + w] = vb;
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 2);
+        if (tig == 0) {
+          const int pa = e0.x & 0xff, pb = e1.x & 0xff;
+          if (pa < BM) acc[(b * BM + pa) * (kCW + 1) + w] = v[0];
+          if (pb < BM) acc[(b * BM + pb) * (kCW + 1) + w] = v[1];
         }
       }
       __threadfence_block();
@@ -413,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   }
 
   if (!GATHER) {
+    const int cx = gid & 3, cy = gid >> 2;
 #pragma unroll
     for (int zb = 0; zb < NZB; ++zb)
 #pragma unroll
@@ -519,7 +533,7 @@ void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
   SE1P_LAUNCH_CHECK();
 }
 
-template <int TZ, bool GATHER>
+template <int TZ, bool GATHER, bool WRAP2>
 static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
   TileArgs a;
   a.dv = pl.dv;
@@ -549,22 +563,30 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) 
   a.BM = BM;
   a.NB = NB;
   const size_t smem = (size_t)tile_smem(BM, NB, a.RS, GATHER).total;
-  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER, WRAP2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const unsigned nblk = (unsigned)(ntx * a.nty * a.ntz);
-  k_tiles<TZ, GATHER><<<nblk, kThreads, smem, st>>>(a);
+  k_tiles<TZ, GATHER, WRAP2><<<nblk, kThreads, smem, st>>>(a);
   SE1P_LAUNCH_CHECK();
 }
 
-void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
-  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, false>(pl, w, N, st);
-  else launch_tiles<16, false>(pl, w, N, st);
+// WRAP2: a stencil can meet a z tile twice (both ends of the periodic axis) iff TZ + P > M.
+template <bool GATHER>
+static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
+  const int TZ = tile_tz(pl.dv.M);
+  const bool wrap2 = TZ + pl.dv.P > pl.dv.M;
+  if (TZ == 32) {
+    if (wrap2) launch_tiles<32, GATHER, true>(pl, w, N, st);
+    else launch_tiles<32, GATHER, false>(pl, w, N, st);
+  } else {
+    if (wrap2) launch_tiles<16, GATHER, true>(pl, w, N, st);
+    else launch_tiles<16, GATHER, false>(pl, w, N, st);
+  }
 }
 
-void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
-  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, true>(pl, w, N, st);
-  else launch_tiles<16, true>(pl, w, N, st);
-}
+void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) { dispatch_tiles<false>(pl, w, N, st); }
+
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) { dispatch_tiles<true>(pl, w, N, st); }
 
 void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st) {
   KDev dv = pl.dv;
