@@ -4,8 +4,9 @@
 
 A step is one pass of the whole k-space hot path (bin/sort, gridding, z-FFT,
 mode stage, inverse z-FFT, gather) over the config's synthetic system with the inputs resident
-in HBM.  value = particles/s over all ranks.  Multi-GPU (torchrun): each rank evaluates its own
-independent system of the config (replicas, no data-path collective yet) -> "scaling": "weak".
+in HBM.  value = particles of the system / time.  Multi-GPU (torchrun): ONE system sharded over
+the ranks (paper_1611_09538_b200/dist.py: x slabs, k3 modes owned by ranks, two all-to-all
+transposes and an all-reduce over NCCL) -> "scaling": "strong"; time = max over ranks.
 The CPU oracle (oracle/) is timed beside it on a bounded sample (cpu_baseline), and
 --impl reference times the oracle as the reference arm.
 """
@@ -113,13 +114,14 @@ class ClockSampler:
 def bench_ours(args, cfg, rank, world, local):
     import torch
     import paper_1611_09538_b200 as se1p
+    from paper_1611_09538_b200 import dist as sdist
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    x_np, q_np = make_system(cfg.N, cfg.L, cfg.seed + 1000 * rank)
+    x_np, q_np = make_system(cfg.N, cfg.L, cfg.seed)        # the same system on every rank
     x = torch.from_numpy(x_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
     phi = torch.empty(cfg.N, dtype=torch.float64, device=dev)
@@ -127,19 +129,30 @@ def bench_ours(args, cfg, rank, world, local):
     kw = kspace_kwargs(cfg)
     info = se1p.plan_info(cfg.L, cfg.xi, cfg.M, cfg.P, **kw)
 
-    def step(out=phi):
-        se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=out, stream=stream, sync=False, skip_checks=True, **kw)
+    def step(xs=x, qs=q):
+        if world > 1:
+            return sdist.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, stream=stream, **kw)
+        se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, sync=False, skip_checks=True, **kw)
+        return phi
 
     se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, **kw)   # plan + workspace, validated inputs
     for _ in range(args.warmup):
         step()
-    launches_per_step = se1p.launch_count()
+    launches_per_step = se1p.launch_count() if world == 1 else None
     torch.cuda.synchronize(dev)
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+
+    def max_over_ranks(v):
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([v], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return v
 
     clk = ClockSampler(local)
     barrier()
@@ -154,37 +167,30 @@ def bench_ours(args, cfg, rank, world, local):
     torch.cuda.synchronize(dev)
     barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # per-stage device times (separate profiled pass; events on the launching stream)
-    stage_sum = {}
-    nprof = max(3, min(args.steps, 10))
-    for _ in range(nprof):
-        se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, skip_checks=True, profile=True, **kw)
-        for k, v in se1p.stage_times().items():
-            stage_sum[k] = stage_sum.get(k, 0.0) + v / nprof
-
-    # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
-    xh = torch.from_numpy(x_np).pin_memory().numpy()
-    qh = torch.from_numpy(q_np).pin_memory().numpy()
-    ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory().numpy()
-    se1p.kspace(xh, qh, cfg.L, cfg.xi, cfg.M, cfg.P, out=ph, **kw)
-    barrier()
-    t0 = time.perf_counter()
+    # end-to-end through the public API: pinned host x, q -> device, the step, phi -> host
+    xh = torch.from_numpy(x_np).pin_memory()
+    qh = torch.from_numpy(q_np).pin_memory()
+    ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
     ke = max(3, args.steps // 2)
+
+    def e2e_step():
+        xd = xh.to(dev, non_blocking=True)
+        qd = qh.to(dev, non_blocking=True)
+        ph.copy_(step(xd, qd), non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
     for _ in range(ke):
-        se1p.kspace(xh, qh, cfg.L, cfg.xi, cfg.M, cfg.P, out=ph, skip_checks=True, **kw)
-    e2e_s = (time.perf_counter() - t0) / ke
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_s = max_over_ranks(f0.elapsed_time(f1) / ke) * 1e-3
 
     if world > 1:
         import torch.distributed as dist
@@ -192,13 +198,24 @@ def bench_ours(args, cfg, rank, world, local):
     if rank != 0:
         return None
 
+    # per-stage device times (separate profiled single-GPU passes; events on the launching stream)
+    stage_sum = {}
+    nprof = max(3, min(args.steps, 10))
+    for _ in range(nprof):
+        se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, skip_checks=True, profile=True, **kw)
+        for k, v in se1p.stage_times().items():
+            stage_sum[k] = stage_sum.get(k, 0.0) + v / nprof
+    if launches_per_step is None:
+        launches_per_step = se1p.launch_count()
+
     spread_ms = stage_sum.get("spread", float("nan"))
     gather_ms = stage_sum.get("gather", float("nan"))
     dom_name, dom_ms = ("gather", gather_ms) if gather_ms >= spread_ms else ("spread", spread_ms)
     flops = kspace_flops_spread(cfg)          # gather: the same N P^3 FMAs
     achieved = flops / (dom_ms * 1e-3) / 1e12
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
-    value = world * cfg.N / (ms * 1e-3)
+    traffic = kernel_traffic(dom_name)
+    value = cfg.N / (ms * 1e-3)
     line = {
         "metric": "SE1P k-space particles/sec (fp64)",
         "value": value,
@@ -208,29 +225,42 @@ def bench_ours(args, cfg, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded uniform neutral charges, se1p_synth.py)",
         "config": {"workload": f"{cfg.name}: N={cfg.N} L={list(cfg.L)} xi={cfg.xi} M={cfg.M} P={cfg.P} "
                                f"n_l={info['n_local']} S0={info['S0']} SI={info['SI']} Ntilde={info['Ntilde']} "
                                f"LK={info['LK']}",
-                   "N": cfg.N, "global_particles": world * cfg.N,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "per-step working set %.0f MB (grid, planes, 2D workspace) > 126 MB L2; no flush"
-                         % (info["workspace_bytes"] / 1e6 + 40 * cfg.N / 1e6)},
+                   "N": cfg.N,
+                   "parallelism": f"mode-sharded x{world} (x slabs + k3 planes, 2 all-to-all + all-reduce)"
+                                  if world > 1 else "single GPU",
+                   "l2": "per-step working set %.0f MB (particle records, grid, planes) > 126 MB L2; no flush"
+                         % (info["workspace_bytes"] / 1e6 + 700 * cfg.N / 1e6)},
         "stages_ms": stage_sum,
-        "roofline": {"bound": "alu", "kernel": dom_name, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                     "note": "FP64 FMA pipe: 2 N P^3 algorithmic flops per launch / avg launch time; peak = "
-                             "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured DMMA 37.1, DFMA 34.2 TFLOP/s)"},
+        "roofline": {"bound": "alu", "kernel": f"k_tiles ({dom_name})", "achieved": achieved,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": traffic,
+                     "note": "FP64 pipe (DMMA): 2 N P^3 algorithmic flops per launch / CUDA-event launch time on "
+                             "the launching stream; peak = 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md; "
+                             "measured DMMA 37.1, DFMA 34.2 TFLOP/s). traffic = ncu dram read+write bytes per "
+                             "launch from profiles/ (null if not captured for this kernel)"},
         "hbm_gbs_peak": peaks.get("hbm_gbs"),
-        "e2e": {"value": world * cfg.N / e2e_s, "unit": "particles/s",
-                "h2d_bytes_per_step": 32 * cfg.N, "d2h_bytes_per_step": 8 * cfg.N},
+        "e2e": {"value": cfg.N / e2e_s, "unit": "particles/s",
+                "h2d_bytes_per_step": 32 * cfg.N * world, "d2h_bytes_per_step": 8 * cfg.N * world},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
     return line
+
+
+def kernel_traffic(which):
+    """dram bytes per launch of the dominant tile kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(path)).get(which)
+    except (OSError, ValueError):
+        return None
 
 
 def bench_reference(args, cfg, rank):

@@ -99,6 +99,51 @@ int se1p_kspace_ex(const se1p_opts* opts, void* stream, const double* x, const d
                    int64_t N, const double L[3], double xi, int M, int P, double eta,
                    double s0, double sf, int n_local, double* phi_out);
 
+/* ---------------------------------------------------------------------------------------
+ * Mode-sharded k-space over R ranks.  One rank per GPU;
+ * the caller moves the plane buffers between ranks (all-to-all) and sums phi_partial (all-reduce).
+ * Every rank holds the full x, q (device pointers).  The free axis x of the extended grid
+ * (M~ = M_free + P rows) is cut into R slabs [slab_lo[r], slab_lo[r+1]), bounds multiples of 16
+ * (the last may be M~); the M/2+1 k3 planes (Hermitian half, reading R-7) are owned by ranks.
+ *
+ * Plane buffers hold complex doubles (re, im pairs):
+ *   slab buffer   (forward output / backward input) of rank r: [M/2+1 slots][W_r][M~], W_r the slab
+ *                 width; slot i holds plane plane_order[i].  With plane_order grouping the planes
+ *                 by owner (rank 0's planes first), the chunk for owner r' is contiguous.
+ *   split buffer  (se1p_kspace_modes) of an owner with n_own planes: the concatenation over source
+ *                 slabs r of [n_own][W_r][M~] -- exactly what an all-to-all of the slab buffers
+ *                 delivers; the mode stage runs in place and the same all-to-all in reverse
+ *                 returns every rank its slab buffer.
+ *
+ * se1p_kspace_slab_forward: Alg. 1 steps 2-3a (AFT step 1 P:749) restricted to the slab:
+ *   bins and sorts all N particles, grids the slab's x rows (output-stationary tiles, so no
+ *   reduction between ranks) and transforms them along z.  planes_out: slab buffer (caller owned).
+ * se1p_kspace_modes: Alg. 2 steps 2-4, the scaling of Alg. 1 step 4 and Alg. 3 steps 1-3
+ *    for the n_own planes plane_ids[] (global k3 indices 0..M/2) held in the
+ *   split buffer `planes` described by nslab, slab_lo[0..nslab] (slab_lo[0] = 0, slab_lo[nslab] = M~).
+ * se1p_kspace_slab_backward: Alg. 3 steps 4-5 for the slab rows and the gather
+ *   (Alg. 1 step 6) over the slab's tiles: phi_partial[n] (user order, N doubles) is the
+ *   slab's share of phi^F at particle n; the sum over all slabs is se1p_kspace's result.  Uses the
+ *   particle state of the last se1p_kspace_slab_forward on this device with the same N and
+ *   parameters (SE1P_EINVAL otherwise).
+ * An empty slab (x_lo == x_hi) is allowed; its buffers may then be NULL.
+ * All three are stream-ordered like the _ex entries (opts->sync), take device pointers only
+ * (opts->host_io is rejected) and share the device's workspace: issue them on one stream.
+ * --------------------------------------------------------------------------------------- */
+int se1p_kspace_slab_forward(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                             int64_t N, const double L[3], double xi, int M, int P, double eta,
+                             double s0, double sf, int n_local, int x_lo, int x_hi,
+                             const int* plane_order, void* planes_out);
+
+int se1p_kspace_modes(const se1p_opts* opts, void* stream, const double L[3], double xi, int M, int P,
+                      double eta, double s0, double sf, int n_local, int n_own, const int* plane_ids,
+                      int nslab, const int* slab_lo, void* planes);
+
+int se1p_kspace_slab_backward(const se1p_opts* opts, void* stream, int64_t N, const double L[3],
+                              double xi, int M, int P, double eta, double s0, double sf, int n_local,
+                              int x_lo, int x_hi, const int* plane_order, const void* planes_in,
+                              double* phi_partial);
+
 /* Real-space erfc sum truncated at |x_m - x_n + alpha L3 e3| <= rc over z-images alpha
    (Eq. (3); truncation P:120; cell lists P:161-162) plus the self term
    -2 xi q_m/sqrt(pi) (Eq. (6)).  Any rc > 0 (all images within rc are included). */

@@ -24,7 +24,8 @@ LIB_PATH = _build.OUT
 STATUS = {0: "OK", 1: "EINVAL", 2: "EDOMAIN", 3: "ENONNEUTRAL", 4: "EPARAM", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query",
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
-           "se1p_version", "se1p_debug_copy"]
+           "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
+           "se1p_kspace_slab_backward"]
 
 
 class SE1PError(RuntimeError):
@@ -73,7 +74,14 @@ def load(build_if_needed: bool = True):
     lib.se1p_version.restype = ctypes.c_char_p
     lib.se1p_debug_copy.argtypes = [i32, vp, i64]
     lib.se1p_debug_copy.restype = i32
-    for f in ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query", "se1p_last_stage_times"]:
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib.se1p_kspace_slab_forward.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32,
+                                             i32, i32, ip, vp]
+    lib.se1p_kspace_modes.argtypes = [ctypes.POINTER(Opts), vp, vp, d, i32, i32, d, d, d, i32, i32, ip, i32, ip, vp]
+    lib.se1p_kspace_slab_backward.argtypes = [ctypes.POINTER(Opts), vp, i64, vp, d, i32, i32, d, d, d, i32, i32, i32,
+                                              ip, vp, vp]
+    for f in ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query", "se1p_last_stage_times",
+              "se1p_kspace_slab_forward", "se1p_kspace_modes", "se1p_kspace_slab_backward"]:
         getattr(lib, f).restype = i32
     _lib = lib
     return lib
@@ -172,6 +180,60 @@ def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False):
 def potential(x, q, L, xi, rc, M, P, **kw):
     """Full singly periodic potential phi = phi^F + phi^R + phi^self (Eq. (2))."""
     return kspace(x, q, L, xi, M, P, **kw) + real(x, q, L, xi, rc)
+
+
+def _ints(v):
+    v = [int(a) for a in v]
+    return (ctypes.c_int * max(1, len(v)))(*v)
+
+
+def slab_forward(x, q, L, xi, M, P, x_lo, x_hi, plane_order, out=None, stream=None, sync=False,
+                 skip_checks=False, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None):
+    """Distributed path, rank stage 1 (include/se1p.h): grid the slab rows [x_lo, x_hi) and
+    z-transform them.  Returns the slab buffer, float64 [M/2+1, x_hi-x_lo, M~, 2] (re, im)."""
+    import torch
+    lib = load()
+    xp, qp, N, host, keep = _args(x, q)
+    if host:
+        raise TypeError("the distributed entries take CUDA tensors")
+    n_planes = int(M) // 2 + 1
+    info = plan_info(L, xi, M, P, eta=eta, s0=s0, sf=sf, n_local=n_local, Ntilde=Ntilde, S0=S0, SI=SI)
+    if out is None:
+        out = torch.empty((n_planes, x_hi - x_lo, info["Mt"], 2), dtype=torch.float64, device=x.device)
+    o = _opts(Ntilde, S0, SI, False, skip_checks, sync)
+    _check(lib.se1p_kspace_slab_forward(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
+                                        int(M), int(P), _neg(eta, 0.0), _neg(s0), _neg(sf),
+                                        -1 if n_local is None else int(n_local), int(x_lo), int(x_hi),
+                                        _ints(plane_order), out.data_ptr()))
+    return out
+
+
+def modes(planes, L, xi, M, P, plane_ids, slab_lo, stream=None, sync=False, eta=None, s0=None, sf=None,
+          n_local=None, Ntilde=None, S0=None, SI=None):
+    """Distributed path, rank stage 2: the mode stage on the owner's split buffer (in place)."""
+    lib = load()
+    o = _opts(Ntilde, S0, SI, False, False, sync)
+    _check(lib.se1p_kspace_modes(ctypes.byref(o), _stream_ptr(stream, planes), _Larr(L), float(xi), int(M), int(P),
+                                 _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local),
+                                 len(plane_ids), _ints(plane_ids), len(slab_lo) - 1, _ints(slab_lo),
+                                 planes.data_ptr()))
+    return planes
+
+
+def slab_backward(planes, N, L, xi, M, P, x_lo, x_hi, plane_order, out=None, stream=None, sync=False, eta=None,
+                  s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None):
+    """Distributed path, rank stage 3: inverse z-transform of the slab rows and the gather over the
+    slab's tiles.  Returns phi_partial [N] (user order)."""
+    import torch
+    lib = load()
+    if out is None:
+        out = torch.empty(int(N), dtype=torch.float64, device=planes.device)
+    o = _opts(Ntilde, S0, SI, False, False, sync)
+    _check(lib.se1p_kspace_slab_backward(ctypes.byref(o), _stream_ptr(stream, planes), int(N), _Larr(L), float(xi),
+                                         int(M), int(P), _neg(eta, 0.0), _neg(s0), _neg(sf),
+                                         -1 if n_local is None else int(n_local), int(x_lo), int(x_hi),
+                                         _ints(plane_order), planes.data_ptr(), out.data_ptr()))
+    return out
 
 
 def plan_info(L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None):

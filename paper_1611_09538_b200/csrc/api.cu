@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/se1p.h"
 #include "kspace.cuh"
@@ -25,6 +26,10 @@ void count_launch() { ++g_launches; }
 
 struct DevState {
   KWork w;
+  KParams fwd_prm{};           // last se1p_kspace_slab_forward (state the backward relies on)
+  int64_t fwd_N = -1;
+  int* dmap = nullptr;          // device copies of plane maps (distributed path)
+  int64_t dmap_cap = 0;
   double* dx = nullptr;   // host_io staging (device side)
   double* dq = nullptr;
   double* dphi = nullptr;
@@ -253,11 +258,6 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
     grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
     grow(w.rec, w.cap_rec, N * (int64_t)rec_stride(dv.P));
   }
-  w.prof_on = o && o->reserved[3] == 1;       // phase counters of the tile kernels
-  if (w.prof_on) {
-    if (!w.prof) SE1P_CUDA_TRY(cudaMalloc(&w.prof, 32 * sizeof(unsigned long long)));
-    SE1P_CUDA_TRY(cudaMemsetAsync(w.prof, 0, 32 * sizeof(unsigned long long), st));
-  }
   // stages (se1p_last_stage_times): bin, records, spread, zfft, modes, izfft, gather, finish
   tm.mark();
   k_bin_particles(*pl, w, dx, dq, N, st);
@@ -268,13 +268,14 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   else k_spread_tiles(*pl, w, N, st);
   tm.mark();
   if (stop == 1) return sync_and_check(st);
-  k_zfft_forward(*pl, w, st);
+  const SlabLayout L1 = single_layout(dv.Mt, pl->n_planes);
+  k_zfft_forward(*pl, w, w.planes, L1, nullptr, st);
   tm.mark();
   if (stop == 2) return sync_and_check(st);
-  k_mode_stage(*pl, w, st);
+  k_mode_stage(*pl, w, w.planes, L1, nullptr, nullptr, 0, nullptr, nullptr, 0, st);
   tm.mark();
   if (stop == 3) return sync_and_check(st);
-  k_zfft_inverse(*pl, w, st);
+  k_zfft_inverse(*pl, w, w.planes, L1, nullptr, st);
   tm.mark();
   if (stop == 4) return sync_and_check(st);
   if (v1) k_gather(*pl, w, N, dphi, st);
@@ -318,6 +319,143 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   if (!o || o->sync || host_io) SE1P_CUDA_TRY(cudaStreamSynchronize(st));
   SE1P_CUDA_TRY(cudaGetLastError());
+}
+
+
+// ------------------------------------------------------------------ distributed path
+static void check_slab(const KPlan& pl, int x_lo, int x_hi) {
+  const int Mt = pl.dv.Mt;
+  if (x_lo < 0 || x_hi > Mt || x_lo > x_hi || (x_lo % 16 && x_lo != Mt) || (x_hi % 16 && x_hi != Mt))
+    throw Error{1, "slab bounds must satisfy 0 <= x_lo <= x_hi <= M~, multiples of 16 or M~"};
+}
+
+static std::vector<int> check_order(const KPlan& pl, const int* plane_order) {
+  if (!plane_order) throw Error{1, "null plane_order"};
+  std::vector<int> slot(pl.n_planes, -1);
+  for (int i = 0; i < pl.n_planes; ++i) {
+    const int n = plane_order[i];
+    if (n < 0 || n >= pl.n_planes || slot[n] >= 0) throw Error{1, "plane_order must be a permutation of 0..M/2"};
+    slot[n] = i;
+  }
+  return slot;
+}
+
+static int* upload_ints(DevState& ds, const std::vector<int>& v, cudaStream_t st) {
+  grow(ds.dmap, ds.dmap_cap, (int64_t)v.size());
+  SE1P_CUDA_TRY(cudaMemcpyAsync(ds.dmap, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, st));
+  return ds.dmap;
+}
+
+static void finish_call(const se1p_opts* o, KWork& w, cudaStream_t st) {
+  if (!o || o->sync) {
+    SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+    int kerr = 0;
+    SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+  }
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
+static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
+                              const double L[3], double xi, int M, int P, double eta, double s0, double sf,
+                              int n_local, int x_lo, int x_hi, const int* plane_order, void* planes_out) {
+  if (!x || !q || (!planes_out && x_hi > x_lo)) throw Error{1, "null pointer"};
+  if (o && o->host_io) throw Error{1, "the distributed entries take device pointers only"};
+  if (N < 1 || N > (int64_t)2000000000) throw Error{1, "N out of range"};
+  const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  KPlan* pl = kplan_get(prm, st);
+  check_slab(*pl, x_lo, x_hi);
+  const std::vector<int> slot = check_order(*pl, plane_order);
+  DevState& ds = dev_state();
+  KWork& w = ds.w;
+  const KDev& dv = pl->dv;
+  ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
+  grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
+  grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+  grow(w.rec, w.cap_rec, N * (int64_t)rec_stride(dv.P));
+  if (!(o && o->skip_checks)) check_inputs(w, x, q, N, L, true, st);
+  SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
+  k_bin_particles(*pl, w, x, q, N, st);
+  k_records_stage(*pl, w, N, st);
+  k_spread_tiles(*pl, w, N, st, x_lo / 16, (int)ceil_div(x_hi, 16));
+  SlabLayout Ls{};
+  Ls.nslab = 1;
+  Ls.nloc = pl->n_planes;
+  Ls.xlo[0] = x_lo;
+  Ls.xlo[1] = x_hi;
+  k_zfft_forward(*pl, w, (double2*)planes_out, Ls, upload_ints(ds, slot, st), st);
+  ds.fwd_prm = prm;
+  ds.fwd_N = N;
+  finish_call(o, w, st);
+}
+
+static void modes_impl(const se1p_opts* o, cudaStream_t st, const double L[3], double xi, int M, int P, double eta,
+                       double s0, double sf, int n_local, int n_own, const int* plane_ids, int nslab,
+                       const int* slab_lo, void* planes) {
+  const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  KPlan* pl = kplan_get(prm, st);
+  const int Mt = pl->dv.Mt;
+  if (n_own < 0 || n_own > pl->n_planes || (n_own > 0 && (!plane_ids || !planes)))
+    throw Error{1, "bad plane list"};
+  if (nslab < 1 || nslab > kMaxSlabs || !slab_lo || slab_lo[0] != 0 || slab_lo[nslab] != Mt)
+    throw Error{1, "slab_lo must hold nslab+1 increasing bounds from 0 to M~ (nslab <= 16)"};
+  SlabLayout Ls{};
+  Ls.nslab = nslab;
+  Ls.nloc = n_own;
+  for (int r = 0; r <= nslab; ++r) {
+    if (r && slab_lo[r] < slab_lo[r - 1]) throw Error{1, "slab bounds must be non-decreasing"};
+    Ls.xlo[r] = slab_lo[r];
+  }
+  std::vector<int> seen(pl->n_planes, 0), maps;   // glK liK glJ liJ
+  std::vector<int> glK, liK, glJ, liJ;
+  for (int i = 0; i < n_own; ++i) {
+    const int n = plane_ids[i];
+    if (n < 0 || n >= pl->n_planes || seen[n]++) throw Error{1, "plane_ids must be distinct planes in 0..M/2"};
+    if (n < pl->n_kernel) {
+      glK.push_back(n);
+      liK.push_back(i);
+    } else {
+      glJ.push_back(n);
+      liJ.push_back(i);
+    }
+  }
+  if (n_own == 0) return;
+  maps.insert(maps.end(), glK.begin(), glK.end());
+  maps.insert(maps.end(), liK.begin(), liK.end());
+  maps.insert(maps.end(), glJ.begin(), glJ.end());
+  maps.insert(maps.end(), liJ.begin(), liJ.end());
+  DevState& ds = dev_state();
+  KWork& w = ds.w;
+  grow(w.T, w.T_cap, pl->t_off_total);
+  if (!w.flag) ensure_particles(w, 1, 1);
+  int* d = upload_ints(ds, maps, st);
+  const int nK = (int)glK.size(), nJ = (int)glJ.size();
+  k_mode_stage(*pl, w, (double2*)planes, Ls, d, d + nK, nK, d + 2 * nK, d + 2 * nK + nJ, nJ, st);
+  finish_call(o, w, st);
+}
+
+static void slab_backward_impl(const se1p_opts* o, cudaStream_t st, int64_t N, const double L[3], double xi, int M,
+                               int P, double eta, double s0, double sf, int n_local, int x_lo, int x_hi,
+                               const int* plane_order, const void* planes_in, double* phi_partial) {
+  if (!phi_partial || (!planes_in && x_hi > x_lo)) throw Error{1, "null pointer"};
+  const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  DevState& ds = dev_state();
+  if (!(ds.fwd_N == N && ds.fwd_prm == prm))
+    throw Error{1, "se1p_kspace_slab_backward needs the particle state of a matching se1p_kspace_slab_forward "
+                   "on this device (same N and parameters)"};
+  KPlan* pl = kplan_get(prm, st);
+  check_slab(*pl, x_lo, x_hi);
+  const std::vector<int> slot = check_order(*pl, plane_order);
+  KWork& w = ds.w;
+  SlabLayout Ls{};
+  Ls.nslab = 1;
+  Ls.nloc = pl->n_planes;
+  Ls.xlo[0] = x_lo;
+  Ls.xlo[1] = x_hi;
+  k_zfft_inverse(*pl, w, (const double2*)planes_in, Ls, upload_ints(ds, slot, st), st);
+  k_gather_tiles(*pl, w, N, st, x_lo / 16, (int)ceil_div(x_hi, 16));
+  k_gather_finish_stage(*pl, w, N, phi_partial, st, x_lo / 16, (int)ceil_div(x_hi, 16));
+  finish_call(o, w, st);
 }
 
 template <typename F>
@@ -378,6 +516,38 @@ int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const dou
   });
 }
 
+int se1p_kspace_slab_forward(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                             const double L[3], double xi, int M, int P, double eta, double s0, double sf,
+                             int n_local, int x_lo, int x_hi, const int* plane_order, void* planes_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    slab_forward_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, s0, sf, n_local, x_lo, x_hi, plane_order,
+                      planes_out);
+  });
+}
+
+int se1p_kspace_modes(const se1p_opts* opts, void* stream, const double L[3], double xi, int M, int P, double eta,
+                      double s0, double sf, int n_local, int n_own, const int* plane_ids, int nslab,
+                      const int* slab_lo, void* planes) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    modes_impl(&o, (cudaStream_t)stream, L, xi, M, P, eta, s0, sf, n_local, n_own, plane_ids, nslab, slab_lo, planes);
+  });
+}
+
+int se1p_kspace_slab_backward(const se1p_opts* opts, void* stream, int64_t N, const double L[3], double xi, int M,
+                              int P, double eta, double s0, double sf, int n_local, int x_lo, int x_hi,
+                              const int* plane_order, const void* planes_in, double* phi_partial) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    slab_backward_impl(&o, (cudaStream_t)stream, N, L, xi, M, P, eta, s0, sf, n_local, x_lo, x_hi, plane_order,
+                       planes_in, phi_partial);
+  });
+}
+
 int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P, double eta, double s0,
                     double sf, int n_local, se1p_plan_info* info) {
   return guarded([&] {
@@ -425,7 +595,7 @@ void se1p_release(void) {
   KWork& w = ds.w;
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
-                  (void*)w.gpart})
+                  (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap})
     if (p) cudaFree(p);
   ds = DevState{};
 }

@@ -11,6 +11,32 @@ constexpr int kTX = 8, kTY = 8, kTZ = 16;
 // Particle bins: xy columns of kBin x kBin cells, z-sorted by cell inside a column.
 constexpr int kBin = 4;
 
+// Layout of a k3-plane buffer: rows x in [xlo[0], xlo[nslab]) split into
+// nslab consecutive x slabs; slab r holds, for each of the nloc plane slots i, its rows
+// xlo[r] .. xlo[r+1]-1.  Element (i, x, y) lives at slab_row(L, i, x, Mt) + y:
+//   ((nloc (xlo[r] - xlo[0]) + i (xlo[r+1] - xlo[r]) + x - xlo[r]) Mt + y).
+// Single GPU: nslab = 1, xlo = {0, Mt}, nloc = M/2+1 -> the plain [plane][x][y] array.
+constexpr int kMaxSlabs = 16;
+struct SlabLayout {
+  int nslab;
+  int nloc;
+  int xlo[kMaxSlabs + 1];
+};
+__host__ __device__ inline int64_t slab_row(const SlabLayout& L, int i, int x, int Mt) {
+  int r = 0;
+  while (r + 1 < L.nslab && x >= L.xlo[r + 1]) ++r;
+  const int W = L.xlo[r + 1] - L.xlo[r];
+  return ((int64_t)L.nloc * (L.xlo[r] - L.xlo[0]) + (int64_t)i * W + (x - L.xlo[r])) * Mt;
+}
+inline SlabLayout single_layout(int Mt, int nloc) {
+  SlabLayout L{};
+  L.nslab = 1;
+  L.nloc = nloc;
+  L.xlo[0] = 0;
+  L.xlo[1] = Mt;
+  return L;
+}
+
 struct KParams {       // everything a k-space plan is keyed on
   double L[3];
   double xi;
@@ -91,15 +117,20 @@ void kplan_release_all();
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
 void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
 void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);   // tiles.cu
-void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);    // DMMA tiles
-void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);
-void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
+// DMMA tile kernels over x tiles [tx_lo, tx_hi) (tx_hi < 0: all), tiles of 16 grid rows
+void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1);
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1);
+void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st, int tx_lo = 0,
+                           int tx_hi = -1);
 int64_t gather_slots(const KDev& dv);
 void slot_geometry(KDev& dv);
 int tile_tz(int M);
-void k_zfft_forward(const KPlan& pl, KWork& w, cudaStream_t st);
-void k_mode_stage(const KPlan& pl, KWork& w, cudaStream_t st);
-void k_zfft_inverse(const KPlan& pl, KWork& w, cudaStream_t st);
+void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
+                    cudaStream_t st);
+void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* glK, const int* liK,
+                  int nK, const int* glJ, const int* liJ, int nJ, cudaStream_t st);
+void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
+                    cudaStream_t st);
 void k_gather(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
 
 }  // namespace se1p

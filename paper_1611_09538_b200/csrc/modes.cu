@@ -22,12 +22,15 @@ static int rows_for(int W) { int r = 98304 / (2 * W * 16); return r < 1 ? 1 : (r
 static int cols_for(int W) { return W > 400 ? 4 : 8; }
 
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
+// Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if
+// null) of the plane buffer in layout L (kspace.cuh, slab_row).
 __global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
-                       const double* __restrict__ grid, double2* __restrict__ planes) {
+                       const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
+                       const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + CB * M;
-  const int x = blockIdx.y, y0 = blockIdx.x * CB;
+  const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   const double* src = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
     const int c = idx / M;
@@ -37,19 +40,20 @@ __global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
   double2* out = fft_rows<-1>(buf, tmp, fz, tw, CB, M, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
-    if (y0 + c < Mt) planes[((int64_t)n * Mt + x) * Mt + y0 + c] = out[c * M + n];
+    if (y0 + c < Mt) planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = out[c * M + n];
   }
 }
 
 __global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
-                       const double2* __restrict__ planes, double* __restrict__ grid) {
+                       const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
+                       const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + CB * M;
-  const int x = blockIdx.y, y0 = blockIdx.x * CB;
+  const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
-    double2 v = (y0 + c < Mt) ? planes[((int64_t)n * Mt + x) * Mt + y0 + c] : make_double2(0.0, 0.0);
+    double2 v = (y0 + c < Mt) ? planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] : make_double2(0.0, 0.0);
     buf[c * M + n] = v;
     if (n > 0 && 2 * n < M) buf[c * M + (M - n)] = make_double2(v.x, -v.y);  // Hermitian half
   }
@@ -63,57 +67,66 @@ __global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
 }
 
 // ------------------------------------------------------------------ 2D passes
-__global__ void k_rowfwd(int Mt, int W, int nfirst, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
-                         const double2* __restrict__ planes, double2* __restrict__ T) {
+// Launched plane blockIdx.y is global plane gl[by] (nfirst + by if null) held in slot li[by]
+// (= its global index if null) of the plane buffer in layout L.
+struct PlaneSel {
+  const int* gl;
+  const int* li;
+  int nfirst;
+  __device__ __forceinline__ int global(int by) const { return gl ? gl[by] : nfirst + by; }
+  __device__ __forceinline__ int slot(int by) const { return li ? li[by] : global(by); }
+};
+
+__global__ void k_rowfwd(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+                         const double2* __restrict__ planes, double2* __restrict__ T, SlabLayout L, PlaneSel S) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + RB * W;
-  const int n = nfirst + blockIdx.y, x0 = blockIdx.x * RB;
+  const int i = S.slot(blockIdx.y), x0 = blockIdx.x * RB;
   const int nr = min(RB, Mt - x0);
-  const double2* src = planes + ((int64_t)n * Mt + x0) * Mt;
-  for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
-    const int r = idx / W, y = idx - r * W;
-    buf[idx] = (r < nr && y < Mt) ? src[r * Mt + y] : make_double2(0.0, 0.0);
+  for (int r = 0; r < RB; ++r) {
+    const double2* src = (r < nr) ? planes + slab_row(L, i, x0 + r, Mt) : nullptr;
+    for (int y = threadIdx.x; y < W; y += blockDim.x)
+      buf[r * W + y] = (src && y < Mt) ? src[y] : make_double2(0.0, 0.0);
   }
   __syncthreads();
   double2* out = fft_rows<-1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
-  double2* dst = T + base + (int64_t)(n - nfirst) * Mt * W + (int64_t)x0 * W;
+  double2* dst = T + base + (int64_t)blockIdx.y * Mt * W + (int64_t)x0 * W;
   for (int idx = threadIdx.x; idx < nr * W; idx += blockDim.x) dst[idx] = out[idx];
 }
 
-__global__ void k_rowinv(int Mt, int W, int nfirst, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
-                         const double2* __restrict__ T, double2* __restrict__ planes) {
+__global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+                         const double2* __restrict__ T, double2* __restrict__ planes, SlabLayout L, PlaneSel S) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + RB * W;
-  const int n = nfirst + blockIdx.y, x0 = blockIdx.x * RB;
+  const int i = S.slot(blockIdx.y), x0 = blockIdx.x * RB;
   const int nr = min(RB, Mt - x0);
-  const double2* src = T + base + (int64_t)(n - nfirst) * Mt * W + (int64_t)x0 * W;
+  const double2* src = T + base + (int64_t)blockIdx.y * Mt * W + (int64_t)x0 * W;
   for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
     const int r = idx / W;
     buf[idx] = (r < nr) ? src[idx] : make_double2(0.0, 0.0);
   }
   __syncthreads();
   double2* out = fft_rows<1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
-  double2* dst = planes + ((int64_t)n * Mt + x0) * Mt;
-  for (int idx = threadIdx.x; idx < nr * Mt; idx += blockDim.x) {
-    const int r = idx / Mt, y = idx - r * Mt;
-    dst[r * Mt + y] = out[r * W + y];
+  for (int r = 0; r < nr; ++r) {
+    double2* dst = planes + slab_row(L, i, x0 + r, Mt);
+    for (int y = threadIdx.x; y < Mt; y += blockDim.x) dst[y] = out[r * W + y];
   }
 }
 
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
-// kernel_class: multiplier = khat[(n - nfirst)][a][y]; else the J-plane scaling.
-__global__ void k_colpass(int Mt, int W, int nfirst, int64_t base, int CB, FftDesc f, const double2* __restrict__ tw,
+// kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
+__global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const double2* __restrict__ tw,
                           double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
-                          const double2* __restrict__ pl) {
+                          const double2* __restrict__ pl, PlaneSel S) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + CB * W;
-  const int n = nfirst + blockIdx.y, y0 = blockIdx.x * CB;
+  const int n = S.global(blockIdx.y), y0 = blockIdx.x * CB;
   const int nc = min(CB, W - y0);
-  double2* Tp = T + base + (int64_t)(n - nfirst) * Mt * W;
+  double2* Tp = T + base + (int64_t)blockIdx.y * Mt * W;
   for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
     const int a = idx / CB, c = idx - a * CB;
     buf[c * W + a] = (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
@@ -127,7 +140,7 @@ __global__ void k_colpass(int Mt, int W, int nfirst, int64_t base, int CB, FftDe
     const int y = min(y0 + c, W - 1);
     double m;
     if (kernel_class) {
-      m = khat[((int64_t)(n - nfirst) * W + a) * W + y];
+      m = khat[((int64_t)n * W + a) * W + y];
     } else {
       m = pn.x * exJ[a] * exJ[y] / (k2J[a] + k2J[y] + pn.y);
     }
@@ -146,26 +159,32 @@ static void set_smem(const void* fn, size_t bytes) {
   SE1P_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-void k_zfft_forward(const KPlan& pl, KWork& w, cudaStream_t st) {
+void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
+                    cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
+  const int rows = L.xlo[L.nslab] - L.xlo[0];
+  if (rows <= 0) return;
   const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
   set_smem((const void*)k_zfwd, smem);
-  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)Mt);
-  k_zfwd<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, w.planes);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
+  k_zfwd<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
   SE1P_LAUNCH_CHECK();
 }
 
-void k_zfft_inverse(const KPlan& pl, KWork& w, cudaStream_t st) {
+void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
+                    cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
+  const int rows = L.xlo[L.nslab] - L.xlo[0];
+  if (rows <= 0) return;
   const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
   set_smem((const void*)k_zinv, smem);
-  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)Mt);
-  k_zinv<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.planes, w.grid);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
+  k_zinv<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
   SE1P_LAUNCH_CHECK();
 }
 
-static void mode_class(const KPlan& pl, KWork& w, int nfirst, int nplanes, int W, const FftDesc& f, int twoff,
-                       int64_t base, int kernel_class, cudaStream_t st) {
+static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, PlaneSel S, int nplanes,
+                       int W, const FftDesc& f, int twoff, int64_t base, int kernel_class, cudaStream_t st) {
   if (nplanes <= 0) return;
   const int Mt = pl.dv.Mt;
   const int RB = rows_for(W), CB = cols_for(W);
@@ -174,22 +193,27 @@ static void mode_class(const KPlan& pl, KWork& w, int nfirst, int nplanes, int W
   set_smem((const void*)k_rowinv, smr);
   set_smem((const void*)k_colpass, smc);
   const double2* tw = pl.d_tw + twoff;
-  k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, nfirst, base, RB, f, tw, w.planes, w.T);
+  k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, base, RB, f, tw, planes, w.T, L, S);
   SE1P_LAUNCH_CHECK();
-  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), 256, smc, st>>>(Mt, W, nfirst, base, CB, f, tw, w.T, kernel_class,
+  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), 256, smc, st>>>(Mt, W, base, CB, f, tw, w.T, kernel_class,
                                                                         pl.d_khat, pl.d_exJ, pl.d_k2J,
-                                                                        (const double2*)pl.d_pl);
+                                                                        (const double2*)pl.d_pl, S);
   SE1P_LAUNCH_CHECK();
-  k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, nfirst, base, RB, f, tw, w.T, w.planes);
+  k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, base, RB, f, tw, w.T, planes, L, S);
   SE1P_LAUNCH_CHECK();
 }
 
-void k_mode_stage(const KPlan& pl, KWork& w, cudaStream_t st) {
+// Kernel planes (k3 = 0 and the I modes, global index < n_kernel) and J planes.  Null maps: all
+// planes, global index = slot.  Otherwise glK/liK (nK entries) and glJ/liJ (nJ entries) are
+// device arrays of global plane indices and their slots in the buffer.
+void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* glK, const int* liK,
+                  int nK, const int* glJ, const int* liJ, int nJ, cudaStream_t st) {
   const int Mt = pl.dv.Mt;
-  // kernel planes 0 .. n_kernel-1 (k3 = 0 and the I modes), then J planes
-  mode_class(pl, w, 0, pl.n_kernel, pl.LK, pl.fK, pl.twK, 0, 1, st);
-  const int64_t baseJ = (int64_t)pl.n_kernel * Mt * pl.LK;
-  mode_class(pl, w, pl.n_kernel, pl.n_planes - pl.n_kernel, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
+  if (!glK) nK = pl.n_kernel;
+  if (!glJ) nJ = pl.n_planes - pl.n_kernel;
+  mode_class(pl, w, planes, L, PlaneSel{glK, liK, 0}, nK, pl.LK, pl.fK, pl.twK, 0, 1, st);
+  const int64_t baseJ = (int64_t)nK * Mt * pl.LK;
+  mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
 }
 
 // ------------------------------------------------------------------ plan-time kernel spectra

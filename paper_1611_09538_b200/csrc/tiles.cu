@@ -39,7 +39,7 @@ struct TileArgs {
   const int* bin_start;
   double* grid;
   double* gpart;
-  int ntz, nty;
+  int ntz, nty, tx_lo;   // launched tiles: tx in [tx_lo, tx_lo + gridDim/(nty ntz))
   int BM, NB, RS;
 };
 
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int tz = blockIdx.x % A.ntz, t2 = blockIdx.x / A.ntz;
-  const int ty = t2 % A.nty, tx = t2 / A.nty;
+  const int ty = t2 % A.nty, tx = A.tx_lo + t2 / A.nty;
   const int X0 = tx * kTXY, Y0 = ty * kTXY, Z0 = tz * TZ;
   const int jmax = min(TZ, M - Z0);
 
@@ -438,9 +438,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
 }
 
 // Sum the per-tile partials of every particle in a fixed order and scatter to user order.
+// Only x tiles in [txlo, txhi) are summed (one slab of the distributed path; all tiles otherwise).
 template <int TZ>
 __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int* __restrict__ perm,
-                                const double* __restrict__ gpart, int64_t N, double* __restrict__ phi) {
+                                const double* __restrict__ gpart, int64_t N, double* __restrict__ phi, int txlo,
+                                int txhi) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= N) return;
   const int4 st = S4[p];
@@ -450,9 +452,12 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   const int nz = zcount(st.w, P, dv.M, TZ);
   const double* g = gpart + p * dv.nslot;
   double s = 0.0;
-  for (int a = 0; a < nx; ++a)
+  const int tx0 = fdiv(st.x, kTXY);
+  for (int a = 0; a < nx; ++a) {
+    if (tx0 + a < txlo || tx0 + a >= txhi) continue;
     for (int b = 0; b < ny; ++b)
       for (int z = 0; z < nz; ++z) s += g[(a * dv.nsxy + b) * dv.nsz + z];
+  }
   phi[perm[p]] = s;
 }
 
@@ -534,7 +539,7 @@ void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
 }
 
 template <int TZ, bool GATHER, bool WRAP2>
-static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
+static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   TileArgs a;
   a.dv = pl.dv;
   KDev& dv = a.dv;
@@ -543,7 +548,9 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) 
   dv.N = N;
   a.ntz = (int)ceil_div(dv.M, TZ);
   a.nty = (int)ceil_div(dv.Mt, kTXY);
-  const int ntx = a.nty;
+  a.tx_lo = tx_lo;
+  const int ntx = tx_hi - tx_lo;
+  if (ntx <= 0) return;
   a.RS = rec_stride(dv.P);
   a.rec = w.rec;
   a.bin_start = w.bin_start;
@@ -572,28 +579,36 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) 
 
 // WRAP2: a stencil can meet a z tile twice (both ends of the periodic axis) iff TZ + P > M.
 template <bool GATHER>
-static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
+static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   const int TZ = tile_tz(pl.dv.M);
   const bool wrap2 = TZ + pl.dv.P > pl.dv.M;
+  if (tx_hi < 0) tx_hi = (int)ceil_div(pl.dv.Mt, kTXY);
   if (TZ == 32) {
-    if (wrap2) launch_tiles<32, GATHER, true>(pl, w, N, st);
-    else launch_tiles<32, GATHER, false>(pl, w, N, st);
+    if (wrap2) launch_tiles<32, GATHER, true>(pl, w, N, tx_lo, tx_hi, st);
+    else launch_tiles<32, GATHER, false>(pl, w, N, tx_lo, tx_hi, st);
   } else {
-    if (wrap2) launch_tiles<16, GATHER, true>(pl, w, N, st);
-    else launch_tiles<16, GATHER, false>(pl, w, N, st);
+    if (wrap2) launch_tiles<16, GATHER, true>(pl, w, N, tx_lo, tx_hi, st);
+    else launch_tiles<16, GATHER, false>(pl, w, N, tx_lo, tx_hi, st);
   }
 }
 
-void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) { dispatch_tiles<false>(pl, w, N, st); }
+void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
+  dispatch_tiles<false>(pl, w, N, tx_lo, tx_hi, st);
+}
 
-void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) { dispatch_tiles<true>(pl, w, N, st); }
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
+  dispatch_tiles<true>(pl, w, N, tx_lo, tx_hi, st);
+}
 
-void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st) {
+void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st, int tx_lo, int tx_hi) {
   KDev dv = pl.dv;
   slot_geometry(dv);
+  if (tx_hi < 0) tx_hi = (int)ceil_div(dv.Mt, kTXY);
   const unsigned nb = (unsigned)ceil_div(N, 256);
-  if (tile_tz(dv.M) == 32) k_gather_finish<32><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi);
-  else k_gather_finish<16><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi);
+  if (tile_tz(dv.M) == 32)
+    k_gather_finish<32><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi, tx_lo, tx_hi);
+  else
+    k_gather_finish<16><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi, tx_lo, tx_hi);
   SE1P_LAUNCH_CHECK();
 }
 

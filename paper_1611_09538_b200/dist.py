@@ -1,0 +1,174 @@
+"""Mode-sharded SE1P k-space over R ranks.
+
+One process per GPU, torch.distributed (NCCL) for the two all-to-all transposes and the final
+all-reduce; every step of the method runs in libse1p's kernels (include/se1p.h, distributed
+entries).  Per rank r:
+
+  1. se1p_kspace_slab_forward: grid the x slab [xlo_r, xlo_{r+1}) of the extended grid
+     (output-stationary tiles: no reduction between ranks) and z-transform it (AFT step 1,
+     P:749) into the slab buffer [M/2+1 slots][W_r][M~], slots ordered by plane owner;
+  2. all-to-all #1: the chunk of owner r' goes to rank r'; rank r receives its owned planes
+     from every slab (the split buffer);
+  3. se1p_kspace_modes on the owned planes (Alg. 2 steps 2-4, scaling, Alg. 3 steps 1-3,
+     P:750-768) -- the k3 modes are independent, which is what shards;
+  4. all-to-all #2 (the reverse) returns every rank its slab buffer;
+  5. se1p_kspace_slab_backward: inverse z-transform and the gather
+     over the slab's tiles -> phi_partial; all-reduce(sum) gives phi^F on every rank.
+
+Plane ownership: greedy longest-processing-time on cost ~ W^2 log2 W per plane (W = the
+plane's transform extent: LK for k3 = 0 and the upsampled I modes, Ntilde otherwise), so the
+expensive upsampled planes spread over ranks.  The index bookkeeping
+(slab bounds, owners, split sizes) is plain Python and is unit-tested on CPU with gloo.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+TILE = 16   # x extent of the gridding/gather tiles: slab bounds are multiples of it
+
+
+def slab_bounds(Mt: int, R: int) -> list:
+    """R+1 x-row bounds 0 = b_0 <= ... <= b_R = Mt, multiples of TILE (b_R = Mt), the
+    ceil(Mt/TILE) tiles split as evenly as possible (lower ranks take the extra ones)."""
+    if R < 1:
+        raise ValueError("R >= 1")
+    nt = (Mt + TILE - 1) // TILE
+    bounds = [0]
+    for r in range(R):
+        cnt = nt // R + (1 if r < nt % R else 0)
+        bounds.append(min(Mt, bounds[-1] + TILE * cnt))
+    bounds[-1] = Mt
+    return bounds
+
+
+def plane_costs(info: dict) -> list:
+    """Relative cost of each of the M/2+1 planes in the mode stage: W^2 log2 W."""
+    n_planes, n_kernel = info["n_planes"], info["n_kernel_planes"]
+    out = []
+    for n in range(n_planes):
+        W = info["LK"] if n < n_kernel else info["Ntilde"]
+        out.append(W * W * math.log2(W))
+    return out
+
+
+def assign_planes(costs: list, R: int) -> list:
+    """LPT: planes in decreasing cost (ties: lower index first) to the least loaded rank (ties:
+    lower rank).  Returns owned[r] = sorted plane indices of rank r."""
+    load = [0.0] * R
+    owned = [[] for _ in range(R)]
+    for n in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(R), key=lambda k: (load[k], k))
+        owned[r].append(n)
+        load[r] += costs[n]
+    return [sorted(o) for o in owned]
+
+
+@dataclasses.dataclass
+class DistPlan:
+    Mt: int
+    n_planes: int
+    R: int
+    bounds: list          # slab bounds (R+1)
+    owned: list           # owned[r]: plane indices
+    order: list           # plane_order: planes grouped by owner, rank 0 first
+
+    def width(self, r):
+        return self.bounds[r + 1] - self.bounds[r]
+
+    def count(self, r):
+        return len(self.owned[r])
+
+    # split sizes in float64 elements (a complex entry is 2 doubles)
+    def splits_to_owners(self, r):
+        """all-to-all #1, rank r: input chunks (to owner r') of its slab buffer."""
+        return [2 * self.count(q) * self.width(r) * self.Mt for q in range(self.R)]
+
+    def splits_from_slabs(self, r):
+        """all-to-all #1, rank r: output chunks (from slab r') of its split buffer."""
+        return [2 * self.count(r) * self.width(q) * self.Mt for q in range(self.R)]
+
+
+def make_plan(info: dict, R: int) -> DistPlan:
+    Mt, n_planes = info["Mt"], info["n_planes"]
+    owned = assign_planes(plane_costs(info), R)
+    order = [n for r in range(R) for n in owned[r]]
+    return DistPlan(Mt, n_planes, R, slab_bounds(Mt, R), owned, order)
+
+
+class CudaBackend:
+    """The product stages: libse1p's distributed entries on this rank's GPU."""
+
+    def __init__(self, L, xi, M, P, stream=None, **kw):
+        self.args = (L, xi, M, P)
+        self.kw = kw
+        self.stream = stream
+
+    def forward(self, x, q, x_lo, x_hi, order):
+        import paper_1611_09538_b200 as se1p
+        return se1p.slab_forward(x, q, *self.args, x_lo, x_hi, order, stream=self.stream, skip_checks=True,
+                                 **self.kw)
+
+    def modes(self, buf, plane_ids, bounds):
+        import paper_1611_09538_b200 as se1p
+        if plane_ids:
+            se1p.modes(buf, *self.args, plane_ids, bounds, stream=self.stream, **self.kw)
+        return buf
+
+    def backward(self, buf, N, x_lo, x_hi, order):
+        import paper_1611_09538_b200 as se1p
+        return se1p.slab_backward(buf, N, *self.args, x_lo, x_hi, order, stream=self.stream, **self.kw)
+
+
+def kspace_rank(x, q, plan: DistPlan, backend, rank: int, group=None):
+    """SPMD body of rank `rank` (torch.distributed initialised; works with nccl and gloo).
+    Returns phi^F (all N particles) on every rank."""
+    import torch
+    import torch.distributed as dist
+    r = rank
+    x_lo, x_hi = plan.bounds[r], plan.bounds[r + 1]
+    N = q.shape[0]
+    slab = backend.forward(x, q, x_lo, x_hi, plan.order)
+    split = torch.empty(2 * plan.count(r) * plan.Mt * plan.Mt, dtype=torch.float64, device=slab.device)
+    dist.all_to_all_single(split, slab.reshape(-1), plan.splits_from_slabs(r), plan.splits_to_owners(r), group=group)
+    backend.modes(split, plan.owned[r], plan.bounds)
+    back = torch.empty_like(slab).reshape(-1)
+    dist.all_to_all_single(back, split, plan.splits_to_owners(r), plan.splits_from_slabs(r), group=group)
+    phi = backend.backward(back.reshape(slab.shape), N, x_lo, x_hi, plan.order)
+    dist.all_reduce(phi, group=group)
+    return phi
+
+
+def kspace_emulated(x, q, plan: DistPlan, backend):
+    """All R ranks of kspace_rank run in turn in one process (the transposes become local copies
+    with the same split sizes).  Used to test the decomposition on one GPU; no kernel waits on
+    another rank."""
+    import torch
+    R, N = plan.R, q.shape[0]
+    slabs = [backend.forward(x, q, plan.bounds[r], plan.bounds[r + 1], plan.order).reshape(-1) for r in range(R)]
+    chunks = [list(torch.split(slabs[r], plan.splits_to_owners(r))) for r in range(R)]
+    splits = [torch.cat([chunks[src][r] for src in range(R)]) for r in range(R)]   # all-to-all #1
+    for r in range(R):
+        backend.modes(splits[r], plan.owned[r], plan.bounds)
+    back = [list(torch.split(splits[r], plan.splits_from_slabs(r))) for r in range(R)]
+    phi = None
+    for r in range(R):
+        buf = torch.cat([back[owner][r] for owner in range(R)])                       # all-to-all #2
+        # the device workspace holds the sorted particle state of the last forward, which is the same
+        # for every rank (same particles and parameters)
+        part = backend.backward(buf.reshape(plan.n_planes, plan.width(r), plan.Mt, 2), N, plan.bounds[r],
+                                plan.bounds[r + 1], plan.order)
+        phi = part.clone() if phi is None else phi + part
+    return phi
+
+
+def kspace(x, q, L, xi, M, P, group=None, stream=None, **kw):
+    """phi^F of one system sharded over the ranks of `group` (default: the world), every rank
+    passing the same x [N,3], q [N] (CUDA, float64) and parameters."""
+    import torch.distributed as dist
+    import paper_1611_09538_b200 as se1p
+    R = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    info = se1p.plan_info(L, xi, M, P, **{k: kw.get(k) for k in ("eta", "s0", "sf", "n_local", "Ntilde", "S0", "SI")})
+    plan = make_plan(info, R)
+    return kspace_rank(x, q, plan, CudaBackend(L, xi, M, P, stream=stream, **kw), rank, group)

@@ -1,0 +1,81 @@
+"""GPU tests of the mode-sharded distributed path's CUDA stages (include/se1p.h distributed
+entries, paper_1611_09538_b200/dist.py).  Only one GPU is available, so R ranks are emulated in
+one process (kspace_emulated: the stages of every rank run in turn, the transposes are local
+copies with the production split sizes -- no kernel waits on another rank), and the real SPMD
+body runs over NCCL with world size 1.  The result must equal the single-GPU path."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import se1p_discrete as sd
+from se1p_synth import CONFIGS, kspace_kwargs, make_system
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1611_09538_b200 as se1p  # noqa: E402
+from paper_1611_09538_b200 import dist as sdist  # noqa: E402
+
+
+def _run(cfgname, R, N=None):
+    c = CONFIGS[cfgname]
+    N = N or c.N
+    x, q = make_system(N, c.L, c.seed)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    kw = kspace_kwargs(c)
+    ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+    info = se1p.plan_info(c.L, c.xi, c.M, c.P, **kw)
+    plan = sdist.make_plan(info, R)
+    phi = sdist.kspace_emulated(xd, qd, plan, sdist.CudaBackend(c.L, c.xi, c.M, c.P, **kw))
+    torch.cuda.synchronize()
+    return ref.cpu().numpy(), phi.cpu().numpy(), x, q
+
+
+@pytest.mark.parametrize("cfg,R", [("C2", 2), ("C2", 3), ("C3", 4), ("C4", 2), ("C4", 8)])
+def test_emulated_ranks_match_single_gpu(cfg, R):
+    ref, phi, _, _ = _run(cfg, R)
+    assert np.max(np.abs(phi - ref)) <= 1e-13 * np.max(np.abs(ref)), (cfg, R)
+
+
+def test_emulated_ranks_match_alg1_oracle():
+    """Small case against the step-by-step Alg. 1 oracle directly (R = 3, one empty slab)."""
+    L, xi, M, P, n_l, S0, SI, SJ = (1.0, 1.0, 1.0), 4.0, 16, 8, 2, 72, 60, 30
+    x, q = make_system(60, L, 5)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    kw = dict(n_local=n_l, S0=S0, SI=SI, Ntilde=SJ)
+    plan = sdist.make_plan(se1p.plan_info(L, xi, M, P, **kw), 3)
+    phi = sdist.kspace_emulated(xd, qd, plan, sdist.CudaBackend(L, xi, M, P, **kw)).cpu().numpy()
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    assert np.max(np.abs(phi - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+
+def test_backward_requires_matching_forward():
+    c = CONFIGS["C2"]
+    kw = kspace_kwargs(c)
+    buf = torch.zeros((c.M // 2 + 1, 16, 52 + 12, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(se1p.SE1PError):
+        se1p.slab_backward(buf, 12345, c.L, c.xi, c.M, c.P, 0, 16, list(range(c.M // 2 + 1)), **kw)
+
+
+def test_nccl_world_one():
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        c = CONFIGS["C3"]
+        x, q = make_system(c.N, c.L, c.seed)
+        xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+        kw = kspace_kwargs(c)
+        phi = sdist.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+        ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+        assert torch.equal(phi, ref)
+    finally:
+        dist.destroy_process_group()
