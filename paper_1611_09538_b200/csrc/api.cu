@@ -377,7 +377,7 @@ static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double*
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   k_bin_particles(*pl, w, x, q, N, st);
   k_records_stage(*pl, w, N, st);
-  k_spread_tiles(*pl, w, N, st, x_lo / 16, (int)ceil_div(x_hi, 16));
+  k_spread_tiles(*pl, w, N, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
   SlabLayout Ls{};
   Ls.nslab = 1;
   Ls.nloc = pl->n_planes;
@@ -453,8 +453,8 @@ static void slab_backward_impl(const se1p_opts* o, cudaStream_t st, int64_t N, c
   Ls.xlo[0] = x_lo;
   Ls.xlo[1] = x_hi;
   k_zfft_inverse(*pl, w, (const double2*)planes_in, Ls, upload_ints(ds, slot, st), st);
-  k_gather_tiles(*pl, w, N, st, x_lo / 16, (int)ceil_div(x_hi, 16));
-  k_gather_finish_stage(*pl, w, N, phi_partial, st, x_lo / 16, (int)ceil_div(x_hi, 16));
+  k_gather_tiles(*pl, w, N, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
+  k_gather_finish_stage(*pl, w, N, phi_partial, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
   finish_call(o, w, st);
 }
 

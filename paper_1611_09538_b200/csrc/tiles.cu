@@ -24,6 +24,7 @@
 // (particle, tile) into a fixed slot and k_gather_finish sums the slots in a fixed order, so
 // results are bitwise reproducible.
 #include <cstdint>
+#include <cstdlib>
 
 #include "tiles.cuh"
 
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     const double* bb = bufs + b * BS;
     // particles of the batch meeting this warp's 4 x 4 column block (order preserving)
     int n = 0;
-    for (int p0 = 0; p0 < cn; p0 += 32) {
+    for (int p0 = 0; p0 < ((dv.dbg & 4) ? 0 : cn); p0 += 32) {
       const int p = p0 + lane;
       bool rel = false;
       int2 e = dummy;
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     if (lane < npad - n) wl[n + lane] = dummy;
     __syncwarp();
 
-    if (!GATHER) {
+    if (dv.dbg & 2) {
+    } else if (!GATHER) {
       // C[16 cols x 8 z] += A[16 cols x 16 particles] B[16 particles x 8 z]; particle of k-slot
       // tig + 4j is list entry k + tig + 4j (A and B agree on it)
       const int cx = gid & 3, cy = gid >> 2;
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
         }
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
-          if ((zm >> zb) & 1) {
+          if (((zm >> zb) & 1) && !(dv.dbg & 1)) {
             const int jz = 8 * zb + gid;
             dmma_16x8x16(c[zb], a, rz[0][zidx(e[0].y, jz)], rz[1][zidx(e[1].y, jz)], rz[2][zidx(e[2].y, jz)],
                          rz[3][zidx(e[3].y, jz)]);
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
         double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
-          if ((zm >> zb) & 1) {
+          if (((zm >> zb) & 1) && !(dv.dbg & 1)) {
             const int j0 = 8 * zb + tig, j1 = j0 + 4;
             const double a[4] = {r0[WZo + zidx(e0.y, j0)], r1[WZo + zidx(e1.y, j0)], r0[WZo + zidx(e0.y, j1)],
                                  r1[WZo + zidx(e1.y, j1)]};
@@ -546,6 +548,10 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   slot_geometry(dv);
   dv.err = w.flag + 1;
   dv.N = N;
+  {
+    const char* e = getenv("SE1P_TILE_DBG");   // experiment bits (tools/tile_experiments.sh); 0 = normal
+    dv.dbg = e ? atoi(e) : 0;
+  }
   a.ntz = (int)ceil_div(dv.M, TZ);
   a.nty = (int)ceil_div(dv.Mt, kTXY);
   a.tx_lo = tx_lo;
