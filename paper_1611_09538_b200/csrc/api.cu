@@ -256,7 +256,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
   if (!v1) {
     grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
-    grow(w.rec, w.cap_rec, N * (int64_t)rec_stride(dv.P));
+    grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
   }
   // stages (se1p_last_stage_times): bin, records, spread, zfft, modes, izfft, gather, finish
   tm.mark();
@@ -372,7 +372,7 @@ static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double*
   ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
   grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
   grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
-  grow(w.rec, w.cap_rec, N * (int64_t)rec_stride(dv.P));
+  grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
   if (!(o && o->skip_checks)) check_inputs(w, x, q, N, L, true, st);
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   k_bin_particles(*pl, w, x, q, N, st);

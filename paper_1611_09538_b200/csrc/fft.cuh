@@ -86,33 +86,55 @@ __device__ __forceinline__ void bfly5(double2* v) {
 }
 
 // ------------------------------------------------------------------ one stage
+// Butterfly j (0 <= j < n/R) of row `row`: inputs j + t n/R, twiddle index k = j mod Ns, outputs
+// (j / Ns) Ns R + k + q Ns.  Threads own a fixed j across rows (when n/R <= nthr) so the index
+// arithmetic and the twiddle loads happen once per stage, not once per butterfly.
+template <int R, int DIR>
+__device__ __forceinline__ void bfly_fixed(double2* v) {
+  if (R == 2) bfly2<DIR>(v);
+  if (R == 3) bfly3<DIR>(v);
+  if (R == 4) bfly4<DIR>(v);
+  if (R == 5) bfly5<DIR>(v);
+}
+
 template <int R, int DIR>
 __device__ __forceinline__ void stage_fixed(const double2* __restrict__ in, double2* __restrict__ out,
                                             int n, int Ns, const double2* __restrict__ tw, int nrows,
                                             int rowstride, int tid, int nthr) {
   const int nb = n / R;
-  const int total = nrows * nb;
-  for (int b = tid; b < total; b += nthr) {
-    const int row = b / nb, j = b - row * nb;
+  int j, row0, rstep, jstep;
+  if (nb <= nthr) {
+    rstep = nthr / nb;
+    if (tid >= rstep * nb) return;
+    j = tid % nb;
+    row0 = tid / nb;
+    jstep = nb;   // one j per thread
+  } else {
+    rstep = 1;
+    j = tid;
+    row0 = 0;
+    jstep = nthr;
+  }
+  for (; j < nb; j += jstep) {
     const int k = j % Ns;
-    const double2* src = in + row * rowstride;
-    double2 v[R];
+    double2 w[R];
 #pragma unroll
-    for (int t = 0; t < R; ++t) v[t] = src[j + t * nb];
-    if (k > 0) {
+    for (int t = 1; t < R; ++t) w[t] = (k > 0) ? tw[k * (R - 1) + t - 1] : make_double2(1.0, 0.0);
+    const int obase = (j / Ns) * Ns * R + k;
+    for (int row = row0; row < nrows; row += rstep) {
+      const double2* src = in + row * rowstride + j;
+      double2 v[R];
 #pragma unroll
-      for (int t = 1; t < R; ++t) {
-        double2 w = tw[k * (R - 1) + t - 1];
-        v[t] = DIR < 0 ? cmul(v[t], w) : cmulc(v[t], w);
+      for (int t = 0; t < R; ++t) v[t] = src[t * nb];
+      if (k > 0) {
+#pragma unroll
+        for (int t = 1; t < R; ++t) v[t] = DIR < 0 ? cmul(v[t], w[t]) : cmulc(v[t], w[t]);
       }
-    }
-    if (R == 2) bfly2<DIR>(v);
-    if (R == 3) bfly3<DIR>(v);
-    if (R == 4) bfly4<DIR>(v);
-    if (R == 5) bfly5<DIR>(v);
-    double2* dst = out + row * rowstride + (j / Ns) * Ns * R + k;
+      bfly_fixed<R, DIR>(v);
+      double2* dst = out + row * rowstride + obase;
 #pragma unroll
-    for (int q = 0; q < R; ++q) dst[q * Ns] = v[q];
+      for (int q = 0; q < R; ++q) dst[q * Ns] = v[q];
+    }
   }
 }
 
@@ -121,31 +143,45 @@ __device__ void stage_generic(const double2* __restrict__ in, double2* __restric
                               int Ns, const double2* __restrict__ tw, const double2* __restrict__ roots,
                               int nrows, int rowstride, int tid, int nthr) {
   const int nb = n / R;
-  const int total = nrows * nb;
-  for (int b = tid; b < total; b += nthr) {
-    const int row = b / nb, j = b - row * nb;
+  int j, row0, rstep, jstep;
+  if (nb <= nthr) {
+    rstep = nthr / nb;
+    if (tid >= rstep * nb) return;
+    j = tid % nb;
+    row0 = tid / nb;
+    jstep = nb;
+  } else {
+    rstep = 1;
+    j = tid;
+    row0 = 0;
+    jstep = nthr;
+  }
+  for (; j < nb; j += jstep) {
     const int k = j % Ns;
-    const double2* src = in + row * rowstride;
-    double2 v[kMaxGenericRadix];
-    for (int t = 0; t < R; ++t) {
-      double2 x = src[j + t * nb];
-      if (k > 0 && t > 0) {
-        double2 w = tw[k * (R - 1) + t - 1];
-        x = DIR < 0 ? cmul(x, w) : cmulc(x, w);
+    const int obase = (j / Ns) * Ns * R + k;
+    for (int row = row0; row < nrows; row += rstep) {
+      const double2* src = in + row * rowstride + j;
+      double2 v[kMaxGenericRadix];
+      for (int t = 0; t < R; ++t) {
+        double2 x = src[t * nb];
+        if (k > 0 && t > 0) {
+          double2 w = tw[k * (R - 1) + t - 1];
+          x = DIR < 0 ? cmul(x, w) : cmulc(x, w);
+        }
+        v[t] = x;
       }
-      v[t] = x;
-    }
-    double2* dst = out + row * rowstride + (j / Ns) * Ns * R + k;
-    for (int q = 0; q < R; ++q) {
-      double2 acc = v[0];
-      int e = 0;
-      for (int t = 1; t < R; ++t) {
-        e += q;
-        if (e >= R) e -= R;
-        double2 w = roots[e];
-        acc = cadd(acc, DIR < 0 ? cmul(v[t], w) : cmulc(v[t], w));
+      double2* dst = out + row * rowstride + obase;
+      for (int q = 0; q < R; ++q) {
+        double2 acc = v[0];
+        int e = 0;
+        for (int t = 1; t < R; ++t) {
+          e += q;
+          if (e >= R) e -= R;
+          double2 w = roots[e];
+          acc = cadd(acc, DIR < 0 ? cmul(v[t], w) : cmulc(v[t], w));
+        }
+        dst[q * Ns] = acc;
       }
-      dst[q * Ns] = acc;
     }
   }
 }

@@ -1,24 +1,28 @@
 // tiles.cu -- gridding (Alg. 1 step 2, Eq. (spread_1p)) and gather (Alg. 1 step 6,
 // Eq. (se1p_complete_discretized)) as output-stationary tile contractions on the
-// FP64 tensor pipe (mma.sync m16n8k8 f64 -> SASS DMMA).  See tiles.cuh.
+// FP64 tensor pipe (mma.sync f64 -> SASS DMMA).  See tiles.cuh.
 //
-// Weights: k_records evaluates every sorted particle's 3 x P one-dimensional window weights
-// e^{-alpha d^2} once per call into a record row (tiles.cuh), so that the P^3 stencil is the
-// outer product of three staged vectors (the separability that Fast Gaussian Gridding, P:807-817,
-// exploits on the CPU).
+// Fast Gaussian Gridding: k_records stores per sorted particle only the stencil
+// starts, q and per axis the two FGG factors A = e^{-alpha d0^2}, E = e^{-2 alpha h d0} (d0 the
+// offset of the first stencil node); the window weight of stencil node t is A E^t f1[t],
+// f1[t] = e^{-alpha h^2 t^2}.  Tiles move these 80-byte records and expand the weights they need
+// in shared memory -- multiplications instead of exponentials.
 //
-// One CTA per tile X0..X0+15 x Y0..Y0+15 x Z0..Z0+TZ-1 (periodic in z), 17 warps:
-//   producer warp: walks the tile's candidate bins (xy columns of 4 x 4 cells, z-sorted) in
-//     z windows of kWinCells cells, columns concatenated inside a window, and moves the records
-//     of each contiguous run with one bulk copy (cp.async.bulk, SASS UBLKCP) into a ring of NB
-//     shared-memory batches of BM rows; completion is signalled by transaction bytes on the
-//     batch's `full` mbarrier.  Gather: it also reduces the finished batches' per-warp partials.
-//   16 consumer warps: warp w owns the 4 x 4 column block (4 (w&3), 4 (w>>2)) over all TZ
-//     nodes; per batch it keeps the particles meeting its block (order preserving) and runs
-//       gridding  C[16 cols x 8 z]        += A[16 cols x 8 particles] B[8 particles x 8 z]
-//                 A = q wx wy (built from the staged rows), B = wz
-//       gather    T[16 cols x 8 particles] = A[16 cols x 8 z] (H~, registers) B[8 z x 8 particles]
-//                 phi_p += sum_cols wx wy T
+// One CTA per tile X0..X0+15 x Y0..Y0+15 x Z0..Z0+TZ-1 (periodic in z), 25 warps:
+//   producer (1 warp): walks the tile's candidate runs (bins: x band of 4 cells, z cell, y cell;
+//     a run = one x band, one z cell, the tile's y range) z-major, 32 runs at a time: a warp scan
+//     places them in the batch stream and every lane moves its run's records with one bulk copy
+//     (cp.async.bulk, SASS UBLKCP) into a ring of NB batches of BM records (mbarrier `raw`,
+//     transaction bytes).  Gather: also reduces finished batches' per-warp partials.
+//   expanders (kEW warps): per batch, the tile windows wx[16], wy[16], wz[TZ] of every particle
+//     (zero outside the stencil, z wraps periodically, gridding folds q into wx) in 16-entry
+//     segments (one FGG recurrence each, started by binary powering of E); then `full`.
+//   consumers (16 warps): warp w owns the 4 x 4 column block (4 (w&3), 4 (w>>2)) over all TZ
+//     nodes; per batch it lists the particles meeting its block (order preserving) and runs
+//       gridding  C[16 cols x 8 z]        += A[16 cols x 16 particles] B[16 particles x 8 z]
+//                 A = (q wx) wy, B = wz                                   (m16n8k16)
+//       gather    T[16 particles x 8 cols] = A[16 particles x 8 z] (wz) B[8 z x 8 cols] (H~)
+//                 per col half, then phi_p += sum_cols wx wy T             (m16n8k8)
 //     skipping 8-node z blocks no particle of the k-step reaches; then arrives on `empty`.
 // No floating-point atomics: gridding writes its tile once; the gather writes one partial per
 // (particle, tile) into a fixed slot and k_gather_finish sums the slots in a fixed order, so
@@ -30,38 +34,53 @@
 
 namespace se1p {
 
-constexpr int kCW = 16;                      // consumer warps
-constexpr int kThreads = (kCW + 1) * 32;     // + 1 producer warp
+constexpr int kCW = 16;                          // consumer warps
+constexpr int kEW = 8;                           // expander warps
+constexpr int kThreads = (kCW + 1 + kEW) * 32;   // + producer
 constexpr int kMaxNB = 4;
+constexpr int kRec = 10;                         // doubles per compact record (80 B)
+constexpr int kMaxP = 64;
+
+// Expanded row: 16-entry window segments wx, wy, wz[0:16), wz[16:32) at offsets 0, 17, 34, 51
+// (17 apart: when 8 particles x 4 segments are written by one warp, the 32 lanes fall into
+// distinct bank pairs); row stride = 4 (mod 16) doubles, so the 4 particles of a consumer
+// k-step start 4 banks apart.
+__host__ __device__ constexpr int exp_stride(int TZ) { return TZ == 32 ? 68 : 52; }
+constexpr int kEX = 0, kEY = 17, kEZ = 34;
+__host__ __device__ constexpr int zoff(int j) { return kEZ + j + (j >= 16 ? 1 : 0); }   // wz[j]
 
 struct TileArgs {
   KDev dv;
-  const double* rec;
+  const double* rec;      // compact records [N][kRec]
   const int* bin_start;
+  const double* f1;
   double* grid;
   double* gpart;
   int ntz, nty, tx_lo;   // launched tiles: tx in [tx_lo, tx_lo + gridDim/(nty ntz))
-  int BM, NB, RS;
+  int BM, NB;
 };
 
 struct TileSmem {
-  int off_pidx, off_lists, off_acc, off_buf, total;
+  int off_pidx, off_lists, off_acc, off_raw, off_exp, total;
 };
 
-__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int RS, bool gather) {
+__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather) {
   TileSmem s;
-  int o = 2 * kMaxNB * 8 + kMaxNB * 4;   // barriers, counts
+  int o = 3 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
   s.off_pidx = o;
   o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
   s.off_lists = o;
-  o += kCW * (BM + 16) * 8;
+  o += kCW * (BM + 16) * 4;
   o = (o + 15) & ~15;
   s.off_acc = o;
   if (gather) o += NB * BM * (kCW + 1) * 8;
   o = (o + 127) & ~127;
-  s.off_buf = o;
-  o += NB * (BM + 1) * RS * 8;
+  s.off_raw = o;
+  o += NB * BM * kRec * 8;
+  o = (o + 127) & ~127;
+  s.off_exp = o;
+  o += NB * (BM + 1) * exp_stride(TZ) * 8;
   s.total = o;
   return s;
 }
@@ -97,7 +116,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-__device__ __forceinline__ int clampw(int t, int P) { return min(max(t, -1), P); }
 // bits of the 8-node z blocks covering tile offsets [lo, hi), hi > lo
 __device__ __forceinline__ int zbits(int lo, int hi) { return ((1 << ((hi + 7) >> 3)) - 1) & ~((1 << (lo >> 3)) - 1); }
 
@@ -127,22 +145,25 @@ __device__ __forceinline__ int zmask_of(int d, int P, int M, int jmax) {
   return zm;
 }
 
-template <int TZ, bool GATHER, bool WRAP2>
+template <int TZ, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   constexpr int NZB = TZ / 8;
+  constexpr int RSE = exp_stride(TZ);
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
-  const int BM = A.BM, NB = A.NB, RS = A.RS, P = dv.P, M = dv.M, Mt = dv.Mt;
-  const int WXo = rec_wx(), WYo = rec_wy(P), WZo = rec_wz(P);
-  const TileSmem L = tile_smem(BM, NB, RS, GATHER);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
+  const TileSmem L = tile_smem(BM, NB, TZ, GATHER);
+  uint64_t* rawb = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = rawb + kMaxNB;
   uint64_t* empty = full + kMaxNB;
   int* cnt = reinterpret_cast<int*>(empty + kMaxNB);
+  double* f1 = reinterpret_cast<double*>(cnt + kMaxNB);
   int* pidx = reinterpret_cast<int*>(smem + L.off_pidx);
-  int2* lists = reinterpret_cast<int2*>(smem + L.off_lists);
+  int* lists = reinterpret_cast<int*>(smem + L.off_lists);
   double* acc = reinterpret_cast<double*>(smem + L.off_acc);
-  double* bufs = reinterpret_cast<double*>(smem + L.off_buf);
-  const int BS = (BM + 1) * RS;   // doubles per batch buffer (row BM: all zero)
+  double* raws = reinterpret_cast<double*>(smem + L.off_raw);
+  double* exps = reinterpret_cast<double*>(smem + L.off_exp);
+  const int ES = (BM + 1) * RSE;   // doubles per expanded batch (row BM: all zero)
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int tz = blockIdx.x % A.ntz, t2 = blockIdx.x / A.ntz;
@@ -152,13 +173,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
 
   if (tid == 0) {
     for (int b = 0; b < kMaxNB; ++b) {
-      mbar_init(&full[b], 1);
+      mbar_init(&rawb[b], 1);
+      mbar_init(&full[b], kEW);
       mbar_init(&empty[b], kCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int k = tid; k < P; k += kThreads) f1[k] = A.f1[k];
   for (int b = 0; b < NB; ++b)
-    for (int k = tid; k < RS; k += kThreads) bufs[b * BS + BM * RS + k] = 0.0;
+    for (int k = tid; k < RSE; k += kThreads) exps[b * ES + BM * RSE + k] = 0.0;
   if (GATHER)
     for (int k = tid; k < NB * BM * (kCW + 1); k += kThreads) acc[k] = 0.0;
   __syncthreads();
@@ -168,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     const int nslot = dv.nslot;
     auto reduce = [&](int b) {   // gather: sum the per-warp partials of batch buffer b
       const int c = cnt[b];
-      const double* bb = bufs + b * BS;
+      const double* rb = raws + b * BM * kRec;
       for (int p = lane; p < c; p += 32) {
-        const int4 s = *reinterpret_cast<const int4*>(bb + p * RS);
+        const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
         double* ap = acc + (b * BM + p) * (kCW + 1);
         const bool hx = s.x <= X0 + kTXY - 1 && s.x + P - 1 >= X0 && s.y <= Y0 + kTXY - 1 && s.y + P - 1 >= Y0;
         const int sz = hx ? zslot(s.w, P, M, TZ, tz) : -1;
@@ -206,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
       __syncwarp();
       if (lane == 0) {
         cnt[b] = c;
-        mbar_arrive(&full[b]);
+        mbar_arrive(&rawb[b]);
       }
       __syncwarp();
       ++k;
@@ -234,30 +257,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
         e = A.bin_start[row + cy1 + 1];
       }
     };
+    // Runs are issued 32 at a time: lane l owns run q0 + l; a warp scan places the runs in the
+    // batch stream (batch k holds stream positions [k BM, (k+1) BM)) and every lane bulk-copies
+    // the part of its run that falls into the open batch, in parallel.
     int sN, eN;
     load_run(lane, sN, eN);
+    int pos = 0;   // stream position of the next record (= k BM + fill)
     for (int q0 = 0; q0 < npc; q0 += 32) {
-      const int sC = sN, eC = eN;
+      const int sC = sN, nC = eN - sN;
       load_run(q0 + 32 + lane, sN, eN);   // prefetch the next 32 runs
-      const int nq = min(32, npc - q0);
-      for (int i = 0; i < nq; ++i) {
-        int s = __shfl_sync(0xffffffffu, sC, i);
-        int n = __shfl_sync(0xffffffffu, eC, i) - s;
-        while (n > 0) {
-          if (!have) acquire();
-          const int take = min(n, BM - fill);
-          double* dst = bufs + b * BS + fill * RS;
-          if (lane == 0) {
-            const unsigned bytes = (unsigned)(take * RS * 8);
-            mbar_expect_tx(&full[b], bytes);
-            bulk_g2s(dst, A.rec + (int64_t)s * RS, bytes, &full[b]);
-          }
-          for (int l = lane; l < take; l += 32) pidx[b * BM + fill + l] = s + l;
-          fill += take;
-          s += take;
-          n -= take;
-          if (fill == BM) publish(BM);
+      int incl = nC;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      const int rlo = pos + incl - nC, rhi = pos + incl;   // this lane's run in stream positions
+      const int end = pos + tot;
+      while (pos < end) {
+        if (!have) acquire();
+        const int blo = k * BM, bhi = blo + BM;
+        const int lo = max(rlo, blo), hi = min(rhi, bhi);
+        if (hi > lo) {
+          const unsigned bytes = (unsigned)((hi - lo) * kRec * 8);
+          mbar_expect_tx(&rawb[b], bytes);
+          bulk_g2s(raws + (b * BM + (lo - blo)) * kRec, A.rec + (int64_t)(sC + (lo - rlo)) * kRec, bytes, &rawb[b]);
+          if (GATHER)
+            for (int j = lo; j < hi; ++j) pidx[b * BM + (j - blo)] = sC + (j - rlo);
         }
+        const int upto = min(end, bhi);
+        fill = upto - blo;
+        pos = upto;
+        if (fill == BM) publish(BM);
       }
     }
     if (fill > 0) publish(fill);
@@ -273,23 +305,92 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     return;
   }
 
+  if (w > kCW) {
+    // ================================================================ expanders
+    // Windows are cut into 16-entry segments: x, y and TZ/16 z segments per particle.  Lane l of
+    // an expander warp takes segment kind l & 3 of particle (group base) + (l >> 2), so one warp
+    // writes 8 particles x 4 segments with conflict-free stores.  Segment entry i holds stencil
+    // node t: free axes t = i + (X0 - jx0); z t = (i + 16 s + (Z0 - a)) mod M.  Inside the
+    // stencil the value is A E^t f1[t]: the start power by binary powering, then E^(t+1) = E^t E.
+    constexpr int NSEG = 2 + TZ / 16;
+    const int ew = w - (kCW + 1), kind = lane & 3;
+    for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
+      mbar_wait(&rawb[b], (unsigned)ph);
+      const int cn = cnt[b];
+      if (cn > 0 && kind < NSEG) {
+        const double* rb = raws + b * BM * kRec;
+        double* eb = exps + b * ES;
+        for (int p = 8 * ew + (lane >> 2); p < cn; p += 8 * kEW) {
+          const double* r = rb + p * kRec;
+          const int4 s = *reinterpret_cast<const int4*>(r);
+          const int ax = kind < 2 ? kind : 2;
+          const double A0 = (ax == 0 && !GATHER) ? r[4] * r[2] : r[4 + 2 * ax];   // gridding: q in wx
+          const double E = r[5 + 2 * ax];
+          int t, lim, Mw;
+          double* o = eb + p * RSE;
+          if (ax < 2) {
+            t = ax == 0 ? X0 - s.x : Y0 - s.y;
+            lim = 16;
+            Mw = 1 << 30;
+            o += ax == 0 ? kEX : kEY;
+          } else {
+            const int i0 = 16 * (kind - 2);
+            t = Z0 + i0 - s.w;
+            if (t < 0) t += M;
+            if (t >= M) t -= M;
+            lim = jmax - i0;
+            Mw = M;
+            o += zoff(i0);
+          }
+          // two interleaved chains of 8 entries: entries 0..7 from node t, 8..15 from node t + 8
+          int tc[2] = {t, t + 8};
+          if (tc[1] >= Mw) tc[1] -= Mw;
+          double g[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int tt = tc[c];
+            double gg = A0, e = E;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {   // binary powering: A E^tt, tt < P <= 64
+              if ((tt >> k) & 1) gg *= e;
+              e *= e;
+            }
+            g[c] = (tt > 0 && tt < P) ? gg : A0;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int tt = tc[c];
+              double v = 0.0;
+              if (tt >= 0 && tt < P && 8 * c + i < lim) {
+                v = g[c] * f1[tt];
+                g[c] *= E;
+              }
+              o[8 * c + i] = v;
+              if (++tc[c] == Mw) {   // periodic wrap: the stencil restarts at node 0
+                tc[c] = 0;
+                g[c] = A0;
+              }
+            }
+          }
+        }
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
+      if (cn < 0) break;
+    }
+    return;
+  }
+
   // ================================================================ consumers
-  // List entry per relevant particle: x = p | zmask << 8 | (ox + 8) << 16 | (oy + 8) << 24 with
-  // ox = X0b - jx0, oy = Y0b - jy0 (window offsets of the warp block), y = the z offset:
-  //   WRAP2:  d = (Z0 - a) mod M, stencil index of tile node j is (d + j) mod M
-  //   else:   e = signed tile offset of the stencil start, stencil index of node j is j - e
+  // list entry per relevant particle: p | zmask << 8 (8-node z blocks of the tile it meets)
   const int gid = lane >> 2, tig = lane & 3;
   const int X0b = X0 + 4 * (w & 3), Y0b = Y0 + 4 * (w >> 2);
-  int2* wl = lists + w * (BM + 16);
-  const int2 dummy = make_int2(BM | (8 << 16) | (8 << 24), WRAP2 ? 0 : -P);
-  auto zidx = [&](int y, int j) -> int {   // stencil index of tile node j, clamped onto a guard
-    if (WRAP2) {
-      int t = y + j;
-      t -= (t >= M) ? M : 0;
-      return min(t, P);
-    }
-    return clampw(j - y, P);
-  };
+  const int xo = 4 * (w & 3), yo = 4 * (w >> 2);   // warp block inside the tile windows
+  int* wl = lists + w * (BM + 16);
+  const int dummy = BM;
 
   // gridding accumulators: C[16 cols x 8 z] per 8-node block; col r -> (r & 3, r >> 2) of the block
   double c[GATHER ? 1 : NZB][4];
@@ -315,22 +416,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     mbar_wait(&full[b], (unsigned)ph);
     const int cn = cnt[b];
     if (cn < 0) break;
-    const double* bb = bufs + b * BS;
+    const double* rb = raws + b * BM * kRec;
+    const double* eb = exps + b * ES;
     // particles of the batch meeting this warp's 4 x 4 column block (order preserving)
     int n = 0;
-    for (int p0 = 0; p0 < ((dv.dbg & 4) ? 0 : cn); p0 += 32) {
+    for (int p0 = 0; p0 < cn; p0 += 32) {
       const int p = p0 + lane;
       bool rel = false;
-      int2 e = dummy;
+      int e = 0;
       if (p < cn) {
-        const int4 s = *reinterpret_cast<const int4*>(bb + p * RS);
+        const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
         const int ox = X0b - s.x, oy = Y0b - s.y;
         if (ox >= -3 && ox <= P - 1 && oy >= -3 && oy <= P - 1) {
           int d = Z0 - s.w;
           if (d < 0) d += M;
           const int zm = zmask_of(d, P, M, jmax);
           rel = zm != 0;
-          e = make_int2(p | (zm << 8) | ((ox + 8) << 16) | ((oy + 8) << 24), WRAP2 ? d : (d < P ? -d : M - d));
+          e = p | (zm << 8);
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
@@ -345,14 +447,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     } else if (!GATHER) {
       // C[16 cols x 8 z] += A[16 cols x 16 particles] B[16 particles x 8 z]; particle of k-slot
       // tig + 4j is list entry k + tig + 4j (A and B agree on it)
-      const int cx = gid & 3, cy = gid >> 2;
+      const int cx = xo + (gid & 3), cy = yo + (gid >> 2);
       for (int k = 0; k < npad; k += 16) {
-        int2 e[4];
-        int zm = 0;
+        int e[4], zm = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           e[j] = wl[k + tig + 4 * j];
-          zm |= e[j].x;
+          zm |= e[j];
         }
         zm = (zm >> 8) & 0xff;
         zm |= __shfl_xor_sync(0xffffffffu, zm, 1);
@@ -361,62 +462,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
         const double* rz[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const double* r = bb + (e[j].x & 0xff) * RS;
-          const int ox = ((e[j].x >> 16) & 0xff) - 8, oy = ((unsigned)e[j].x >> 24) - 8;
-          const double wq = r[2] * r[WXo + clampw(ox + cx, P)];
-          a[2 * j] = wq * r[WYo + clampw(oy + cy, P)];
-          a[2 * j + 1] = wq * r[WYo + clampw(oy + cy + 2, P)];
-          rz[j] = r + WZo;
+          const double* r = eb + (e[j] & 0xff) * RSE;
+          const double wq = r[kEX + cx];
+          a[2 * j] = wq * r[kEY + cy];
+          a[2 * j + 1] = wq * r[kEY + cy + 2];
+          rz[j] = r + gid;
         }
 #pragma unroll
-        for (int zb = 0; zb < NZB; ++zb) {
-          if (((zm >> zb) & 1) && !(dv.dbg & 1)) {
-            const int jz = 8 * zb + gid;
-            dmma_16x8x16(c[zb], a, rz[0][zidx(e[0].y, jz)], rz[1][zidx(e[1].y, jz)], rz[2][zidx(e[2].y, jz)],
-                         rz[3][zidx(e[3].y, jz)]);
-          }
-        }
+        for (int zb = 0; zb < NZB; ++zb)
+          if ((zm >> zb) & 1)
+            dmma_16x8x16(c[zb], a, rz[0][zoff(8 * zb)], rz[1][zoff(8 * zb)], rz[2][zoff(8 * zb)], rz[3][zoff(8 * zb)]);
       }
     } else {
       // T[16 particles x 8 cols] = A[16 particles x 8 z] (wz) B[8 z x 8 cols] (H~), per col half;
       // particle of row gid (gid + 8) is list entry k + gid (k + gid + 8)
+      const int cx0 = xo + 2 * (tig & 1), cy0 = yo + (tig >> 1);   // this thread's cols (x +0/+1, y +0/+2)
       for (int k = 0; k < npad; k += 16) {
-        const int2 e0 = wl[k + gid], e1 = wl[k + gid + 8];
-        int zm = ((e0.x | e1.x) >> 8) & 0xff;
+        const int e0 = wl[k + gid], e1 = wl[k + gid + 8];
+        int zm = ((e0 | e1) >> 8) & 0xff;
         zm |= __shfl_xor_sync(0xffffffffu, zm, 4);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 8);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 16);
-        const double* r0 = bb + (e0.x & 0xff) * RS;
-        const double* r1 = bb + (e1.x & 0xff) * RS;
+        const double* r0 = eb + (e0 & 0xff) * RSE;
+        const double* r1 = eb + (e1 & 0xff) * RSE;
+        const double* z0 = r0 + tig;
+        const double* z1 = r1 + tig;
         double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
-          if (((zm >> zb) & 1) && !(dv.dbg & 1)) {
-            const int j0 = 8 * zb + tig, j1 = j0 + 4;
-            const double a[4] = {r0[WZo + zidx(e0.y, j0)], r1[WZo + zidx(e1.y, j0)], r0[WZo + zidx(e0.y, j1)],
-                                 r1[WZo + zidx(e1.y, j1)]};
+          if ((zm >> zb) & 1) {
+            const double a[4] = {z0[zoff(8 * zb)], z1[zoff(8 * zb)], z0[zoff(8 * zb + 4)], z1[zoff(8 * zb + 4)]};
             dmma_16x8x8(t0, a, hB[zb][0][0], hB[zb][0][1]);
             dmma_16x8x8(t1, a, hB[zb][1][0], hB[zb][1][1]);
           }
         }
-        // this thread's cols: x = 2 (tig & 1) + {0, 1}, y = (tig >> 1) + {0 (half 0), 2 (half 1)}
-        const int cx0 = 2 * (tig & 1), cy0 = tig >> 1;
-        double v[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int2 eh = h ? e1 : e0;
-          const double* r = h ? r1 : r0;
-          const int ox = ((eh.x >> 16) & 0xff) - 8, oy = ((unsigned)eh.x >> 24) - 8;
-          const double wx0 = r[WXo + clampw(ox + cx0, P)], wx1 = r[WXo + clampw(ox + cx0 + 1, P)];
-          const double wy0 = r[WYo + clampw(oy + cy0, P)], wy2 = r[WYo + clampw(oy + cy0 + 2, P)];
-          v[h] = wy0 * fma(wx0, t0[2 * h], wx1 * t0[2 * h + 1]) + wy2 * fma(wx0, t1[2 * h], wx1 * t1[2 * h + 1]);
-        }
+        const double v0 = r0[kEY + cy0] * fma(r0[kEX + cx0], t0[0], r0[kEX + cx0 + 1] * t0[1]) +
+                          r0[kEY + cy0 + 2] * fma(r0[kEX + cx0], t1[0], r0[kEX + cx0 + 1] * t1[1]);
+        const double v1 = r1[kEY + cy0] * fma(r1[kEX + cx0], t0[2], r1[kEX + cx0 + 1] * t0[3]) +
+                          r1[kEY + cy0 + 2] * fma(r1[kEX + cx0], t1[2], r1[kEX + cx0 + 1] * t1[3]);
+        double v[2] = {v0, v1};
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 2);
         if (tig == 0) {
-          const int pa = e0.x & 0xff, pb = e1.x & 0xff;
+          const int pa = e0 & 0xff, pb = e1 & 0xff;
           if (pa < BM) acc[(b * BM + pa) * (kCW + 1) + w] = v[0];
           if (pb < BM) acc[(b * BM + pb) * (kCW + 1) + w] = v[1];
         }
@@ -463,57 +553,33 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   phi[perm[p]] = s;
 }
 
-// Record rows of the sorted particles (layout in tiles.cuh).  Window weights by Fast Gaussian
-// Gridding: with d0 the signed distance from the particle to the first stencil node,
-//   e^{-alpha (d0 + t h)^2} = e^{-alpha d0^2} (e^{-2 alpha h d0})^t e^{-alpha h^2 t^2},
-// i.e. two exponentials per particle and axis plus the particle-independent table f1[t]
-// (reading R-3 for the node positions).  kRecPB particles per block are assembled in shared
-// memory and written out as one coalesced run.
-constexpr int kRecPB = 16;
-
-__global__ void __launch_bounds__(128) k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4,
-                                                 int64_t N, int RS, const double* __restrict__ f1,
-                                                 double* __restrict__ rec) {
-  extern __shared__ __align__(16) double srow[];
-  const int P = dv.P;
-  const int64_t i0 = (int64_t)blockIdx.x * kRecPB;
-  const int np = (int)((N - i0 < kRecPB) ? (N - i0) : kRecPB);
-  for (int k = threadIdx.x; k < kRecPB * RS; k += blockDim.x) srow[k] = 0.0;
-  __syncthreads();
-  if (threadIdx.x < 3 * np) {
-    const int p = threadIdx.x / 3, ax = threadIdx.x - 3 * p;
-    const int64_t i = i0 + p;
-    const double4 pp = P4[i];
-    const int4 s = S4[i];
-    double* row = srow + p * RS;
-    double d0;
-    int off;
-    if (ax == 0) {
-      d0 = ((double)s.x - 0.5 * P) * dv.h - pp.x;
-      off = rec_wx();
-      reinterpret_cast<int4*>(row)[0] = s;
-      row[2] = pp.w;
-    } else if (ax == 1) {
-      d0 = ((double)s.y - 0.5 * P) * dv.h - pp.y;
-      off = rec_wy(P);
-    } else {
-      d0 = (double)s.z * dv.h - pp.z;
-      off = rec_wz(P);
-    }
-    double g = exp(-dv.alpha * d0 * d0);
-    const double E = exp(-2.0 * dv.alpha * dv.h * d0);
-    for (int t = 0; t < P; ++t) {
-      row[off + t] = g * f1[t];
-      g *= E;
-    }
+// Compact records of the sorted particles: {jx0, jy0, lz0, lz0 mod M} (reading R-3), q, 0, and
+// per axis the Fast Gaussian Gridding factors of the first stencil node offset d0:
+//   A = e^{-alpha d0^2},  E = e^{-2 alpha h d0}   (node t: A E^t f1[t]).
+__global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, int64_t N,
+                          double* __restrict__ rec) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const double4 pp = P4[i];
+  const int4 s = S4[i];
+  const double P2 = 0.5 * dv.P;
+  const double d0[3] = {((double)s.x - P2) * dv.h - pp.x, ((double)s.y - P2) * dv.h - pp.y, (double)s.z * dv.h - pp.z};
+  double r[kRec];
+  r[2] = pp.w;
+  r[3] = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    r[4 + 2 * ax] = exp(-dv.alpha * d0[ax] * d0[ax]);
+    r[5 + 2 * ax] = exp(-2.0 * dv.alpha * dv.h * d0[ax]);
   }
-  __syncthreads();
-  const double2* src = reinterpret_cast<const double2*>(srow);
-  double2* dst = reinterpret_cast<double2*>(rec + i0 * RS);
-  for (int k = threadIdx.x; k < np * RS / 2; k += blockDim.x) dst[k] = src[k];
+  double2* out = reinterpret_cast<double2*>(rec + i * kRec);
+  out[0] = make_double2(__hiloint2double(s.y, s.x), __hiloint2double(s.w, s.z));
+#pragma unroll
+  for (int k = 1; k < kRec / 2; ++k) out[k] = make_double2(r[2 * k], r[2 * k + 1]);
 }
 
 int tile_tz(int M) { return M >= 64 ? 32 : 16; }
+int rec_doubles(int P) { return (void)P, kRec; }
 
 // Slots of the gather partials: x and y tiles per stencil, then z tiles (<= ceil(P/TZ)+2 once
 // the stencil wraps around the periodic axis).
@@ -531,20 +597,16 @@ int64_t gather_slots(const KDev& dv) {
 }
 
 void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
-  const int RS = rec_stride(pl.dv.P);
-  const size_t smem = sizeof(double) * kRecPB * RS;
-  if (smem > 48 * 1024)
-    SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_records, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_records<<<(unsigned)ceil_div(N, kRecPB), 128, smem, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, RS,
-                                                               pl.d_f1, w.rec);
+  k_records<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, w.rec);
   SE1P_LAUNCH_CHECK();
 }
 
-template <int TZ, bool GATHER, bool WRAP2>
+template <int TZ, bool GATHER>
 static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   TileArgs a;
   a.dv = pl.dv;
   KDev& dv = a.dv;
+  if (dv.P > kMaxP) throw Error{4, "P > 64 is not supported by the tile kernels"};
   slot_geometry(dv);
   dv.err = w.flag + 1;
   dv.N = N;
@@ -557,45 +619,37 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   a.tx_lo = tx_lo;
   const int ntx = tx_hi - tx_lo;
   if (ntx <= 0) return;
-  a.RS = rec_stride(dv.P);
   a.rec = w.rec;
   a.bin_start = w.bin_start;
+  a.f1 = pl.d_f1;
   a.grid = w.grid;
   a.gpart = GATHER ? w.gpart : nullptr;
   int BM = 0, NB = 0;
   const int limit = 227 * 1024 - 1024;
-  for (int bm : {64, 32, 16}) {
+  for (int bm : {64, 32}) {
     for (int nb = kMaxNB; nb >= 2 && !BM; --nb)
-      if (tile_smem(bm, nb, a.RS, GATHER).total <= limit) {
+      if (tile_smem(bm, nb, TZ, GATHER).total <= limit) {
         BM = bm;
         NB = nb;
       }
     if (BM) break;
   }
-  if (!BM) throw Error{4, "P too large for the tile kernels (shared memory)"};
+  if (!BM) throw Error{4, "tile kernels do not fit in shared memory"};
   a.BM = BM;
   a.NB = NB;
-  const size_t smem = (size_t)tile_smem(BM, NB, a.RS, GATHER).total;
-  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER, WRAP2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER).total;
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const unsigned nblk = (unsigned)(ntx * a.nty * a.ntz);
-  k_tiles<TZ, GATHER, WRAP2><<<nblk, kThreads, smem, st>>>(a);
+  k_tiles<TZ, GATHER><<<nblk, kThreads, smem, st>>>(a);
   SE1P_LAUNCH_CHECK();
 }
 
-// WRAP2: a stencil can meet a z tile twice (both ends of the periodic axis) iff TZ + P > M.
 template <bool GATHER>
 static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
-  const int TZ = tile_tz(pl.dv.M);
-  const bool wrap2 = TZ + pl.dv.P > pl.dv.M;
   if (tx_hi < 0) tx_hi = (int)ceil_div(pl.dv.Mt, kTXY);
-  if (TZ == 32) {
-    if (wrap2) launch_tiles<32, GATHER, true>(pl, w, N, tx_lo, tx_hi, st);
-    else launch_tiles<32, GATHER, false>(pl, w, N, tx_lo, tx_hi, st);
-  } else {
-    if (wrap2) launch_tiles<16, GATHER, true>(pl, w, N, tx_lo, tx_hi, st);
-    else launch_tiles<16, GATHER, false>(pl, w, N, tx_lo, tx_hi, st);
-  }
+  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, GATHER>(pl, w, N, tx_lo, tx_hi, st);
+  else launch_tiles<16, GATHER>(pl, w, N, tx_lo, tx_hi, st);
 }
 
 void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {

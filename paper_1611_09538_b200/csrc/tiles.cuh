@@ -15,26 +15,8 @@ namespace se1p {
 constexpr int kTXY = 16;        // CTA tile extent in x and y (grid nodes)
 constexpr int kBXY = 4;         // particle bins: xy columns of kBXY x kBXY cells, z-sorted inside
 
-// Particle record (one row per sorted particle, RS doubles, built by k_records):
-//   [0,1] int4 {jx0, jy0, lz0, lz0 mod M}   stencil starts (reading R-3)
-//   [2]   q
-//   [3]   0                          guard (index -1 of wx)
-//   [4, 4+P)        wx[t]            window weights e^{-alpha d_t^2} per axis
-//   [4+P]           0                guard
-//   [5+P, 5+2P)     wy[t]
-//   [5+2P]          0
-//   [6+2P, 6+3P)    wz[t]
-//   [6+3P]          0
-// RS = smallest value >= 7+3P with RS = 4 (mod 16): rows are 16-byte aligned for the bulk copy
-// and consecutive rows start 4 doubles (8 banks) apart in shared memory.
-__host__ __device__ inline int rec_stride(int P) {
-  int r = 7 + 3 * P;
-  while (r % 16 != 4) ++r;
-  return r;
-}
-__host__ __device__ inline int rec_wx() { return 4; }
-__host__ __device__ inline int rec_wy(int P) { return 5 + P; }
-__host__ __device__ inline int rec_wz(int P) { return 6 + 2 * P; }
+// Doubles per particle weight row (tiles.cu, k_records).
+int rec_doubles(int P);
 
 __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], double b0, double b1) {
   asm volatile(
