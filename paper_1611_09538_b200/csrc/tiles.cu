@@ -66,7 +66,7 @@ struct TileSmem {
 
 __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather) {
   TileSmem s;
-  int o = 3 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
+  int o = 4 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
   s.off_pidx = o;
   o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   uint64_t* rawb = reinterpret_cast<uint64_t*>(smem);
   uint64_t* full = rawb + kMaxNB;
   uint64_t* empty = full + kMaxNB;
-  int* cnt = reinterpret_cast<int*>(empty + kMaxNB);
+  uint64_t* freeb = empty + kMaxNB;   // gather: batch reduced, buffers reusable
+  int* cnt = reinterpret_cast<int*>(freeb + kMaxNB);
   double* f1 = reinterpret_cast<double*>(cnt + kMaxNB);
   int* pidx = reinterpret_cast<int*>(smem + L.off_pidx);
   int* lists = reinterpret_cast<int*>(smem + L.off_lists);
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
       mbar_init(&rawb[b], 1);
       mbar_init(&full[b], kEW);
       mbar_init(&empty[b], kCW);
+      mbar_init(&freeb[b], kEW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,42 +188,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     for (int k = tid; k < NB * BM * (kCW + 1); k += kThreads) acc[k] = 0.0;
   __syncthreads();
 
+  const int nslot = dv.nslot;
+// gather: sum the per-warp partials of batch buffer b into the particles' slots (expander warps)
+auto reduce = [&](int b, int rt) {
+    const int c = cnt[b];
+    const double* rb = raws + b * BM * kRec;
+    for (int p = rt; p < c; p += 32 * kEW) {
+      const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
+      double* ap = acc + (b * BM + p) * (kCW + 1);
+      const bool hx = s.x <= X0 + kTXY - 1 && s.x + P - 1 >= X0 && s.y <= Y0 + kTXY - 1 && s.y + P - 1 >= Y0;
+      const int sz = hx ? zslot(s.w, P, M, TZ, tz) : -1;
+      if (sz >= 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int v = 0; v < kCW; ++v) {
+          sum += ap[v];
+          ap[v] = 0.0;
+        }
+        const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
+        A.gpart[(int64_t)pidx[b * BM + p] * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = sum;
+      } else if (hx) {
+        for (int v = 0; v < kCW; ++v)
+          if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
+      }
+    }
+  };
+
+
   if (w == kCW) {
     // ================================================================ producer
-    const int nslot = dv.nslot;
-    auto reduce = [&](int b) {   // gather: sum the per-warp partials of batch buffer b
-      const int c = cnt[b];
-      const double* rb = raws + b * BM * kRec;
-      for (int p = lane; p < c; p += 32) {
-        const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
-        double* ap = acc + (b * BM + p) * (kCW + 1);
-        const bool hx = s.x <= X0 + kTXY - 1 && s.x + P - 1 >= X0 && s.y <= Y0 + kTXY - 1 && s.y + P - 1 >= Y0;
-        const int sz = hx ? zslot(s.w, P, M, TZ, tz) : -1;
-        if (sz >= 0) {
-          double sum = 0.0;
-#pragma unroll
-          for (int v = 0; v < kCW; ++v) {
-            sum += ap[v];
-            ap[v] = 0.0;
-          }
-          const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
-          A.gpart[(int64_t)pidx[b * BM + p] * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = sum;
-        } else if (hx) {
-          for (int v = 0; v < kCW; ++v)
-            if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
-        }
-      }
-      __syncwarp();
-    };
-
     int k = 0, fill = 0, b = 0;
     bool have = false;
     auto acquire = [&]() {
       b = k % NB;
-      if (k >= NB) {
-        mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1));
-        if (GATHER) reduce(b);
-      }
+      if (k >= NB) mbar_wait(GATHER ? &freeb[b] : &empty[b], (unsigned)(((k - NB) / NB) & 1));
       have = true;
     };
     auto publish = [&](int c) {
@@ -295,13 +295,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     if (fill > 0) publish(fill);
     acquire();
     publish(-1);   // end marker
-    if (GATHER) {
-      const int kend = k;   // batches 0 .. kend-2 are real; those < kend-NB were reduced already
-      for (int j = max(0, kend - NB); j <= kend - 2; ++j) {
-        mbar_wait(&empty[j % NB], (unsigned)((j / NB) & 1));
-        reduce(j % NB);
-      }
-    }
     return;
   }
 
@@ -312,9 +305,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
     // writes 8 particles x 4 segments with conflict-free stores.  Segment entry i holds stencil
     // node t: free axes t = i + (X0 - jx0); z t = (i + 16 s + (Z0 - a)) mod M.  Inside the
     // stencil the value is A E^t f1[t]: the start power by binary powering, then E^(t+1) = E^t E.
+    // Gather: after expanding batch j the expanders reduce batch j-2 (once the consumers released
+    // it) and free its buffers for the producer.
     constexpr int NSEG = 2 + TZ / 16;
     const int ew = w - (kCW + 1), kind = lane & 3;
-    for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
+    auto reduce_batch = [&](int j) {
+      const int bj = j % NB;
+      mbar_wait(&empty[bj], (unsigned)((j / NB) & 1));
+      reduce(bj, tid - (kCW + 1) * 32);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&freeb[bj]);
+    };
+    for (int b = 0, ph = 0, j = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0), ++j) {
       mbar_wait(&rawb[b], (unsigned)ph);
       const int cn = cnt[b];
       if (cn > 0 && kind < NSEG) {
@@ -379,6 +381,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
       __threadfence_block();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
+      if (GATHER) {
+        if (j >= 2) reduce_batch(j - 2);
+        if (cn < 0 && j >= 1) reduce_batch(j - 1);
+      }
       if (cn < 0) break;
     }
     return;
