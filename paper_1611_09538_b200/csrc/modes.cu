@@ -28,19 +28,20 @@ __global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
+  const int S = M + 1;   // padded row stride: the transposed accesses below stay conflict-free
   double2* buf = sm;
-  double2* tmp = sm + CB * M;
+  double2* tmp = sm + CB * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   const double* src = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
     const int c = idx / M;
-    buf[idx] = make_double2((y0 + c < Mt) ? src[idx] : 0.0, 0.0);
+    buf[idx + c] = make_double2((y0 + c < Mt) ? src[idx] : 0.0, 0.0);
   }
   __syncthreads();
-  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CB, M, threadIdx.x, blockDim.x);
+  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CB, S, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
-    if (y0 + c < Mt) planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = out[c * M + n];
+    if (y0 + c < Mt) planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = out[c * S + n];
   }
 }
 
@@ -48,21 +49,22 @@ __global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
+  const int S = M + 1;   // padded row stride (conflict-free transposed accesses)
   double2* buf = sm;
-  double2* tmp = sm + CB * M;
+  double2* tmp = sm + CB * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
     double2 v = (y0 + c < Mt) ? planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] : make_double2(0.0, 0.0);
-    buf[c * M + n] = v;
-    if (n > 0 && 2 * n < M) buf[c * M + (M - n)] = make_double2(v.x, -v.y);  // Hermitian half
+    buf[c * S + n] = v;
+    if (n > 0 && 2 * n < M) buf[c * S + (M - n)] = make_double2(v.x, -v.y);  // Hermitian half
   }
   __syncthreads();
-  double2* out = fft_rows<1>(buf, tmp, fz, tw, CB, M, threadIdx.x, blockDim.x);
+  double2* out = fft_rows<1>(buf, tmp, fz, tw, CB, S, threadIdx.x, blockDim.x);
   double* dst = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
     const int c = idx / M;
-    if (y0 + c < Mt) dst[idx] = out[idx].x;
+    if (y0 + c < Mt) dst[idx] = out[idx + c].x;
   }
 }
 
@@ -122,17 +124,18 @@ __global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const 
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
                           const double2* __restrict__ pl, PlaneSel S) {
   extern __shared__ double2 sm[];
+  const int SW = W + 1;   // padded row stride: the transposed accesses stay conflict-free
   double2* buf = sm;
-  double2* tmp = sm + CB * W;
+  double2* tmp = sm + CB * SW;
   const int n = S.global(blockIdx.y), y0 = blockIdx.x * CB;
   const int nc = min(CB, W - y0);
   double2* Tp = T + base + (int64_t)blockIdx.y * Mt * W;
   for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
     const int a = idx / CB, c = idx - a * CB;
-    buf[c * W + a] = (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
+    buf[c * SW + a] = (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, W, threadIdx.x, blockDim.x);
+  double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
   double2* oth = (out == buf) ? tmp : buf;
   const double2 pn = pl[n];
   for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
@@ -144,14 +147,14 @@ __global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const 
     } else {
       m = pn.x * exJ[a] * exJ[y] / (k2J[a] + k2J[y] + pn.y);
     }
-    double2 v = out[idx];
-    out[idx] = make_double2(v.x * m, v.y * m);
+    double2 v = out[c * SW + a];
+    out[c * SW + a] = make_double2(v.x * m, v.y * m);
   }
   __syncthreads();
-  double2* res = fft_rows<1>(out, oth, f, tw, CB, W, threadIdx.x, blockDim.x);
+  double2* res = fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < Mt * CB; idx += blockDim.x) {
     const int a = idx / CB, c = idx - a * CB;
-    if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * W + a];
+    if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * SW + a];
   }
 }
 
@@ -164,7 +167,7 @@ void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
+  const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zfwd, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
   k_zfwd<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
@@ -176,7 +179,7 @@ void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const Slab
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)CB * M * sizeof(double2);
+  const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zinv, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
   k_zinv<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
@@ -188,7 +191,7 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
   if (nplanes <= 0) return;
   const int Mt = pl.dv.Mt;
   const int RB = rows_for(W), CB = cols_for(W);
-  const size_t smr = 2 * (size_t)RB * W * sizeof(double2), smc = 2 * (size_t)CB * W * sizeof(double2);
+  const size_t smr = 2 * (size_t)RB * W * sizeof(double2), smc = 2 * (size_t)CB * (W + 1) * sizeof(double2);
   set_smem((const void*)k_rowfwd, smr);
   set_smem((const void*)k_rowinv, smr);
   set_smem((const void*)k_colpass, smc);
