@@ -40,6 +40,7 @@ constexpr int kThreads = (kCW + 1 + kEW) * 32;   // + producer
 constexpr int kMaxNB = 4;
 constexpr int kRec = 10;                         // doubles per compact record (80 B)
 constexpr int kMaxP = 64;
+constexpr int kEntB = 7, kEntZ = 9;              // gridding list entry: p (7 bits), buffer (2), z mask
 
 // Expanded row: 16-entry window segments wx, wy, wz[0:16), wz[16:32) at offsets 0, 17, 34, 51
 // (17 apart: when 8 particles x 4 segments are written by one warp, the 32 lanes fall into
@@ -71,7 +72,7 @@ __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gathe
   o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
   s.off_lists = o;
-  o += kCW * (BM + 16) * 4;
+  o += kCW * (BM + 32) * 4;
   o = (o + 15) & ~15;
   s.off_acc = o;
   if (gather) o += NB * BM * (kCW + 1) * 8;
@@ -395,7 +396,7 @@ auto reduce = [&](int b, int rt) {
   const int gid = lane >> 2, tig = lane & 3;
   const int X0b = X0 + 4 * (w & 3), Y0b = Y0 + 4 * (w >> 2);
   const int xo = 4 * (w & 3), yo = 4 * (w >> 2);   // warp block inside the tile windows
-  int* wl = lists + w * (BM + 16);
+  int* wl = lists + w * (BM + 32);
   const int dummy = BM;
 
   // gridding accumulators: C[16 cols x 8 z] per 8-node block; col r -> (r & 3, r >> 2) of the block
@@ -418,6 +419,91 @@ auto reduce = [&](int b, int rt) {
         }
   }
 
+  if (!GATHER) {
+    // Gridding, batches in order.  Entries left over after the last full k-step of a batch (< 16)
+    // are carried into the next batch's list (entries name their buffer), so k-steps are padded
+    // only at the end of the tile; a batch is released (empty) once no carried entry refers to it.
+    const int cx = xo + (gid & 3), cy = yo + (gid >> 2);
+    auto ksteps = [&](int k0, int k1) {
+      for (int k = k0; k < k1; k += 16) {
+        int e[4], zm = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          e[j] = wl[k + tig + 4 * j];
+          zm |= e[j];
+        }
+        zm = (zm >> kEntZ) & 0xff;
+        zm |= __shfl_xor_sync(0xffffffffu, zm, 1);
+        zm |= __shfl_xor_sync(0xffffffffu, zm, 2);
+        double a[8];
+        const double* rz[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double* r = exps + ((e[j] >> kEntB) & 3) * ES + (e[j] & ((1 << kEntB) - 1)) * RSE;
+          const double wq = r[kEX + cx];
+          a[2 * j] = wq * r[kEY + cy];
+          a[2 * j + 1] = wq * r[kEY + cy + 2];
+          rz[j] = r + gid;
+        }
+#pragma unroll
+        for (int zb = 0; zb < NZB; ++zb)
+          if ((zm >> zb) & 1)
+            dmma_16x8x16(c[zb], a, rz[0][zoff(8 * zb)], rz[1][zoff(8 * zb)], rz[2][zoff(8 * zb)], rz[3][zoff(8 * zb)]);
+      }
+    };
+    int held = 0, bprev = -1;
+    for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
+      mbar_wait(&full[b], (unsigned)ph);
+      const int cn = cnt[b];
+      if (cn < 0) {
+        if (held > 0) {   // flush the carried entries, padded to 16
+          if (lane < 16 - held) wl[held + lane] = dummy;
+          __syncwarp();
+          ksteps(0, 16);
+        }
+        __syncwarp();
+        if (lane == 0 && bprev >= 0) mbar_arrive(&empty[bprev]);
+        break;
+      }
+      const double* rb = raws + b * BM * kRec;
+      int n = held;
+      for (int p0 = 0; p0 < cn; p0 += 32) {
+        const int p = p0 + lane;
+        bool rel = false;
+        int e = 0;
+        if (p < cn) {
+          const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
+          const int ox = X0b - s.x, oy = Y0b - s.y;
+          if (ox >= -3 && ox <= P - 1 && oy >= -3 && oy <= P - 1) {
+            int d = Z0 - s.w;
+            if (d < 0) d += M;
+            const int zm = zmask_of(d, P, M, jmax);
+            rel = zm != 0;
+            e = p | (b << kEntB) | (zm << kEntZ);
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
+        n += __popc(bal);
+      }
+      __syncwarp();
+      int kend = n & ~15;
+      if (kend < held) {   // fewer than 16 entries and some carried: flush everything (padded)
+        kend = (n + 15) & ~15;
+        if (lane < kend - n) wl[n + lane] = dummy;
+        __syncwarp();
+      }
+      if (!(dv.dbg & 2)) ksteps(0, kend);
+      const int rest = n > kend ? n - kend : 0;   // carry the rest (all from this batch)
+      const int mv = lane < rest ? wl[kend + lane] : 0;
+      __syncwarp();
+      if (lane < rest) wl[lane] = mv;
+      __syncwarp();
+      held = rest;
+      if (lane == 0 && bprev >= 0) mbar_arrive(&empty[bprev]);
+      bprev = b;
+    }
+  } else
   for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
     mbar_wait(&full[b], (unsigned)ph);
     const int cn = cnt[b];
