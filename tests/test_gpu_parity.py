@@ -176,3 +176,62 @@ def test_reference_kernels_match_oracle(case):
     ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
     got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, reference_kernels=True)
     assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), name
+
+
+EDGE = [
+    # name, N, L, xi, M, P, n_l, S0, SI, SJ, seed
+    ("odd-P7", 90, (1, 1, 1), 4.0, 16, 7, 2, 64, 48, 24, 21),
+    ("odd-P9-M18", 70, (1, 1, 1), 4.0, 18, 9, 3, 70, 56, 28, 22),
+    ("P32-M48", 120, (1, 1, 1), 6.0, 48, 32, 4, 200, 160, 80, 23),
+    ("P40-M64", 60, (1, 1, 1), 7.0, 64, 40, 3, 260, 208, 104, 24),
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=[c[0] for c in EDGE])
+def test_kspace_odd_and_large_stencils(case):
+    """Odd P (reading R-3 covers both parities) and stencils wider than a 32-node z tile and
+    than the 16-column tiles (several tiles per axis, periodic wrap of the stencil)."""
+    name, N, L, xi, M, P, n_l, S0, SI, SJ, seed = case
+    x, q = make_system(N, L, seed)
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), (name, np.max(np.abs(got - ref)))
+
+
+def test_kspace_degenerate_positions():
+    """Particles exactly on grid nodes, on the faces x = 0, y = 0, z = 0, just below L3, and
+    coincident pairs (same (x, y): rho = 0 in the zero mode; same point up to z images)."""
+    L, xi, M, P, n_l, S0, SI, SJ = (1.0, 1.0, 1.0), 4.0, 16, 10, 3, 80, 64, 26
+    h = 1.0 / M
+    x = np.array([[0.0, 0.0, 0.0], [5 * h, 7 * h, 3 * h], [0.5, 0.5, np.nextafter(1.0, 0.0)],
+                  [0.25, 0.75, 0.5], [0.25, 0.75, 0.9], [np.nextafter(1.0, 0.0), 0.3, 0.2],
+                  [0.6, np.nextafter(1.0, 0.0), 0.0], [0.6, 0.1, 0.45]])
+    q = np.array([1.0, -0.5, 0.25, -1.0, 0.75, 0.5, -0.25, -0.75])
+    q -= q.mean()
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+
+def test_empty_and_tiny_inputs_rejected_or_exact():
+    L = (1.0, 1.0, 1.0)
+    xd = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    qd = torch.zeros(0, dtype=torch.float64, device="cuda")
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(xd, qd, L, 4.0, 16, 8)
+    assert e.value.code == 1
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.real(xd, qd, L, 4.0, 0.5)
+    assert e.value.code == 1
+
+
+def test_ragged_tiles_all_configs_of_tz():
+    """Grids whose extents are not multiples of the tile sizes: M~ = M_free + P not a multiple of
+    16 and M not a multiple of the 32-node z tile (M >= 64 uses TZ = 32)."""
+    for (N, M, P, SJ, seed) in [(200, 72, 13, 90, 31), (150, 66, 10, 80, 32)]:
+        L = (1.0, 1.0, 1.0)
+        x, q = make_system(N, L, seed)
+        xi = 0.25 * M / 1.0 * 0.5
+        ref = sd.se1p_kspace(x, q, L, xi, M, P, 3, 2 * (M + P), 2 * (M + P), SJ)
+        got = _gpu_kspace(x, q, L, xi, M, P, 3, 2 * (M + P), 2 * (M + P), SJ)
+        assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), (M, P)
