@@ -221,7 +221,7 @@ __device__ double2* fft_rows(double2* buf, double2* tmp, const FftDesc& d, const
 bool fft_factor(int n, std::vector<int>& rad);
 // Build the descriptor and append its twiddle/root table to `table` (host), setting offsets.
 bool fft_make(int n, FftDesc& d, std::vector<double2>& table);
-// "FFT-friendly": only factors 2, 3, 5, 7.
+// "FFT-friendly": only factors 2, 3, 5.
 bool fft_friendly(int n);
 int next_friendly(int n);
 

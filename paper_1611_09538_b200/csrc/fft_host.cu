@@ -55,11 +55,12 @@ bool fft_make(int n, FftDesc& d, std::vector<double2>& table) {
 
 bool fft_friendly(int n) {
   if (n < 1) return false;
-  for (int p : {2, 3, 5, 7})
+  for (int p : {2, 3, 5})
     while (n % p == 0) n /= p;
   return n == 1;
 }
 
+// Smallest n' >= n whose factors are 2, 3, 5: every stage then has a dedicated butterfly.
 int next_friendly(int n) {
   while (!fft_friendly(n)) ++n;
   return n;

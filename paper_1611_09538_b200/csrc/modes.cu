@@ -20,6 +20,7 @@ namespace se1p {
 static int zcols(int M) { return M >= 256 ? 8 : (M >= 64 ? 16 : 32); }
 static int rows_for(int W) { int r = 98304 / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? 4 : 8; }
+constexpr int kFftThreads = 256;   // threads per block of the FFT passes
 
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
 // Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if
@@ -170,7 +171,7 @@ void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout
   const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zfwd, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zfwd<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
+  k_zfwd<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -182,7 +183,7 @@ void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const Slab
   const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zinv, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zinv<<<grid, 256, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
+  k_zinv<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -196,13 +197,13 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
   set_smem((const void*)k_rowinv, smr);
   set_smem((const void*)k_colpass, smc);
   const double2* tw = pl.d_tw + twoff;
-  k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, base, RB, f, tw, planes, w.T, L, S);
+  k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), kFftThreads, smr, st>>>(Mt, W, base, RB, f, tw, planes, w.T, L, S);
   SE1P_LAUNCH_CHECK();
-  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), 256, smc, st>>>(Mt, W, base, CB, f, tw, w.T, kernel_class,
+  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), kFftThreads, smc, st>>>(Mt, W, base, CB, f, tw, w.T, kernel_class,
                                                                         pl.d_khat, pl.d_exJ, pl.d_k2J,
                                                                         (const double2*)pl.d_pl, S);
   SE1P_LAUNCH_CHECK();
-  k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), 256, smr, st>>>(Mt, W, base, RB, f, tw, w.T, planes, L, S);
+  k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), kFftThreads, smr, st>>>(Mt, W, base, RB, f, tw, w.T, planes, L, S);
   SE1P_LAUNCH_CHECK();
 }
 
