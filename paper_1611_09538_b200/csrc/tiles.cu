@@ -62,14 +62,12 @@ struct TileArgs {
 };
 
 struct TileSmem {
-  int off_pidx, off_lists, off_acc, off_raw, off_exp, total;
+  int off_lists, off_acc, off_raw, off_exp, total;
 };
 
 __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather) {
   TileSmem s;
   int o = 4 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
-  s.off_pidx = o;
-  o += kMaxNB * BM * 4;
   o = (o + 15) & ~15;
   s.off_lists = o;
   o += kCW * (BM + 32) * 4;
@@ -160,7 +158,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   uint64_t* freeb = empty + kMaxNB;   // gather: batch reduced, buffers reusable
   int* cnt = reinterpret_cast<int*>(freeb + kMaxNB);
   double* f1 = reinterpret_cast<double*>(cnt + kMaxNB);
-  int* pidx = reinterpret_cast<int*>(smem + L.off_pidx);
   int* lists = reinterpret_cast<int*>(smem + L.off_lists);
   double* acc = reinterpret_cast<double*>(smem + L.off_acc);
   double* raws = reinterpret_cast<double*>(smem + L.off_raw);
@@ -207,7 +204,8 @@ auto reduce = [&](int b, int rt) {
           ap[v] = 0.0;
         }
         const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
-        A.gpart[(int64_t)pidx[b * BM + p] * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = sum;
+        const int64_t i = __double_as_longlong(rb[p * kRec + 3]);   // sorted index (k_records)
+        A.gpart[i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = sum;
       } else if (hx) {
         for (int v = 0; v < kCW; ++v)
           if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
@@ -284,8 +282,6 @@ auto reduce = [&](int b, int rt) {
           const unsigned bytes = (unsigned)((hi - lo) * kRec * 8);
           mbar_expect_tx(&rawb[b], bytes);
           bulk_g2s(raws + (b * BM + (lo - blo)) * kRec, A.rec + (int64_t)(sC + (lo - rlo)) * kRec, bytes, &rawb[b]);
-          if (GATHER)
-            for (int j = lo; j < hi; ++j) pidx[b * BM + (j - blo)] = sC + (j - rlo);
         }
         const int upto = min(end, bhi);
         fill = upto - blo;
@@ -645,7 +641,8 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   phi[perm[p]] = s;
 }
 
-// Compact records of the sorted particles: {jx0, jy0, lz0, lz0 mod M} (reading R-3), q, 0, and
+// Compact records of the sorted particles: {jx0, jy0, lz0, lz0 mod M} (reading R-3), q, the
+// sorted index, and
 // per axis the Fast Gaussian Gridding factors of the first stencil node offset d0:
 //   A = e^{-alpha d0^2},  E = e^{-2 alpha h d0}   (node t: A E^t f1[t]).
 __global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, int64_t N,
@@ -658,7 +655,7 @@ __global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* _
   const double d0[3] = {((double)s.x - P2) * dv.h - pp.x, ((double)s.y - P2) * dv.h - pp.y, (double)s.z * dv.h - pp.z};
   double r[kRec];
   r[2] = pp.w;
-  r[3] = 0.0;
+  r[3] = __longlong_as_double((long long)i);   // the gather's slot index
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
     r[4 + 2 * ax] = exp(-dv.alpha * d0[ax] * d0[ax]);
