@@ -17,7 +17,7 @@
 
 namespace se1p {
 
-static int zcols(int M) { return M >= 256 ? 8 : (M >= 64 ? 16 : 32); }
+static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // columns (2 per FFT)
 static int rows_for(int W) { int r = 98304 / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? 4 : 8; }
 constexpr int kFftThreads = 256;   // threads per block of the FFT passes
@@ -25,47 +25,64 @@ constexpr int kFftThreads = 256;   // threads per block of the FFT passes
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
 // Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if
 // null) of the plane buffer in layout L (kspace.cuh, slab_row).
+// Two real z columns per complex FFT (columns 2r and 2r+1 of the block as z_r = col_2r + i col_2r+1):
+// their spectra separate as A[n] = (Z[n] + conj Z[M-n])/2, B[n] = (Z[n] - conj Z[M-n])/(2i).
 __global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   const int S = M + 1;   // padded row stride: the transposed accesses below stay conflict-free
+  const int CH = CB / 2;
   double2* buf = sm;
-  double2* tmp = sm + CB * S;
+  double2* tmp = sm + CH * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   const double* src = grid + ((int64_t)x * Mt + y0) * M;
+  double* bd = reinterpret_cast<double*>(buf);
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
-    const int c = idx / M;
-    buf[idx + c] = make_double2((y0 + c < Mt) ? src[idx] : 0.0, 0.0);
+    const int c = idx / M, k = idx - c * M;
+    bd[2 * ((c >> 1) * S + k) + (c & 1)] = (y0 + c < Mt) ? src[idx] : 0.0;
   }
   __syncthreads();
-  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CB, S, threadIdx.x, blockDim.x);
+  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
-    if (y0 + c < Mt) planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = out[c * S + n];
+    if (y0 + c < Mt) {
+      const double2 Z = out[(c >> 1) * S + n], Zm = out[(c >> 1) * S + (n ? M - n : 0)];
+      const double2 v = (c & 1) ? make_double2(0.5 * (Z.y + Zm.y), 0.5 * (Zm.x - Z.x))    // (Z - conj Zm)/(2i)
+                                : make_double2(0.5 * (Z.x + Zm.x), 0.5 * (Z.y - Zm.y));   // (Z + conj Zm)/2
+      planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = v;
+    }
   }
 }
 
+// Inverse: the Hermitian spectra a, b of columns 2r, 2r+1 combine into W[n] = a[n] + i b[n],
+// W[M-n] = conj a[n] + i conj b[n]; the complex inverse FFT gives col_2r + i col_2r+1.
 __global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   const int S = M + 1;   // padded row stride (conflict-free transposed accesses)
+  const int CH = CB / 2;
   double2* buf = sm;
-  double2* tmp = sm + CB * S;
+  double2* tmp = sm + CH * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
-  for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
-    const int n = idx / CB, c = idx - n * CB;
-    double2 v = (y0 + c < Mt) ? planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] : make_double2(0.0, 0.0);
-    buf[c * S + n] = v;
-    if (n > 0 && 2 * n < M) buf[c * S + (M - n)] = make_double2(v.x, -v.y);  // Hermitian half
+  for (int idx = threadIdx.x; idx < nplanes * CH; idx += blockDim.x) {
+    const int n = idx / CH, r = idx - n * CH;
+    const int64_t row = slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + 2 * r;
+    const double2 a = (y0 + 2 * r < Mt) ? planes[row] : make_double2(0.0, 0.0);
+    const double2 b = (y0 + 2 * r + 1 < Mt) ? planes[row + 1] : make_double2(0.0, 0.0);
+    buf[r * S + n] = make_double2(a.x - b.y, a.y + b.x);
+    if (n > 0 && 2 * n < M) buf[r * S + (M - n)] = make_double2(a.x + b.y, b.x - a.y);   // Hermitian half
   }
   __syncthreads();
-  double2* out = fft_rows<1>(buf, tmp, fz, tw, CB, S, threadIdx.x, blockDim.x);
+  double2* out = fft_rows<1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   double* dst = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
-    const int c = idx / M;
-    if (y0 + c < Mt) dst[idx] = out[idx + c].x;
+    const int c = idx / M, k = idx - c * M;
+    if (y0 + c < Mt) {
+      const double2 v = out[(c >> 1) * S + k];
+      dst[idx] = (c & 1) ? v.y : v.x;
+    }
   }
 }
 
@@ -168,7 +185,7 @@ void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
+  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zfwd, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
   k_zfwd<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
@@ -180,7 +197,7 @@ void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const Slab
   const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)CB * (M + 1) * sizeof(double2);
+  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zinv, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
   k_zinv<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
