@@ -64,6 +64,13 @@ def _load():
         lib.orc_phi_self.argtypes = [P, d, P, i64, P]
         lib.orc_phi_exact.argtypes = [P, P, i64, P, d, P, i64, P, P]
         lib.orc_phi_brute.argtypes = [P, P, i64, P, i64, P, i64, P]
+        lib.orc_dK0db.restype = d
+        lib.orc_dK0db.argtypes = [d, d]
+        lib.orc_field_real.argtypes = [P, P, i64, P, d, d, P, i64, P]
+        lib.orc_field_k3nz.argtypes = [P, P, i64, P, d, i32, P, i64, P]
+        lib.orc_field_k30.argtypes = [P, P, i64, P, d, P, i64, P]
+        lib.orc_field_exact.argtypes = [P, P, i64, P, d, P, i64, P, P]
+        lib.orc_field_brute.argtypes = [P, P, i64, P, i64, P, i64, P]
         lib.orc_modes_needed.restype = i32
         lib.orc_modes_needed.argtypes = [d, d]
         lib.orc_rc_converged.restype = d
@@ -185,6 +192,59 @@ def phi_kspace_reference(x, q, L, xi, targets=None):
     total: phi - phi^R(xi, converged) - phi^self(xi) (Eq. (2)).  Cheap at any xi."""
     tot = phi_exact(x, q, L, targets)
     return tot - phi_real(x, q, L, xi, None, targets) - phi_self(q, xi, targets)
+
+
+def dK0db(a, b):
+    """dK0(a,b)/db = -int_0^1 e^{-a/s - bs} ds (P:95 differentiated)."""
+    return _load().orc_dK0db(float(a), float(b))
+
+
+def _field(fn, x, q, L, targets, *args):
+    x, q, L, N, targets, _ = _prep(x, q, L, targets)
+    out = np.zeros((targets.size, 3))
+    fn(_p(x), _p(q), N, _p(L), *args, _p(targets), targets.size, _p(out))
+    return out
+
+
+def field_real(x, q, L, xi, rc, targets=None):
+    """E^R = -grad phi^R at each target (Eq. (3) differentiated), truncated at d <= rc (None: converged)."""
+    lib = _load()
+    if rc is None:
+        rc = lib.orc_rc_converged(float(xi))
+    return _field(lib.orc_field_real, x, q, L, targets, float(xi), float(rc))
+
+
+def field_k3nz(x, q, L, xi, J=None, targets=None):
+    lib = _load()
+    if J is None:
+        J = lib.orc_modes_needed(float(xi), float(np.asarray(L, dtype=float)[2]))
+    return _field(lib.orc_field_k3nz, x, q, L, targets, float(xi), int(J))
+
+
+def field_k30(x, q, L, xi, targets=None):
+    return _field(_load().orc_field_k30, x, q, L, targets, float(xi))
+
+
+def field_exact(x, q, L, targets=None, xi_o=0.0):
+    """E = -grad phi at each target (own charge excluded), converged at xi_o; force = q E."""
+    lib = _load()
+    x, q, L, N, targets, _ = _prep(x, q, L, targets)
+    out = np.zeros((targets.size, 3))
+    lib.orc_field_exact(_p(x), _p(q), N, _p(L), float(xi_o), _p(targets), targets.size, _p(out), None)
+    return out
+
+
+def field_brute(x, q, L, A, targets=None):
+    return _field(_load().orc_field_brute, x, q, L, targets, int(A))
+
+
+def field_brute_extrapolated(x, q, L, A=2000, targets=None):
+    return (4.0 * field_brute(x, q, L, 2 * A, targets) - field_brute(x, q, L, A, targets)) / 3.0
+
+
+def field_kspace_reference(x, q, L, xi, targets=None):
+    """E^F(xi) = E - E^R(xi, converged) (the self term has no gradient)."""
+    return field_exact(x, q, L, targets) - field_real(x, q, L, xi, None, targets)
 
 
 def rel_rms(a, ref):

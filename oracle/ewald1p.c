@@ -197,6 +197,42 @@ double orc_K0inc(double a, double b) {
   return 2.0 * orc_k0(2.0 * sqrt(a * b)) - k0_split(b, a, v);
 }
 
+/* dK0(a,b)/db = -int_0^1 e^{-a/s - b s} ds (differentiating P:95 under the integral after
+   s = 1/t).  The integrand is analytic on (0,1] with a boundary layer e^{-a/s} at 0 and its
+   peak at s* = sqrt(a/b); [0,1] is cut into pieces with endpoint ratio <= 2 around s*, each by
+   ORC_GL_N-point Gauss-Legendre (the construction of DESIGN.md reading R-10). */
+static double kd_piece(double a, double b, double lo, double hi) {
+  if (hi <= lo) return 0.0;
+  double half = 0.5 * (hi - lo), mid = 0.5 * (hi + lo);
+  nsum s = {0.0, 0.0};
+  for (int i = 0; i < ORC_GL_N; ++i) {
+    double t = mid + half * gl_x[i];
+    nsum_add(&s, gl_w[i] * exp(-a / t - b * t));
+  }
+  return half * nsum_get(&s);
+}
+
+double orc_dK0db(double a, double b) {
+  if (!gl_ready) gl_init();
+  if (!(a > 0.0) || b < 0.0) return NAN;
+  const double sstar = (b > 0.0) ? fmin(sqrt(a / b), 1.0) : 1.0;
+  double s = 0.0;
+  for (double lo = sstar; lo < 1.0;) {   /* [s*, 1] in doubling pieces */
+    double hi = fmin(2.0 * lo, 1.0);
+    s += kd_piece(a, b, lo, hi);
+    lo = hi;
+  }
+  double hi = sstar;                     /* [0, s*] in halving pieces */
+  for (int k = 0; k < 2000 && hi > 1e-300; ++k) {
+    double lo = 0.5 * hi;
+    double piece = kd_piece(a, b, lo, hi);
+    s += piece;
+    if (piece <= 1e-21 * fabs(s) || a / hi > 800.0) break;
+    hi = lo;
+  }
+  return -s;
+}
+
 /* ---------------------------------------------------------------- the sums */
 /* P_1 images: p = (0, 0, alpha L3).  Targets are indices into the same particle set
    (target points = charge locations, Alg. 1 step 6 P:270). */
@@ -324,5 +360,135 @@ void orc_phi_brute(const double* x, const double* q, int64_t N, const double* L,
       nsum_add(&s, q[n] * nsum_get(&sn));
     }
     out[it] = nsum_get(&s);
+  }
+}
+
+
+/* ---------------------------------------------------------------- fields (forces) */
+/* Electric field E = -grad phi at the target, the target's own charge excluded exactly as in
+   the potential (the force on particle m is q_m E(x_m), P:535-551 -- written here as the
+   gradients of Eqs. (3)-(5), not copied).  out[3*it + c], c = x, y, z. */
+
+/* E^R: -grad of q_n erfc(xi d)/d = q_n (erfc(xi d)/d + 2 xi/sqrt(pi) e^{-xi^2 d^2}) r/d^2, d <= rc. */
+void orc_field_real(const double* x, const double* q, int64_t N, const double* L, double xi,
+                    double rc, const int64_t* targets, int64_t m, double* out) {
+  const double L3 = L[2];
+  const int64_t A = (int64_t)ceil(rc / L3) + 1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t it = 0; it < m; ++it) {
+    const int64_t t = targets[it];
+    nsum s[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t alpha = -A; alpha <= A; ++alpha) {
+      for (int64_t n = 0; n < N; ++n) {
+        if (alpha == 0 && n == t) continue;
+        double r[3] = {x[3 * t] - x[3 * n], x[3 * t + 1] - x[3 * n + 1], x[3 * t + 2] - x[3 * n + 2] + alpha * L3};
+        double d2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2], d = sqrt(d2);
+        if (d > rc) continue;
+        double f = q[n] * (erfc(xi * d) / d + 2.0 * xi / sqrt(ORC_PI) * exp(-xi * xi * d2)) / d2;
+        for (int c = 0; c < 3; ++c) nsum_add(&s[c], f * r[c]);
+      }
+    }
+    for (int c = 0; c < 3; ++c) out[3 * it + c] = nsum_get(&s[c]);
+  }
+}
+
+/* E^{F,k3!=0} from Eq. (4b): phi = (2/L3) sum_j sum_n q_n cos(k dz) K0(a_j, xi^2 rho^2):
+   E_z = (2/L3) sum q_n k sin(k dz) K0,  E_r = -(2/L3) sum q_n cos(k dz) dK0/db 2 xi^2 (r_m - r_n). */
+void orc_field_k3nz(const double* x, const double* q, int64_t N, const double* L, double xi,
+                    int J, const int64_t* targets, int64_t m, double* out) {
+  if (!gl_ready) gl_init();
+  const double L3 = L[2];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t it = 0; it < m; ++it) {
+    const int64_t t = targets[it];
+    nsum s[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int j = 1; j <= J; ++j) {
+      const double k3 = 2.0 * ORC_PI * j / L3;
+      const double a = k3 * k3 / (4.0 * xi * xi);
+      for (int64_t n = 0; n < N; ++n) {
+        double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
+        double dz = x[3 * t + 2] - x[3 * n + 2];
+        double b = xi * xi * (dx * dx + dy * dy);
+        nsum_add(&s[2], q[n] * 2.0 * k3 * sin(k3 * dz) * orc_K0inc(a, b));
+        if (b > 0.0) {
+          double g = -q[n] * 2.0 * cos(k3 * dz) * orc_dK0db(a, b) * 2.0 * xi * xi;
+          nsum_add(&s[0], g * dx);
+          nsum_add(&s[1], g * dy);
+        }
+      }
+    }
+    for (int c = 0; c < 3; ++c) out[3 * it + c] = nsum_get(&s[c]) / L3;
+  }
+}
+
+/* E^{F,k3=0} from Eq. (5): phi = -(1/L3) sum_{n!=m} q_n g(xi^2 rho^2), g'(u) = (1 - e^{-u})/u:
+   E_r = (1/L3) sum q_n g'(u) 2 xi^2 (r_m - r_n), E_z = 0. */
+void orc_field_k30(const double* x, const double* q, int64_t N, const double* L, double xi,
+                   const int64_t* targets, int64_t m, double* out) {
+  const double L3 = L[2];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t it = 0; it < m; ++it) {
+    const int64_t t = targets[it];
+    nsum s[2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t n = 0; n < N; ++n) {
+      if (n == t) continue;
+      double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
+      double u = xi * xi * (dx * dx + dy * dy);
+      double gp = (u < 1e-8) ? 1.0 - 0.5 * u : -expm1(-u) / u;
+      double f = q[n] * gp * 2.0 * xi * xi;
+      nsum_add(&s[0], f * dx);
+      nsum_add(&s[1], f * dy);
+    }
+    out[3 * it] = nsum_get(&s[0]) / L3;
+    out[3 * it + 1] = nsum_get(&s[1]) / L3;
+    out[3 * it + 2] = 0.0;
+  }
+}
+
+/* Full field at the oracle's xi_o, converged (independent of xi_o like the potential).
+   comps (optional, 9*m): R, k3!=0, k3=0 (3 components each). */
+void orc_field_exact(const double* x, const double* q, int64_t N, const double* L, double xi_o,
+                     const int64_t* targets, int64_t m, double* out, double* comps) {
+  if (xi_o <= 0.0) xi_o = 0.7 / L[2];
+  double* r = (double*)malloc(sizeof(double) * 9 * (size_t)m);
+  orc_field_real(x, q, N, L, xi_o, orc_rc_converged(xi_o), targets, m, r);
+  orc_field_k3nz(x, q, N, L, xi_o, orc_modes_needed(xi_o, L[2]), targets, m, r + 3 * m);
+  orc_field_k30(x, q, N, L, xi_o, targets, m, r + 6 * m);
+  for (int64_t i = 0; i < m; ++i)
+    for (int c = 0; c < 3; ++c) {
+      nsum s = {0.0, 0.0};
+      for (int k = 0; k < 3; ++k) nsum_add(&s, r[k * 3 * m + 3 * i + c]);
+      out[3 * i + c] = nsum_get(&s);
+      if (comps)
+        for (int k = 0; k < 3; ++k) comps[9 * i + 3 * k + c] = r[k * 3 * m + 3 * i + c];
+    }
+  free(r);
+}
+
+/* The definition: E = sum_alpha sum'_n q_n r / |r|^3, r = x_m - x_n - alpha L3 e3, |alpha| <= A
+   (symmetric; callers extrapolate in A). */
+void orc_field_brute(const double* x, const double* q, int64_t N, const double* L, int64_t A,
+                     const int64_t* targets, int64_t m, double* out) {
+  const double L3 = L[2];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t it = 0; it < m; ++it) {
+    const int64_t t = targets[it];
+    nsum s[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t n = 0; n < N; ++n) {
+      double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
+      double dz0 = x[3 * t + 2] - x[3 * n + 2];
+      double rho2 = dx * dx + dy * dy;
+      nsum sn[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int64_t alpha = A; alpha >= -A; --alpha) {
+        if (alpha == 0 && n == t) continue;
+        double dz = dz0 + alpha * L3;
+        double d2 = rho2 + dz * dz, inv3 = 1.0 / (d2 * sqrt(d2));
+        nsum_add(&sn[0], dx * inv3);
+        nsum_add(&sn[1], dy * inv3);
+        nsum_add(&sn[2], dz * inv3);
+      }
+      for (int c = 0; c < 3; ++c) nsum_add(&s[c], q[n] * nsum_get(&sn[c]));
+    }
+    for (int c = 0; c < 3; ++c) out[3 * it + c] = nsum_get(&s[c]);
   }
 }
