@@ -98,8 +98,10 @@ def mode_extent(nprime, n_l, S0, SI, SJ):
     return SJ
 
 
-def se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, eta=None, return_all=False):
-    """phi^F(x_m) = phi^{F,k3!=0} + phi^{F,k3=0} by Alg. 1."""
+def se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, eta=None, return_all=False, return_field=False):
+    """phi^F(x_m) = phi^{F,k3!=0} + phi^{F,k3=0} by Alg. 1; with return_field also the
+    k-space field E^F = -grad phi^F at the particles (the SE force is the gradient of the gather,
+    Eq. (force_se1p); the constant follows reading R-1)."""
     x = np.asarray(x, dtype=np.float64)
     q = np.asarray(q, dtype=np.float64)
     d = derived(L, xi, M, P, eta)
@@ -134,21 +136,36 @@ def se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, eta=None, return_all=False):
     Htil = np.fft.ifft(Ht, axis=2).real
 
     # step 6: gather (reading R-1 for the constant)
+    phi, E = _gather(x, Htil, xi, d["h"], P, M, Mt2, eta, field=return_field)
+    if return_field:
+        return (phi, E, dict(H=H, Htilde=Htil, derived=d, R=R)) if return_all else (phi, E)
+    if return_all:
+        return phi, dict(H=H, Htilde=Htil, derived=d, R=R)
+    return phi
+
+
+def _gather(x, Htil, xi, h, P, M, Mt2, eta, field=False):
+    """Step 6: phi(x_m) = C sum H~ wx wy wz (Eq. (se1p_complete_discretized), reading R-1), and with
+    `field` the electric field E = -grad phi: d/dx_m e^{-alpha (node - x_m)^2} = 2 alpha (node - x_m) w."""
     alpha = 2.0 * xi ** 2 / eta
     pref = (2.0 * xi ** 2 / (math.pi * eta)) ** 1.5
     C = 4.0 * math.pi * h ** 3 * pref
-    phi = np.empty(q.size)
+    phi = np.empty(x.shape[0])
+    E = np.empty((x.shape[0], 3)) if field else None
     flat = Htil.ravel()
-    for s in range(0, q.size, 2048):
+    for s in range(0, x.shape[0], 2048):
         xs = x[s:s + 2048]
         jx, jy, lz, dx, dy, dz = _stencils(xs, h, P, M)
         wx, wy, wz = np.exp(-alpha * dx ** 2), np.exp(-alpha * dy ** 2), np.exp(-alpha * dz ** 2)
         idx = (jx[:, :, None, None] * Mt2 + jy[:, None, :, None]) * M + lz[:, None, None, :]
-        w = wx[:, :, None, None] * wy[:, None, :, None] * wz[:, None, None, :]
-        phi[s:s + 2048] = C * np.sum(flat[idx] * w, axis=(1, 2, 3))
-    if return_all:
-        return phi, dict(H=H, Htilde=Htil, derived=d, R=R)
-    return phi
+        Hs = flat[idx]
+        phi[s:s + 2048] = C * np.einsum("ni,nj,nk,nijk->n", wx, wy, wz, Hs)
+        if field:
+            gx, gy, gz = 2 * alpha * dx * wx, 2 * alpha * dy * wy, 2 * alpha * dz * wz
+            E[s:s + 2048, 0] = -C * np.einsum("ni,nj,nk,nijk->n", gx, wy, wz, Hs)
+            E[s:s + 2048, 1] = -C * np.einsum("ni,nj,nk,nijk->n", wx, gy, wz, Hs)
+            E[s:s + 2048, 2] = -C * np.einsum("ni,nj,nk,nijk->n", wx, wy, gz, Hs)
+    return phi, E
 
 
 def extents_from_factors(Mt, s0, sl, SJ=None):

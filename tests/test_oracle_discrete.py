@@ -114,3 +114,19 @@ def test_table1_error_levels(row):
     ref = _kspace_exact(x, q, L, xi)
     err = math.sqrt(np.mean((phi - ref) ** 2))
     assert err_paper / 10 <= err <= err_paper * 10, (err, err_paper)
+
+
+def test_alg1_field_matches_exact_field():
+    """The SE k-space field (gradient of the gather, Eq. (force_se1p)) converges to the
+    exact k-space field -grad(phi^{F,k3!=0} + phi^{F,k3=0}) like the potential (Thm 1)."""
+    L = (1.0, 1.0, 1.0)
+    x, q = make_system(60, L, 31)
+    xi, M = 6.0, 24
+    ref = oracle.field_kspace_reference(x, q, L, xi)
+    errs = []
+    for P in [8, 12, 18]:
+        Mt = M + P
+        _, E = sd.se1p_kspace(x, q, L, xi, M, P, M // 2, 6 * Mt, 6 * Mt, 2 * Mt, return_field=True)
+        errs.append(np.sqrt(np.mean((E - ref) ** 2) / np.mean(ref ** 2)))
+    assert all(b < a / 20 for a, b in zip(errs, errs[1:]))
+    assert errs[-1] < 1e-9
