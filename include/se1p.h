@@ -153,6 +153,25 @@ int se1p_real(const double* x, const double* q, int64_t N, const double L[3], do
 int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
                  int64_t N, const double L[3], double xi, double rc, double* phi_out);
 
+/* Electric field E = -grad phi at the particles (force on particle n: F_n = q_n E_n), the
+   derivative the paper's force expressions take: SURVEY.md 8(f) NEXT-1.
+   se1p_kspace_field_ex: the k-space field E^F = -grad phi^F of Alg. 1 -- the same grid H~
+     (steps 1-5) gathered with the gradient of the Gaussian window (step 6 differentiated,
+     P:270-275: d/dx_n e^{-alpha|x-x_n|^2} = 2 alpha (x - x_n) e^{-alpha|x-x_n|^2}).
+   se1p_real_field_ex: E^R = -grad phi^R of Eq. (3) with the same truncation as se1p_real
+     (the self term has no gradient).
+   field_out: [N][3] doubles (x, y, z components) in the caller's particle order, required;
+   phi_out: N doubles or NULL -- when given, the potential of the matching non-field call is
+   written too (same values).  Arguments, ownership, opts and errors as the _ex entries above.
+   The k-space field runs on the tile kernels only (opts->reserved[2] == 1 -> SE1P_EINVAL). */
+int se1p_kspace_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                         int64_t N, const double L[3], double xi, int M, int P, double eta,
+                         double s0, double sf, int n_local, double* phi_out, double* field_out);
+
+int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                       int64_t N, const double L[3], double xi, double rc, double* phi_out,
+                       double* field_out);
+
 /* Resolve the plan the k-space call with these arguments would use (no device work
    beyond plan creation).  Returns SE1P_OK or the same errors as se1p_kspace_ex. */
 int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P,

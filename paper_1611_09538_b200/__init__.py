@@ -25,7 +25,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EDOMAIN", 3: "ENONNEUTRAL", 4: "EPARAM", 5: 
 EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query",
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
-           "se1p_kspace_slab_backward"]
+           "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex"]
 
 
 class SE1PError(RuntimeError):
@@ -67,6 +67,8 @@ def load(build_if_needed: bool = True):
     lib.se1p_kspace_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_real.argtypes = [vp, vp, i64, vp, d, d, vp]
     lib.se1p_real_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, d, vp]
+    lib.se1p_kspace_field_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
+    lib.se1p_real_field_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, d, vp, vp]
     lib.se1p_plan_query.argtypes = [ctypes.POINTER(Opts), vp, d, i32, i32, d, d, d, i32, ctypes.POINTER(PlanInfo)]
     lib.se1p_last_stage_times.argtypes = [vp, i32]
     lib.se1p_last_launch_count.restype = i32
@@ -141,45 +143,66 @@ def _neg(v, default=-1.0):
     return default if v is None else float(v)
 
 
+def _outputs(x, N, field, out, field_out):
+    """Output buffers on the inputs' side (numpy for host I/O, CUDA tensors otherwise)."""
+    if isinstance(x, np.ndarray):
+        out = np.zeros(N) if out is None else out
+        fo = (np.zeros((N, 3)) if field_out is None else field_out) if field else None
+        return out, fo, out.ctypes.data, (fo.ctypes.data if field else None)
+    import torch
+    out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
+    fo = (torch.empty(N, 3, dtype=torch.float64, device=x.device) if field_out is None else field_out) if field else None
+    return out, fo, out.data_ptr(), (fo.data_ptr() if field else None)
+
+
 def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
            out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0,
-           reference_kernels=False):
+           reference_kernels=False, field=False, field_out=None):
     """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1).
+    field=True returns (phi^F, E^F) with E^F = -grad phi^F, [N,3] (forces q E).
     reference_kernels=True selects the simple v1 gridding/gather kernels (A/B testing)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
-    if host:
-        out = np.zeros(N) if out is None else out
-        optr = out.ctypes.data
-    else:
-        import torch
-        out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
-        optr = out.data_ptr()
+    out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
     o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels)
-    _check(lib.se1p_kspace_ex(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
-                              _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr))
+    args = (ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
+            _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr)
+    if field:
+        _check(lib.se1p_kspace_field_ex(*args, fptr))
+        return out, fo
+    _check(lib.se1p_kspace_ex(*args))
     return out
 
 
-def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False):
-    """phi^R + phi^self (Eq. (3) truncated at rc, Eq. (6))."""
+def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False, field=False, field_out=None):
+    """phi^R + phi^self (Eq. (3) truncated at rc, Eq. (6)).
+    field=True returns (phi^R + phi^self, E^R), E^R = -grad phi^R, [N,3]."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
-    if host:
-        out = np.zeros(N) if out is None else out
-        optr = out.ctypes.data
-    else:
-        import torch
-        out = torch.empty(N, dtype=torch.float64, device=x.device) if out is None else out
-        optr = out.data_ptr()
+    out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
     o = _opts(host_io=host, skip_checks=skip_checks, sync=sync)
-    _check(lib.se1p_real_ex(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr))
+    args = (ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr)
+    if field:
+        _check(lib.se1p_real_field_ex(*args, fptr))
+        return out, fo
+    _check(lib.se1p_real_ex(*args))
     return out
 
 
 def potential(x, q, L, xi, rc, M, P, **kw):
     """Full singly periodic potential phi = phi^F + phi^R + phi^self (Eq. (2))."""
     return kspace(x, q, L, xi, M, P, **kw) + real(x, q, L, xi, rc)
+
+
+def energy_forces(x, q, L, xi, rc, M, P, **kw):
+    """(U, phi, F): the electrostatic energy U = 1/2 sum_n q_n phi_n, the potentials and the forces
+    F_n = q_n E_n, E = E^F + E^R (Eq. (2) and its gradient)."""
+    pk, ek = kspace(x, q, L, xi, M, P, field=True, **kw)
+    pr, er = real(x, q, L, xi, rc, field=True)
+    phi, E = pk + pr, ek + er
+    U = 0.5 * float((q * phi).sum())
+    F = E * (q[:, None] if not isinstance(q, np.ndarray) else np.asarray(q)[:, None])
+    return U, phi, F
 
 
 def _ints(v):

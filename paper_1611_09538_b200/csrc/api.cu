@@ -225,8 +225,8 @@ static void sync_and_check(cudaStream_t st) {
 
 static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
                         const double L[3], double xi, int M, int P, double eta, double s0, double sf, int n_local,
-                        double* phi_out) {
-  if (!x || !q || !phi_out) throw Error{1, "null pointer"};
+                        double* phi_out, double* field_out = nullptr) {
+  if (!x || !q || (!phi_out && !field_out)) throw Error{1, "null pointer"};
   if (N < 1) throw Error{1, "N must be >= 1"};
   if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
   const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
@@ -239,13 +239,16 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   grow(w.planes, w.planes_cap, (int64_t)pl->n_planes * dv.Mt * dv.Mt);
   grow(w.T, w.T_cap, pl->t_off_total);
   const bool host_io = o && o->host_io;
+  const bool field = field_out != nullptr;
   const double *dx = x, *dq = q;
   double* dphi = phi_out;
+  double* dfield = field_out;
   if (host_io) {
-    grow(ds.dx, ds.io_cap, 5 * N);
+    grow(ds.dx, ds.io_cap, 8 * N);
     dx = ds.dx;
     dq = ds.dx + 3 * N;
-    dphi = ds.dx + 4 * N;
+    dphi = phi_out ? ds.dx + 4 * N : nullptr;
+    dfield = field ? ds.dx + 5 * N : nullptr;
     SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
     SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
   }
@@ -254,8 +257,9 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   const int stop = o ? o->reserved[1] : 0;
   const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
+  if (field && v1) throw Error{1, "the field is computed by the tile kernels only"};
   if (!v1) {
-    grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+    grow(w.gpart, w.gpart_cap, N * gather_slots(dv) * (field ? 4 : 1));
     grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
   }
   // stages (se1p_last_stage_times): bin, records, spread, zfft, modes, izfft, gather, finish
@@ -279,11 +283,16 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   tm.mark();
   if (stop == 4) return sync_and_check(st);
   if (v1) k_gather(*pl, w, N, dphi, st);
-  else k_gather_tiles(*pl, w, N, st);
+  else {
+    if (field) k_records_stage(*pl, w, N, st, true);   // field records add the position
+    k_gather_tiles(*pl, w, N, st, 0, -1, field);
+  }
   tm.mark();
-  if (!v1) k_gather_finish_stage(*pl, w, N, dphi, st);
+  if (!v1) k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
   tm.mark();
-  if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  if (host_io && phi_out) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  if (host_io && field)
+    SE1P_CUDA_TRY(cudaMemcpyAsync(field_out, dfield, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));
   tm.finish();
   if (!o || o->sync || host_io) {
     SE1P_CUDA_TRY(cudaStreamSynchronize(st));
@@ -295,8 +304,8 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
 }
 
 static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
-                      const double L[3], double xi, double rc, double* phi_out) {
-  if (!x || !q || !phi_out || !L) throw Error{1, "null pointer"};
+                      const double L[3], double xi, double rc, double* phi_out, double* field_out = nullptr) {
+  if (!x || !q || (!phi_out && !field_out) || !L) throw Error{1, "null pointer"};
   if (N < 1) throw Error{1, "N must be >= 1"};
   if (!(xi > 0) || !(rc > 0) || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "xi, rc, L must be > 0"};
   const RDev d = real_geometry(L, xi, rc);
@@ -306,17 +315,22 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   const bool host_io = o && o->host_io;
   const double *dx = x, *dq = q;
   double* dphi = phi_out;
+  double* dfield = field_out;
   if (host_io) {
-    grow(ds.dx, ds.io_cap, 5 * N);
+    grow(ds.dx, ds.io_cap, 8 * N);
     dx = ds.dx;
     dq = ds.dx + 3 * N;
-    dphi = ds.dx + 4 * N;
+    dphi = phi_out ? ds.dx + 4 * N : nullptr;
+    dfield = field_out ? ds.dx + 5 * N : nullptr;
     SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
     SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
   }
   if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, false, st);
-  real_space(d, w, dx, dq, N, dphi, st);
-  if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  real_space(d, w, dx, dq, N, dphi, st, dfield);
+  if (host_io && phi_out)
+    SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  if (host_io && field_out)
+    SE1P_CUDA_TRY(cudaMemcpyAsync(field_out, dfield, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));
   if (!o || o->sync || host_io) SE1P_CUDA_TRY(cudaStreamSynchronize(st));
   SE1P_CUDA_TRY(cudaGetLastError());
 }
@@ -513,6 +527,27 @@ int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const dou
     se1p_opts o{};
     if (opts) o = *opts;
     real_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, rc, phi_out);
+  });
+}
+
+int se1p_kspace_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                         const double L[3], double xi, int M, int P, double eta, double s0, double sf, int n_local,
+                         double* phi_out, double* field_out) {
+  return guarded([&] {
+    if (!field_out) throw Error{1, "null pointer"};
+    se1p_opts o{};
+    if (opts) o = *opts;
+    kspace_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, s0, sf, n_local, phi_out, field_out);
+  });
+}
+
+int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                       const double L[3], double xi, double rc, double* phi_out, double* field_out) {
+  return guarded([&] {
+    if (!field_out) throw Error{1, "null pointer"};
+    se1p_opts o{};
+    if (opts) o = *opts;
+    real_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, rc, phi_out, field_out);
   });
 }
 

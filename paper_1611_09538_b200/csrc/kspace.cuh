@@ -116,12 +116,14 @@ void kplan_release_all();
 // Stages (launch on st).
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
 void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
-void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);   // tiles.cu
+void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field = false);   // tiles.cu
 // DMMA tile kernels over x tiles [tx_lo, tx_hi) (tx_hi < 0: all), tiles of 16 grid rows
 void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1);
-void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1);
+// field: also E = -grad phi (3 doubles per particle, user order) -- the gradient of the gather
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1,
+                    bool field = false);
 void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st, int tx_lo = 0,
-                           int tx_hi = -1);
+                           int tx_hi = -1, double* field = nullptr);
 int64_t gather_slots(const KDev& dv);
 void slot_geometry(KDev& dv);
 int tile_tz(int M);

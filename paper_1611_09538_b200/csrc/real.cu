@@ -37,9 +37,12 @@ __global__ void k_real_permute(RDev d, const double* __restrict__ x, const doubl
 }
 
 // One thread per target (sorted order, so neighbouring threads share cells).
+// FIELD: also E^R = -grad_m phi^R = sum_n q_n (erfc(xi r)/r + 2 xi/sqrt(pi) e^{-xi^2 r^2}) r_vec/r^2,
+// r_vec = x_m - x_n - alpha L3 e3 (Eq. (3) differentiated; the self term has no gradient).
+template <bool FIELD>
 __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restrict__ P4, const int* __restrict__ perm,
                                                   const int* __restrict__ cell_start, int64_t N,
-                                                  double* __restrict__ phi_out) {
+                                                  double* __restrict__ phi_out, double* __restrict__ field_out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= N) return;
   const double4 pt = P4[t];
@@ -47,7 +50,7 @@ __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restr
   const int cy = min(max((int)floor(pt.y / d.cs[1]), 0), d.nc[1] - 1);
   const int cz = min(max((int)floor(pt.z / d.cs[2]), 0), d.nc[2] - 1);
   const double rc2 = d.rc * d.rc;
-  double acc = 0.0;
+  double acc = 0.0, ex = 0.0, ey = 0.0, ez = 0.0;
   for (int ax = max(0, cx - 1); ax <= min(d.nc[0] - 1, cx + 1); ++ax)
     for (int ay = max(0, cy - 1); ay <= min(d.nc[1] - 1, cy + 1); ++ay)
       for (int u = cz - d.K; u <= cz + d.K; ++u) {
@@ -63,11 +66,25 @@ __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restr
           const double r2 = dx * dx + dy * dy + dz * dz;
           if (r2 <= rc2) {
             const double r = sqrt(r2);
-            acc = fma(ps.w, erfc(d.xi * r) / r, acc);
+            const double ec = erfc(d.xi * r) / r;
+            acc = fma(ps.w, ec, acc);
+            if (FIELD) {
+              const double g = ps.w * (ec + 1.128379167095512573896158903121545172 * d.xi *   // 2/sqrt(pi)
+                                                exp(-d.xi * d.xi * r2)) / r2;
+              ex = fma(g, dx, ex);
+              ey = fma(g, dy, ey);
+              ez = fma(g, dz, ez);
+            }
           }
         }
       }
-  phi_out[perm[t]] = acc - 2.0 * d.xi * pt.w * 0.564189583547756286948079451560772586;  // 1/sqrt(pi)
+  const int64_t u = perm[t];
+  if (phi_out) phi_out[u] = acc - 2.0 * d.xi * pt.w * 0.564189583547756286948079451560772586;  // 1/sqrt(pi)
+  if (FIELD) {
+    field_out[3 * u] = ex;
+    field_out[3 * u + 1] = ey;
+    field_out[3 * u + 2] = ez;
+  }
 }
 
 RDev real_geometry(const double L[3], double xi, double rc) {
@@ -85,7 +102,7 @@ RDev real_geometry(const double L[3], double xi, double rc) {
 }
 
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
-                cudaStream_t st) {
+                cudaStream_t st, double* field_out) {
   const int ncell = d.nc[0] * d.nc[1] * d.nc[2];
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
@@ -93,7 +110,11 @@ void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64
   stable_bin_sort(w.keys, N, ncell, w.perm, w.bin_start, w.scratch, st);
   k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
   SE1P_LAUNCH_CHECK();
-  k_real_sum<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out);
+  const unsigned nt = (unsigned)ceil_div(N, 128);
+  if (field_out)
+    k_real_sum<true><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out, field_out);
+  else
+    k_real_sum<false><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out, nullptr);
   SE1P_LAUNCH_CHECK();
 }
 

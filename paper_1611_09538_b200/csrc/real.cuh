@@ -17,6 +17,6 @@ struct RDev {
 
 RDev real_geometry(const double L[3], double xi, double rc);
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
-                cudaStream_t st);
+                cudaStream_t st, double* field_out = nullptr);
 
 }  // namespace se1p

@@ -35,10 +35,13 @@
 namespace se1p {
 
 constexpr int kCW = 16;                          // consumer warps
-constexpr int kEW = 8;                           // expander warps
-constexpr int kThreads = (kCW + 1 + kEW) * 32;   // + producer
+// expander warps: 8, or 4 for the field gather (32-particle batches, more consumer registers)
+__host__ __device__ constexpr int n_exp_warps(bool field) { return field ? 4 : 8; }
+__host__ __device__ constexpr int n_threads(bool field) { return (kCW + 1 + n_exp_warps(field)) * 32; }
 constexpr int kMaxNB = 4;
-constexpr int kRec = 10;                         // doubles per compact record (80 B)
+// doubles per compact record: {s4, q, index, (A, E) per axis} (80 B); the field gather adds the
+// particle position (112 B)
+__host__ __device__ constexpr int rec_len(bool field) { return field ? 14 : 10; }
 constexpr int kMaxP = 64;
 constexpr int kEntB = 7, kEntZ = 9;              // gridding list entry: p (7 bits), buffer (2), z mask
 
@@ -46,13 +49,17 @@ constexpr int kEntB = 7, kEntZ = 9;              // gridding list entry: p (7 bi
 // (17 apart: when 8 particles x 4 segments are written by one warp, the 32 lanes fall into
 // distinct bank pairs); row stride = 4 (mod 16) doubles, so the 4 particles of a consumer
 // k-step start 4 banks apart.
-__host__ __device__ constexpr int exp_stride(int TZ) { return TZ == 32 ? 68 : 52; }
+// The field gather appends the z-derivative window wz'[j] = 2 alpha (node - z_p) wz[j] at 68 and 85.
+__host__ __device__ constexpr int exp_stride(int TZ, bool field = false) {
+  return field ? (TZ == 32 ? 116 : 68) : (TZ == 32 ? 68 : 52);
+}
 constexpr int kEX = 0, kEY = 17, kEZ = 34;
 __host__ __device__ constexpr int zoff(int j) { return kEZ + j + (j >= 16 ? 1 : 0); }   // wz[j]
+__host__ __device__ constexpr int zoffd(int TZ, int j) { return (TZ == 32 ? 68 : 51) + j + (j >= 16 ? 1 : 0); }
 
 struct TileArgs {
   KDev dv;
-  const double* rec;      // compact records [N][kRec]
+  const double* rec;      // compact records [N][rec_len]
   const int* bin_start;
   const double* f1;
   double* grid;
@@ -65,7 +72,7 @@ struct TileSmem {
   int off_lists, off_acc, off_raw, off_exp, total;
 };
 
-__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather) {
+__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather, bool field = false) {
   TileSmem s;
   int o = 4 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
   o = (o + 15) & ~15;
@@ -73,13 +80,13 @@ __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gathe
   o += kCW * (BM + 32) * 4;
   o = (o + 15) & ~15;
   s.off_acc = o;
-  if (gather) o += NB * BM * (kCW + 1) * 8;
+  if (gather) o += NB * BM * (kCW + 1) * (field ? 4 : 1) * 8;
   o = (o + 127) & ~127;
   s.off_raw = o;
-  o += NB * BM * kRec * 8;
+  o += NB * BM * rec_len(field) * 8;
   o = (o + 127) & ~127;
   s.off_exp = o;
-  o += NB * (BM + 1) * exp_stride(TZ) * 8;
+  o += NB * (BM + 1) * exp_stride(TZ, field) * 8;
   s.total = o;
   return s;
 }
@@ -144,14 +151,18 @@ __device__ __forceinline__ int zmask_of(int d, int P, int M, int jmax) {
   return zm;
 }
 
-template <int TZ, bool GATHER>
-__global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
+// FIELD (gather only): also the field E = -grad phi at the particles -- the gradient of the
+// gather (Eq. (force_se1p)): d/dx_p e^{-alpha (node - x_p)^2} = 2 alpha (node - x_p) w.
+template <int TZ, bool GATHER, bool FIELD = false>
+__global__ void __launch_bounds__(n_threads(FIELD), 1) k_tiles(const TileArgs A) {
   constexpr int NZB = TZ / 8;
-  constexpr int RSE = exp_stride(TZ);
+  constexpr int RSE = exp_stride(TZ, FIELD);
+  constexpr int kEW = n_exp_warps(FIELD), kThreads = n_threads(FIELD), kRec = rec_len(FIELD);
+  constexpr int NC = FIELD ? 4 : 1;   // gather outputs per particle: phi (and d/dx, d/dy, d/dz)
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
-  const TileSmem L = tile_smem(BM, NB, TZ, GATHER);
+  const TileSmem L = tile_smem(BM, NB, TZ, GATHER, FIELD);
   uint64_t* rawb = reinterpret_cast<uint64_t*>(smem);
   uint64_t* full = rawb + kMaxNB;
   uint64_t* empty = full + kMaxNB;
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tiles(const TileArgs A) {
   for (int b = 0; b < NB; ++b)
     for (int k = tid; k < RSE; k += kThreads) exps[b * ES + BM * RSE + k] = 0.0;
   if (GATHER)
-    for (int k = tid; k < NB * BM * (kCW + 1); k += kThreads) acc[k] = 0.0;
+    for (int k = tid; k < NB * BM * (kCW + 1) * NC; k += kThreads) acc[k] = 0.0;
   __syncthreads();
 
   const int nslot = dv.nslot;
@@ -193,21 +204,24 @@ auto reduce = [&](int b, int rt) {
     const double* rb = raws + b * BM * kRec;
     for (int p = rt; p < c; p += 32 * kEW) {
       const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
-      double* ap = acc + (b * BM + p) * (kCW + 1);
+      double* ap = acc + (b * BM + p) * (kCW + 1) * NC;
       const bool hx = s.x <= X0 + kTXY - 1 && s.x + P - 1 >= X0 && s.y <= Y0 + kTXY - 1 && s.y + P - 1 >= Y0;
       const int sz = hx ? zslot(s.w, P, M, TZ, tz) : -1;
       if (sz >= 0) {
-        double sum = 0.0;
-#pragma unroll
-        for (int v = 0; v < kCW; ++v) {
-          sum += ap[v];
-          ap[v] = 0.0;
-        }
         const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
         const int64_t i = __double_as_longlong(rb[p * kRec + 3]);   // sorted index (k_records)
-        A.gpart[i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz] = sum;
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double sum = 0.0;
+#pragma unroll
+          for (int v = 0; v < kCW; ++v) {
+            sum += ap[v * NC + cc];
+            ap[v * NC + cc] = 0.0;
+          }
+          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NC + cc] = sum;
+        }
       } else if (hx) {
-        for (int v = 0; v < kCW; ++v)
+        for (int v = 0; v < kCW * NC; ++v)
           if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
       }
     }
@@ -327,6 +341,7 @@ auto reduce = [&](int b, int rt) {
           const double E = r[5 + 2 * ax];
           int t, lim, Mw;
           double* o = eb + p * RSE;
+          double* od = nullptr;   // field: z-derivative window 2 alpha (node - z_p) wz
           if (ax < 2) {
             t = ax == 0 ? X0 - s.x : Y0 - s.y;
             lim = 16;
@@ -339,6 +354,7 @@ auto reduce = [&](int b, int rt) {
             if (t >= M) t -= M;
             lim = jmax - i0;
             Mw = M;
+            if (FIELD) od = o + zoffd(TZ, i0);
             o += zoff(i0);
           }
           // two interleaved chains of 8 entries: entries 0..7 from node t, 8..15 from node t + 8
@@ -367,6 +383,7 @@ auto reduce = [&](int b, int rt) {
                 g[c] *= E;
               }
               o[8 * c + i] = v;
+              if (FIELD && od) od[8 * c + i] = 2.0 * dv.alpha * ((double)(s.z + tt) * dv.h - r[12]) * v;
               if (++tc[c] == Mw) {   // periodic wrap: the stencil restarts at node 0
                 tc[c] = 0;
                 g[c] = A0;
@@ -576,27 +593,60 @@ auto reduce = [&](int b, int rt) {
         const double* z0 = r0 + tig;
         const double* z1 = r1 + tig;
         double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
+        double u0[4] = {0.0, 0.0, 0.0, 0.0}, u1[4] = {0.0, 0.0, 0.0, 0.0};   // field: wz' H~
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
           if ((zm >> zb) & 1) {
             const double a[4] = {z0[zoff(8 * zb)], z1[zoff(8 * zb)], z0[zoff(8 * zb + 4)], z1[zoff(8 * zb + 4)]};
             dmma_16x8x8(t0, a, hB[zb][0][0], hB[zb][0][1]);
             dmma_16x8x8(t1, a, hB[zb][1][0], hB[zb][1][1]);
+            if (FIELD) {
+              const double ad[4] = {z0[zoffd(TZ, 8 * zb)], z1[zoffd(TZ, 8 * zb)], z0[zoffd(TZ, 8 * zb + 4)],
+                                    z1[zoffd(TZ, 8 * zb + 4)]};
+              dmma_16x8x8(u0, ad, hB[zb][0][0], hB[zb][0][1]);
+              dmma_16x8x8(u1, ad, hB[zb][1][0], hB[zb][1][1]);
+            }
           }
         }
-        const double v0 = r0[kEY + cy0] * fma(r0[kEX + cx0], t0[0], r0[kEX + cx0 + 1] * t0[1]) +
-                          r0[kEY + cy0 + 2] * fma(r0[kEX + cx0], t1[0], r0[kEX + cx0 + 1] * t1[1]);
-        const double v1 = r1[kEY + cy0] * fma(r1[kEX + cx0], t0[2], r1[kEX + cx0 + 1] * t0[3]) +
-                          r1[kEY + cy0 + 2] * fma(r1[kEX + cx0], t1[2], r1[kEX + cx0 + 1] * t1[3]);
-        double v[2] = {v0, v1};
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 2);
+        // phi_p = sum_cols wx wy T; field: d/dx uses wx' = 2 alpha (node_x - x_p) wx, d/dy likewise,
+        // d/dz the wz'-transformed U (the particles' positions sit in their raw records)
+        double v[2][NC];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double* r = h ? r1 : r0;
+          const double* tt0 = t0 + 2 * h;
+          const double* tt1 = t1 + 2 * h;
+          const double wx0 = r[kEX + cx0], wx1 = r[kEX + cx0 + 1], wy0 = r[kEY + cy0], wy2 = r[kEY + cy0 + 2];
+          v[h][0] = wy0 * fma(wx0, tt0[0], wx1 * tt0[1]) + wy2 * fma(wx0, tt1[0], wx1 * tt1[1]);
+          if (FIELD) {
+            const int ph = (h ? e1 : e0) & 0xff;
+            const double* rr = rb + (ph < BM ? ph : 0) * kRec;
+            const double px = rr[10], py = rr[11];
+            const double nx0 = ((double)(X0 + cx0) - 0.5 * P) * dv.h - px, ny0 = ((double)(Y0 + cy0) - 0.5 * P) * dv.h - py;
+            const double ta = 2.0 * dv.alpha;
+            const double wxd0 = ta * nx0 * wx0, wxd1 = ta * (nx0 + dv.h) * wx1;
+            const double wyd0 = ta * ny0 * wy0, wyd2 = ta * (ny0 + 2.0 * dv.h) * wy2;
+            const double* uu0 = u0 + 2 * h;
+            const double* uu1 = u1 + 2 * h;
+            v[h][1] = wy0 * fma(wxd0, tt0[0], wxd1 * tt0[1]) + wy2 * fma(wxd0, tt1[0], wxd1 * tt1[1]);
+            v[h][2] = wyd0 * fma(wx0, tt0[0], wx1 * tt0[1]) + wyd2 * fma(wx0, tt1[0], wx1 * tt1[1]);
+            v[h][3] = wy0 * fma(wx0, uu0[0], wx1 * uu0[1]) + wy2 * fma(wx0, uu1[0], wx1 * uu1[1]);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            v[h][cc] += __shfl_xor_sync(0xffffffffu, v[h][cc], 1);
+            v[h][cc] += __shfl_xor_sync(0xffffffffu, v[h][cc], 2);
+          }
         if (tig == 0) {
           const int pa = e0 & 0xff, pb = e1 & 0xff;
-          if (pa < BM) acc[(b * BM + pa) * (kCW + 1) + w] = v[0];
-          if (pb < BM) acc[(b * BM + pb) * (kCW + 1) + w] = v[1];
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            if (pa < BM) acc[((b * BM + pa) * (kCW + 1) + w) * NC + cc] = v[0][cc];
+            if (pb < BM) acc[((b * BM + pb) * (kCW + 1) + w) * NC + cc] = v[1][cc];
+          }
         }
       }
       __threadfence_block();
@@ -619,10 +669,12 @@ auto reduce = [&](int b, int rt) {
 
 // Sum the per-tile partials of every particle in a fixed order and scatter to user order.
 // Only x tiles in [txlo, txhi) are summed (one slab of the distributed path; all tiles otherwise).
-template <int TZ>
+// FIELD: the slots hold (phi, dphi/dx, dphi/dy, dphi/dz); field = -grad phi (3 per particle).
+template <int TZ, bool FIELD>
 __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int* __restrict__ perm,
-                                const double* __restrict__ gpart, int64_t N, double* __restrict__ phi, int txlo,
-                                int txhi) {
+                                const double* __restrict__ gpart, int64_t N, double* __restrict__ phi,
+                                double* __restrict__ field, int txlo, int txhi) {
+  constexpr int NC = FIELD ? 4 : 1;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= N) return;
   const int4 st = S4[p];
@@ -630,23 +682,33 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   const int nx = fdiv(st.x + P - 1, kTXY) - fdiv(st.x, kTXY) + 1;
   const int ny = fdiv(st.y + P - 1, kTXY) - fdiv(st.y, kTXY) + 1;
   const int nz = zcount(st.w, P, dv.M, TZ);
-  const double* g = gpart + p * dv.nslot;
-  double s = 0.0;
+  const double* g = gpart + p * dv.nslot * NC;
+  double s[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s[c] = 0.0;
   const int tx0 = fdiv(st.x, kTXY);
   for (int a = 0; a < nx; ++a) {
     if (tx0 + a < txlo || tx0 + a >= txhi) continue;
     for (int b = 0; b < ny; ++b)
-      for (int z = 0; z < nz; ++z) s += g[(a * dv.nsxy + b) * dv.nsz + z];
+      for (int z = 0; z < nz; ++z)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) s[c] += g[((a * dv.nsxy + b) * dv.nsz + z) * NC + c];
   }
-  phi[perm[p]] = s;
+  const int64_t u = perm[p];
+  if (phi) phi[u] = s[0];
+  if (FIELD)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) field[3 * u + c] = -s[1 + c];
 }
 
 // Compact records of the sorted particles: {jx0, jy0, lz0, lz0 mod M} (reading R-3), q, the
-// sorted index, and
-// per axis the Fast Gaussian Gridding factors of the first stencil node offset d0:
-//   A = e^{-alpha d0^2},  E = e^{-2 alpha h d0}   (node t: A E^t f1[t]).
+// sorted index, and per axis the Fast Gaussian Gridding factors of the first stencil
+// node offset d0:  A = e^{-alpha d0^2},  E = e^{-2 alpha h d0}   (node t: A E^t f1[t]);
+// FIELD records add the particle position.
+template <bool FIELD>
 __global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4, int64_t N,
                           double* __restrict__ rec) {
+  constexpr int kRec = rec_len(FIELD);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const double4 pp = P4[i];
@@ -661,6 +723,12 @@ __global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* _
     r[4 + 2 * ax] = exp(-dv.alpha * d0[ax] * d0[ax]);
     r[5 + 2 * ax] = exp(-2.0 * dv.alpha * dv.h * d0[ax]);
   }
+  if (FIELD) {
+    r[10] = pp.x;
+    r[11] = pp.y;
+    r[12] = pp.z;
+    r[kRec - 1] = 0.0;
+  }
   double2* out = reinterpret_cast<double2*>(rec + i * kRec);
   out[0] = make_double2(__hiloint2double(s.y, s.x), __hiloint2double(s.w, s.z));
 #pragma unroll
@@ -668,7 +736,7 @@ __global__ void k_records(KDev dv, const double4* __restrict__ P4, const int4* _
 }
 
 int tile_tz(int M) { return M >= 64 ? 32 : 16; }
-int rec_doubles(int P) { return (void)P, kRec; }
+int rec_doubles(int P) { return (void)P, rec_len(true); }
 
 // Slots of the gather partials: x and y tiles per stencil, then z tiles (<= ceil(P/TZ)+2 once
 // the stencil wraps around the periodic axis).
@@ -685,12 +753,17 @@ int64_t gather_slots(const KDev& dv) {
   return d.nslot;
 }
 
-void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st) {
-  k_records<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, w.rec);
+void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field) {
+  if (field)
+    k_records<true><<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N,
+                                                                 w.rec);
+  else
+    k_records<false><<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N,
+                                                                  w.rec);
   SE1P_LAUNCH_CHECK();
 }
 
-template <int TZ, bool GATHER>
+template <int TZ, bool GATHER, bool FIELD>
 static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   TileArgs a;
   a.dv = pl.dv;
@@ -715,9 +788,10 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   a.gpart = GATHER ? w.gpart : nullptr;
   int BM = 0, NB = 0;
   const int limit = 227 * 1024 - 1024;
-  for (int bm : {64, 32}) {
-    for (int nb = kMaxNB; nb >= 2 && !BM; --nb)
-      if (tile_smem(bm, nb, TZ, GATHER).total <= limit) {
+  for (int bm : {64, 32, 16}) {   // the gather's lag-2 reduction needs NB >= 3
+    if (FIELD && bm > 32) continue;
+    for (int nb = kMaxNB; nb >= (GATHER ? 3 : 2) && !BM; --nb)
+      if (tile_smem(bm, nb, TZ, GATHER, FIELD).total <= limit) {
         BM = bm;
         NB = nb;
       }
@@ -726,38 +800,44 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   if (!BM) throw Error{4, "tile kernels do not fit in shared memory"};
   a.BM = BM;
   a.NB = NB;
-  const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER).total;
-  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+  const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER, FIELD).total;
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER, FIELD>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned nblk = (unsigned)(ntx * a.nty * a.ntz);
-  k_tiles<TZ, GATHER><<<nblk, kThreads, smem, st>>>(a);
+  k_tiles<TZ, GATHER, FIELD><<<nblk, n_threads(FIELD), smem, st>>>(a);
   SE1P_LAUNCH_CHECK();
 }
 
-template <bool GATHER>
+template <bool GATHER, bool FIELD>
 static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   if (tx_hi < 0) tx_hi = (int)ceil_div(pl.dv.Mt, kTXY);
-  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, GATHER>(pl, w, N, tx_lo, tx_hi, st);
-  else launch_tiles<16, GATHER>(pl, w, N, tx_lo, tx_hi, st);
+  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, GATHER, FIELD>(pl, w, N, tx_lo, tx_hi, st);
+  else launch_tiles<16, GATHER, FIELD>(pl, w, N, tx_lo, tx_hi, st);
 }
 
 void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
-  dispatch_tiles<false>(pl, w, N, tx_lo, tx_hi, st);
+  dispatch_tiles<false, false>(pl, w, N, tx_lo, tx_hi, st);
 }
 
-void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
-  dispatch_tiles<true>(pl, w, N, tx_lo, tx_hi, st);
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi, bool field) {
+  if (field) dispatch_tiles<true, true>(pl, w, N, tx_lo, tx_hi, st);
+  else dispatch_tiles<true, false>(pl, w, N, tx_lo, tx_hi, st);
 }
 
-void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st, int tx_lo, int tx_hi) {
+void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st, int tx_lo, int tx_hi,
+                           double* field) {
   KDev dv = pl.dv;
   slot_geometry(dv);
   if (tx_hi < 0) tx_hi = (int)ceil_div(dv.Mt, kTXY);
   const unsigned nb = (unsigned)ceil_div(N, 256);
-  if (tile_tz(dv.M) == 32)
-    k_gather_finish<32><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi, tx_lo, tx_hi);
-  else
-    k_gather_finish<16><<<nb, 256, 0, st>>>(dv, (const int4*)w.s4, w.perm, w.gpart, N, phi, tx_lo, tx_hi);
+  const int4* s4 = (const int4*)w.s4;
+  if (tile_tz(dv.M) == 32) {
+    if (field) k_gather_finish<32, true><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+    else k_gather_finish<32, false><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+  } else {
+    if (field) k_gather_finish<16, true><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+    else k_gather_finish<16, false><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+  }
   SE1P_LAUNCH_CHECK();
 }
 

@@ -1,0 +1,134 @@
+"""GPU parity of the electric field E = -grad phi (forces F = q E).
+
+Tolerances:
+  * k-space field element-wise vs the step-by-step Alg. 1 oracle's gradient gather
+    (`sd.se1p_kspace(..., return_field=True)`): |d| <= 1e-11 max|E| -- same discrete sums in fp64.
+  * real-space field vs the oracle's direct sum: |d| <= 1e-12 max|E|.
+  * full field vs the exact Ewald1P field (oracle.field_exact): relative rms <= 1e-9 at the
+    configurations' parameters, the potential's bar (measured 2.2e-10 at C1, ~1e-12 at C2-C4;
+    DESIGN.md).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import se1p_discrete as sd
+from se1p_synth import CONFIGS, kspace_kwargs, make_system
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1611_09538_b200 as se1p  # noqa: E402
+
+from test_gpu_fullsize import _targets  # noqa: E402
+from test_gpu_parity import CASES  # noqa: E402
+
+
+def _dev(x, q):
+    return (torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_kspace_field_matches_alg1_oracle(case):
+    name, N, L, xi, M, P, n_l, S0, SI, SJ, seed = case
+    x, q = make_system(N, L, seed)
+    ref_phi, ref_E = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, return_field=True)
+    xd, qd = _dev(x, q)
+    phi, E = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=S0, SI=SI, Ntilde=SJ, field=True)
+    phi, E = phi.cpu().numpy(), E.cpu().numpy()
+    assert E.shape == (N, 3)
+    errE = np.max(np.abs(E - ref_E))
+    assert errE <= 1e-11 * np.max(np.abs(ref_E)), (name, errE, np.max(np.abs(ref_E)))
+    assert np.max(np.abs(phi - ref_phi)) <= 1e-11 * np.max(np.abs(ref_phi))
+    # the potential of the field call is the plain call's up to summation order
+    plain = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=S0, SI=SI, Ntilde=SJ).cpu().numpy()
+    assert np.max(np.abs(phi - plain)) <= 1e-13 * np.max(np.abs(plain))
+
+
+def test_real_field_vs_oracle():
+    for L, xi, rc, N, seed in [((1, 1, 1), 4.0, 1.158, 100, 1), ((1, 1, 2), 12.0, 0.401, 800, 3),
+                               ((2, 2, 2), 30.0, 0.1, 3000, 5), ((1, 1, 1), 3.0, 2.7, 40, 4)]:
+        x, q = make_system(N, L, seed)
+        xd, qd = _dev(x, q)
+        phi, E = se1p.real(xd, qd, L, xi, rc, field=True)
+        ref = oracle.field_real(x, q, L, xi, rc)
+        E = E.cpu().numpy()
+        assert np.max(np.abs(E - ref)) <= 1e-12 * np.max(np.abs(ref)), (L, xi, rc)
+        plain = se1p.real(xd, qd, L, xi, rc).cpu().numpy()
+        assert np.array_equal(phi.cpu().numpy(), plain)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_field_vs_exact_oracle(cfg):
+    c = CONFIGS[cfg]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    U, phi, F = se1p.energy_forces(xd, qd, c.L, c.xi, c.rc, c.M, c.P, **kspace_kwargs(c))
+    E = (F / qd[:, None]).cpu().numpy()
+    ref = oracle.field_exact(x, q, c.L)
+    err = oracle.rel_rms(E, ref)
+    print(f"{cfg} field rel rms {err:.3e}")
+    assert err <= 1e-9
+    ref_phi = oracle.phi_exact(x, q, c.L)
+    assert abs(U - 0.5 * float(np.dot(q, ref_phi))) <= 1e-9 * 0.5 * float(np.dot(np.abs(q), np.abs(ref_phi)))
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_field_at_full_size_sampled(cfg):
+    """Full-size configurations: the exact field at the seeded oracle targets (plus targets near a
+    free face)."""
+    c = CONFIGS[cfg]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    _, Ek = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, field=True, **kspace_kwargs(c))
+    _, Er = se1p.real(xd, qd, c.L, c.xi, c.rc, field=True)
+    E = (Ek + Er).cpu().numpy()
+    t = _targets(c, x)
+    ref = oracle.field_exact(x, q, c.L, t)
+    err = oracle.rel_rms(E[t], ref)
+    print(f"{cfg} field rel rms {err:.3e} on {t.size} targets")
+    assert err <= 1e-9
+
+
+def test_field_host_io_determinism_and_linearity():
+    c = CONFIGS["C2"]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    kw = kspace_kwargs(c)
+    _, a = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, field=True, **kw)
+    _, b = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, field=True, **kw)
+    _, h = se1p.kspace(x, q, c.L, c.xi, c.M, c.P, field=True, **kw)      # numpy -> host I/O
+    assert torch.equal(a, b)
+    assert np.array_equal(a.cpu().numpy(), h)
+    _, n = se1p.kspace(xd, -3.0 * qd, c.L, c.xi, c.M, c.P, field=True, **kw)
+    assert torch.max(torch.abs(n + 3.0 * a)) <= 1e-12 * torch.max(torch.abs(a))
+    _, hr = se1p.real(x, q, c.L, c.xi, c.rc, field=True)
+    _, dr = se1p.real(xd, qd, c.L, c.xi, c.rc, field=True)
+    assert np.array_equal(hr, dr.cpu().numpy())
+
+
+def test_field_newton_third_law():
+    """Sum of forces over a neutral system vanishes for the exact field (pairwise antisymmetric
+    interactions, images included); the SE field reproduces it to its accuracy."""
+    c = CONFIGS["C2"]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    _, _, F = se1p.energy_forces(xd, qd, c.L, c.xi, c.rc, c.M, c.P, **kspace_kwargs(c))
+    F = F.cpu().numpy()
+    assert np.max(np.abs(F.sum(axis=0))) <= 1e-7 * np.sqrt(c.N) * np.max(np.abs(F))
+
+
+def test_field_errors():
+    L = (1.0, 1.0, 1.0)
+    x, q = make_system(50, L, 12)
+    xd, qd = _dev(x, q)
+    lib = se1p.load()
+    o = se1p._opts()
+    rc = lib.se1p_kspace_field_ex(se1p.ctypes.byref(o), None, xd.data_ptr(), qd.data_ptr(), 50, se1p._Larr(L),
+                                  4.0, 16, 8, 0.0, -1.0, -1.0, -1, None, None)
+    assert rc == 1
+    with pytest.raises(se1p.SE1PError):
+        se1p.kspace(xd, qd, L, 4.0, 16, 8, field=True, reference_kernels=True)

@@ -1,7 +1,7 @@
 set -x
-B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
-timeout 600 python bench.py --steps 20 --warmup 3 --cpu-seconds 10 > gpurun_out/r1q_bench.log 2>&1
-$B > gpurun_out/r1q_plain.log 2>&1 &&
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r1q_launches.csv $B > gpurun_out/r1q_ncu1.log 2>&1
-python tools/profile_one.py C5 1 > gpurun_out/r1q_p1.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:k_tiles -c 2 -o gpurun_out/r1q_tiles python tools/profile_one.py C5 1 > gpurun_out/r1q_ncu2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_field.py -x -q -s > gpurun_out/r1q_field.log 2>&1
+tail -30 gpurun_out/r1q_field.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r1q_pytest.log 2>&1
+tail -3 gpurun_out/r1q_pytest.log
+for c in C5; do timeout 300 python tools/stage_times.py $c; done > gpurun_out/r1q_stages.log 2>&1
+cat gpurun_out/r1q_stages.log
