@@ -177,6 +177,32 @@ int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, con
 int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P,
                     double eta, double s0, double sf, int n_local, se1p_plan_info* info);
 
+/* Parameters from an absolute rms error tolerance: the paper's recipe
+   "Parameter selection" -- rc and kinf by inverting the Kolafa-Perram estimates
+   (Eqs. (rc), (kinf), Lambert W), M = 2 kinf (even, FFT-friendly, L1/h and L2/h
+   integers), P the smallest even integer with A e^{-c^2 pi P/2} <= tol (Eq.
+   (approximation_error_oneterm), c = 0.95), eta, s_l from e^{-2 pi s_l} < tol
+   (P:697), n_l = ceil(M/10), s0 = 1 + sqrt(2).  Host-only (no device
+   work).  Non-cubic boxes: DESIGN.md reading R-18.  Q = sum q_n^2; xi is the caller's choice
+   (the paper balances real- and k-space run time).  Each estimate is inverted at a share
+   of tol (real space tol/2, k-space truncation and aliasing tol/10, window tol/100) and M is
+   raised until eta <= 0.8 (reading R-18), so the measured rms error meets tol.
+   Errors: SE1P_EINVAL (null, Q/xi/L <= 0, tol not in (0,1)), SE1P_EPARAM (no admissible M <=
+   8192, non-square cross-section). */
+typedef struct se1p_tol_plan {
+  double xi, tol, Q;
+  double rc;                 /* real-space cutoff, Eq. (rc)                                  */
+  double kinf;               /* Eq. (kinf) (unrounded)                                       */
+  int M, P, Mfree, Mt;       /* periodic points, support, L1/h, M~ = Mfree + P               */
+  double h, eta;
+  int n_local;               /* n_l                                                          */
+  double s_l, s0;            /* upsampling factors                                           */
+  int SI, S0, Ntilde;        /* extents for se1p_opts (SI = ceil(s_l M~), S0 = ceil(s0 M~))  */
+  double est_real, est_fourier, est_approx;   /* the three estimates at the chosen values   */
+} se1p_tol_plan;
+
+int se1p_plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out);
+
 /* Per-stage device time of the last _ex call on this thread, in milliseconds, measured
    with CUDA events on the call's stream when opts->reserved[0] == 1 (profiling mode).
    Stages: 0 bin/sort, 1 particle records (window weights), 2 gridding tiles, 3 z-FFT,

@@ -25,7 +25,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EDOMAIN", 3: "ENONNEUTRAL", 4: "EPARAM", 5: 
 EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query",
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
-           "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex"]
+           "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol"]
 
 
 class SE1PError(RuntimeError):
@@ -49,6 +49,16 @@ class PlanInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class TolPlan(ctypes.Structure):
+    _d, _i = ctypes.c_double, ctypes.c_int
+    _fields_ = [("xi", _d), ("tol", _d), ("Q", _d), ("rc", _d), ("kinf", _d), ("M", _i), ("P", _i), ("Mfree", _i),
+                ("Mt", _i), ("h", _d), ("eta", _d), ("n_local", _i), ("s_l", _d), ("s0", _d), ("SI", _i), ("S0", _i),
+                ("Ntilde", _i), ("est_real", _d), ("est_fourier", _d), ("est_approx", _d)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -64,12 +74,13 @@ def load(build_if_needed: bool = True):
     lib = ctypes.CDLL(LIB_PATH)
     d, i64, i32, vp = ctypes.c_double, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
     lib.se1p_kspace.argtypes = [vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
-    lib.se1p_kspace_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
+    lib.se1p_kspace_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_real.argtypes = [vp, vp, i64, vp, d, d, vp]
-    lib.se1p_real_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, d, vp]
-    lib.se1p_kspace_field_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
-    lib.se1p_real_field_ex.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, d, vp, vp]
-    lib.se1p_plan_query.argtypes = [ctypes.POINTER(Opts), vp, d, i32, i32, d, d, d, i32, ctypes.POINTER(PlanInfo)]
+    lib.se1p_real_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp]
+    lib.se1p_plan_from_tol.argtypes = [vp, d, d, d, vp]
+    lib.se1p_kspace_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
+    lib.se1p_real_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp, vp]
+    lib.se1p_plan_query.argtypes = [vp, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_last_stage_times.argtypes = [vp, i32]
     lib.se1p_last_launch_count.restype = i32
     lib.se1p_last_error.restype = ctypes.c_char_p
@@ -77,10 +88,10 @@ def load(build_if_needed: bool = True):
     lib.se1p_debug_copy.argtypes = [i32, vp, i64]
     lib.se1p_debug_copy.restype = i32
     ip = ctypes.POINTER(ctypes.c_int)
-    lib.se1p_kspace_slab_forward.argtypes = [ctypes.POINTER(Opts), vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32,
+    lib.se1p_kspace_slab_forward.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32,
                                              i32, i32, ip, vp]
-    lib.se1p_kspace_modes.argtypes = [ctypes.POINTER(Opts), vp, vp, d, i32, i32, d, d, d, i32, i32, ip, i32, ip, vp]
-    lib.se1p_kspace_slab_backward.argtypes = [ctypes.POINTER(Opts), vp, i64, vp, d, i32, i32, d, d, d, i32, i32, i32,
+    lib.se1p_kspace_modes.argtypes = [vp, vp, vp, d, i32, i32, d, d, d, i32, i32, ip, i32, ip, vp]
+    lib.se1p_kspace_slab_backward.argtypes = [vp, vp, i64, vp, d, i32, i32, d, d, d, i32, i32, i32,
                                               ip, vp, vp]
     for f in ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query", "se1p_last_stage_times",
               "se1p_kspace_slab_forward", "se1p_kspace_modes", "se1p_kspace_slab_backward"]:
@@ -165,7 +176,7 @@ def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=N
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
     o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels)
-    args = (ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
+    args = (ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
             _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr)
     if field:
         _check(lib.se1p_kspace_field_ex(*args, fptr))
@@ -181,7 +192,7 @@ def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False, f
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
     o = _opts(host_io=host, skip_checks=skip_checks, sync=sync)
-    args = (ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr)
+    args = (ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr)
     if field:
         _check(lib.se1p_real_field_ex(*args, fptr))
         return out, fo
@@ -224,7 +235,7 @@ def slab_forward(x, q, L, xi, M, P, x_lo, x_hi, plane_order, out=None, stream=No
     if out is None:
         out = torch.empty((n_planes, x_hi - x_lo, info["Mt"], 2), dtype=torch.float64, device=x.device)
     o = _opts(Ntilde, S0, SI, False, skip_checks, sync)
-    _check(lib.se1p_kspace_slab_forward(ctypes.byref(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
+    _check(lib.se1p_kspace_slab_forward(ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
                                         int(M), int(P), _neg(eta, 0.0), _neg(s0), _neg(sf),
                                         -1 if n_local is None else int(n_local), int(x_lo), int(x_hi),
                                         _ints(plane_order), out.data_ptr()))
@@ -236,7 +247,7 @@ def modes(planes, L, xi, M, P, plane_ids, slab_lo, stream=None, sync=False, eta=
     """Distributed path, rank stage 2: the mode stage on the owner's split buffer (in place)."""
     lib = load()
     o = _opts(Ntilde, S0, SI, False, False, sync)
-    _check(lib.se1p_kspace_modes(ctypes.byref(o), _stream_ptr(stream, planes), _Larr(L), float(xi), int(M), int(P),
+    _check(lib.se1p_kspace_modes(ctypes.addressof(o), _stream_ptr(stream, planes), _Larr(L), float(xi), int(M), int(P),
                                  _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local),
                                  len(plane_ids), _ints(plane_ids), len(slab_lo) - 1, _ints(slab_lo),
                                  planes.data_ptr()))
@@ -252,7 +263,7 @@ def slab_backward(planes, N, L, xi, M, P, x_lo, x_hi, plane_order, out=None, str
     if out is None:
         out = torch.empty(int(N), dtype=torch.float64, device=planes.device)
     o = _opts(Ntilde, S0, SI, False, False, sync)
-    _check(lib.se1p_kspace_slab_backward(ctypes.byref(o), _stream_ptr(stream, planes), int(N), _Larr(L), float(xi),
+    _check(lib.se1p_kspace_slab_backward(ctypes.addressof(o), _stream_ptr(stream, planes), int(N), _Larr(L), float(xi),
                                          int(M), int(P), _neg(eta, 0.0), _neg(s0), _neg(sf),
                                          -1 if n_local is None else int(n_local), int(x_lo), int(x_hi),
                                          _ints(plane_order), planes.data_ptr(), out.data_ptr()))
@@ -263,9 +274,25 @@ def plan_info(L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None
     lib = load()
     info = PlanInfo()
     o = _opts(Ntilde, S0, SI)
-    _check(lib.se1p_plan_query(ctypes.byref(o), _Larr(L), float(xi), int(M), int(P), _neg(eta, 0.0), _neg(s0),
-                               _neg(sf), -1 if n_local is None else int(n_local), ctypes.byref(info)))
+    _check(lib.se1p_plan_query(ctypes.addressof(o), _Larr(L), float(xi), int(M), int(P), _neg(eta, 0.0), _neg(s0),
+                               _neg(sf), -1 if n_local is None else int(n_local), ctypes.addressof(info)))
     return info.as_dict()
+
+
+def plan_from_tol(L, Q, xi, tol):
+    """Parameters for an absolute rms error tolerance by the paper's recipe (host
+    only).  Returns a dict: rc, kinf, M, P, eta, n_local, s_l, s0, extents SI, S0, Ntilde and the
+    three error estimates.  `kspace_args(plan)` turns it into kspace() keyword arguments."""
+    lib = load()
+    out = TolPlan()
+    _check(lib.se1p_plan_from_tol(_Larr(L), float(Q), float(xi), float(tol), ctypes.addressof(out)))
+    return out.as_dict()
+
+
+def kspace_args(plan):
+    """(M, P, kwargs) of kspace() for a plan_from_tol() result."""
+    return plan["M"], plan["P"], dict(eta=plan["eta"], n_local=plan["n_local"], S0=plan["S0"], SI=plan["SI"],
+                                      Ntilde=plan["Ntilde"])
 
 
 def stage_times():

@@ -592,6 +592,10 @@ int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, 
   });
 }
 
+int se1p_plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out) {
+  return guarded([&] { plan_from_tol(L, Q, xi, tol, out); });
+}
+
 int se1p_last_stage_times(double* ms, int max_stages) {
   int n = std::min(max_stages, g_nstages);
   for (int i = 0; i < n; ++i) ms[i] = g_stage_ms[i];

@@ -2,6 +2,7 @@
 #pragma once
 #include <vector>
 
+#include "../../include/se1p.h"
 #include "fft.cuh"
 
 namespace se1p {
@@ -112,6 +113,8 @@ struct KWork {                  // per-N workspace (grown on demand)
 
 KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached
 void kplan_release_all();
+void plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out);   // planner.cu
+double lambert_w0(double x);
 
 // Stages (launch on st).
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
