@@ -30,7 +30,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *sources(), "-lcudart"]
+    extra = os.environ.get("SE1P_NVCC_EXTRA", "").split()   # experiment defines (tools/)
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT + ".tmp", *sources(), "-lcudart"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -9,7 +9,8 @@
 //   P     smallest even integer with A e^{-c^2 pi P/2} <= E, A = sqrt(Q xi L3)/L3 (Eq.
 //         (approximation_error_oneterm); "set to even integers" P:690)
 //   eta   Eq. (comp_eta), c = 0.95
-//   s_l   e^{-2 pi s_l} < E (Eq. (choose_sl)), extent ceil(s_l M~)
+//   s_l   e^{-2 pi s_l} < E (Eq. (choose_sl)) and the image-distance form of the same
+//         estimate for non-cubic boxes (reading R-18), extent ceil(s_l M~)
 //   n_l   M ~ 10 n_l (Eq. (choose_nl)): ceil(M/10)
 //   s0    the minimal 1 + sqrt(2) of P:522 ("s0 ~ 2.4"), extent ceil(s0 M~)
 //   Ntilde  >= M~, widened by the aliasing rule of reading R-8 (FFT-friendly).
@@ -86,15 +87,18 @@ void plan_from_tol(const double L[3], double Q, double xi, double E, se1p_tol_pl
   o->Mt = o->Mfree + P;
   o->eta = P * xi * xi * o->h * o->h / (c * c * kPi);
   o->n_local = std::min(M / 2, std::max(1, (int)std::ceil(M / 10.0 - 1e-12)));
-  o->s_l = std::max(1.0, std::log(1.0 / EF) / (2.0 * kPi));
+  // Upsampled and J planes: after the padded transform of length S h, mode k3 sees the periodic
+  // images of the free-space solution at distance S h - L_free, which contribute ~ sqrt(Q)
+  // e^{-|k3| (S h - L_free)} (the paper's e^{-2 pi |k3|/h_k} of Eq. (proof_I2d), with
+  // h_k = 2 pi/(S h) and the charges' extent taken off; reading R-8 / R-18).  The slowest mode
+  // of each set binds: k3 = 2 pi/L3 for the I planes, 2 pi (n_l+1)/L3 for the J planes.
+  const double budget = std::max(0.0, std::log(std::sqrt(Q) / EF));
+  const double dI = budget * L3 / (2.0 * kPi), dJ = dI / (o->n_local + 1);
+  o->s_l = std::max({1.0, std::log(1.0 / EF) / (2.0 * kPi), (L[0] + dI) / (o->Mt * o->h)});   // (choose_sl) P:697
   o->SI = (int)std::ceil(o->s_l * o->Mt - 1e-9);
   o->s0 = 1.0 + std::sqrt(2.0);
   o->S0 = (int)std::ceil(o->s0 * o->Mt - 1e-9);
-  // J planes (|k3| > n_l, no upsampling): the free-axis FFT extent Ntilde >= M~ is widened until
-  // the periodic images of the free-space solution at distance Ntilde h - L_free are below the
-  // budget for the slowest J mode k3 = 2 pi (n_l+1)/L3 (reading R-8, SURVEY c-6)
-  const double gap = std::max(0.0, std::log(1.0 / (EF * L3))) * L3 / (2.0 * kPi * (o->n_local + 1));
-  o->Ntilde = next_friendly(std::max(o->Mt, (int)std::ceil((L[0] + gap) / o->h - 1e-9)));
+  o->Ntilde = next_friendly(std::max(o->Mt, (int)std::ceil((L[0] + dJ) / o->h - 1e-9)));
   o->est_real = std::sqrt(Q * o->rc / (2.0 * V)) / (xi * o->rc * xi * o->rc) * std::exp(-xi * xi * o->rc * o->rc);
   const double ki = M / 2.0;   // the grid resolves |k3| <= 2 pi (M/2)/L3
   o->est_fourier = xi / (kPi * kPi) * std::pow(ki, -1.5) * std::sqrt(Q) * std::exp(-std::pow(kPi * ki / (xi * L3), 2));

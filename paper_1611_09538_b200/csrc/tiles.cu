@@ -35,8 +35,16 @@
 namespace se1p {
 
 constexpr int kCW = 16;                          // consumer warps
-// expander warps: 8, or 4 for the field gather (32-particle batches, more consumer registers)
-__host__ __device__ constexpr int n_exp_warps(bool field) { return field ? 4 : 8; }
+// expander warps: 8, or 4 for the field gather (32-particle batches, more consumer registers).
+// ptxas budgets registers for the thread count rounded up to 4 warps: 25 warps -> 72 registers,
+// 24 -> 80, 20 -> 96.  Measured (C5): 7/3 and 6/2 expander warps are 8-20% slower, field 5-8 equal.
+#ifndef SE1P_EXP_WARPS
+#define SE1P_EXP_WARPS 8
+#endif
+#ifndef SE1P_EXP_WARPS_FIELD
+#define SE1P_EXP_WARPS_FIELD 4
+#endif
+__host__ __device__ constexpr int n_exp_warps(bool field) { return field ? SE1P_EXP_WARPS_FIELD : SE1P_EXP_WARPS; }
 __host__ __device__ constexpr int n_threads(bool field) { return (kCW + 1 + n_exp_warps(field)) * 32; }
 constexpr int kMaxNB = 4;
 // doubles per compact record: {s4, q, index, (A, E) per axis} (80 B); the field gather adds the

@@ -56,6 +56,10 @@ def test_plan_inverts_the_estimates(L, Q, xi, tol):
     assert p["n_local"] == max(1, math.ceil(M / 10))
     assert p["SI"] >= p["s_l"] * p["Mt"] - 1e-9 and p["S0"] >= (1 + math.sqrt(2)) * p["Mt"] - 1e-9
     assert p["Ntilde"] >= p["Mt"] and p["Mt"] == p["Mfree"] + p["P"]
+    # image distance of the padded transforms (reading R-18): sqrt(Q) e^{-k3 (S h - L_free)} <= tol/10
+    # at the slowest mode of each set (k3 = 2 pi/L3 for I, 2 pi (n_l+1)/L3 for J)
+    for S, k3 in [(p["SI"], 2 * math.pi / L3), (p["Ntilde"], 2 * math.pi * (p["n_local"] + 1) / L3)]:
+        assert math.sqrt(Q) * math.exp(-k3 * (S * h - L[0])) <= 0.1 * tol * (1 + 1e-9)
 
 
 def test_lambert_region_and_errors():
@@ -75,7 +79,8 @@ def test_lambert_region_and_errors():
 ACHIEVE = [((10.0, 10.0, 10.0), 120, True, 1.5, 1e-6), ((10.0, 10.0, 10.0), 120, True, 3.0, 1e-6),
            ((10.0, 10.0, 10.0), 120, True, 1.5, 1e-12), ((10.0, 10.0, 10.0), 120, True, 3.0, 1e-12),
            ((1.0, 1.0, 1.0), 300, False, 6.0, 1e-8), ((1.0, 1.0, 2.0), 300, False, 5.0, 1e-10),
-           ((1.0, 1.0, 1.0), 300, False, 8.0, 1e-4), ((1.0, 1.0, 1.0), 300, False, 12.0, 1e-10)]
+           ((1.0, 1.0, 1.0), 300, False, 8.0, 1e-4), ((1.0, 1.0, 1.0), 300, False, 12.0, 1e-10),
+           ((1.0, 1.0, 2.0), 500, False, 6.0, 1e-6)]
 
 
 @pytest.mark.parametrize("L,N,norm,xi,tol", ACHIEVE)
