@@ -29,15 +29,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ewald1p.c")
+_SRCS = [_SRC, os.path.join(_HERE, "ewald3p.c")]
 _LIB = os.path.join(_HERE, "liborc.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile the C oracle with gcc (OpenMP, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-fno-fast-math",
-               "-o", _LIB, _SRC, "-lm"]
+               "-o", _LIB, *_SRCS, "-lm"]
         subprocess.check_call(cmd)
     return _LIB
 
@@ -71,6 +72,13 @@ def _load():
         lib.orc_field_k30.argtypes = [P, P, i64, P, d, P, i64, P]
         lib.orc_field_exact.argtypes = [P, P, i64, P, d, P, i64, P, P]
         lib.orc_field_brute.argtypes = [P, P, i64, P, i64, P, i64, P]
+        lib.orc3_phi_real.argtypes = [P, P, i64, P, d, d, P, i64, P]
+        lib.orc3_phi_kspace.argtypes = [P, P, i64, P, d, i32, P, i64, P]
+        lib.orc3_phi_exact.argtypes = [P, P, i64, P, d, P, i64, P]
+        lib.orc3_rc_converged.restype = d
+        lib.orc3_rc_converged.argtypes = [d]
+        lib.orc3_kmax_converged.restype = i32
+        lib.orc3_kmax_converged.argtypes = [d, P]
         lib.orc_modes_needed.restype = i32
         lib.orc_modes_needed.argtypes = [d, d]
         lib.orc_rc_converged.restype = d
@@ -252,3 +260,33 @@ def rel_rms(a, ref):
     a = np.asarray(a)
     ref = np.asarray(ref)
     return float(np.sqrt(np.sum((a - ref) ** 2) / np.sum(ref ** 2)))
+
+
+# ---------------------------------------------------------------- triply periodic (NEXT-4)
+# ewald3p.c: the classic 3P Ewald sum (tin-foil), the SE3P baseline's exact answer.
+
+def phi3_real(x, q, L, xi, rc=None, targets=None):
+    lib = _load()
+    x, q, L, N, targets, out = _prep(x, q, L, targets)
+    if rc is None:
+        rc = lib.orc3_rc_converged(float(xi))
+    lib.orc3_phi_real(_p(x), _p(q), N, _p(L), float(xi), float(rc), _p(targets), targets.size, _p(out))
+    return out
+
+
+def phi3_kspace(x, q, L, xi, K=None, targets=None):
+    """(4 pi/V) sum_{k != 0, |j_d| <= K} e^{-k^2/4xi^2}/k^2 sum_n q_n cos(k.(x_m - x_n)); K=None: converged."""
+    lib = _load()
+    x, q, L, N, targets, out = _prep(x, q, L, targets)
+    if K is None:
+        K = lib.orc3_kmax_converged(float(xi), _p(L))
+    lib.orc3_phi_kspace(_p(x), _p(q), N, _p(L), float(xi), int(K), _p(targets), targets.size, _p(out))
+    return out
+
+
+def phi3_exact(x, q, L, targets=None, xi_o=0.0):
+    """Triply periodic potential (tin-foil boundary), converged Ewald sum at the oracle's xi_o."""
+    lib = _load()
+    x, q, L, N, targets, out = _prep(x, q, L, targets)
+    lib.orc3_phi_exact(_p(x), _p(q), N, _p(L), float(xi_o), _p(targets), targets.size, _p(out))
+    return out
