@@ -177,6 +177,18 @@ int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, con
 int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P,
                     double eta, double s0, double sf, int n_local, se1p_plan_info* info);
 
+/* SE3P baseline (the paper's Ex. 5, compares SE1P with the
+   triply periodic SE3P): the k-space part of the triply periodic Ewald sum with tin-foil boundary,
+     phi^F(x_m) = (4 pi/V) sum_{k != 0} e^{-k^2/4 xi^2}/k^2 sum_n q_n cos(k.(x_m - x_n)),
+   by Spectral Ewald: the same gridding and gather as se1p_kspace (Gaussians of Eq. (spread_1p)
+   truncated to P^3 nodes, h = L[2]/M, eta as in se1p_kspace), a plain 3D FFT of the
+   M_free x M_free x M periodic grid (no upsampling) and the scaling e^{-(1-eta)k^2/4xi^2}/k^2
+   (k = 0 dropped).  P must be even; x, y in [0,L1) x [0,L2) (any z).  Same pointers, ownership,
+   opts and errors as se1p_kspace_ex. */
+int se1p_kspace3p_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                     int64_t N, const double L[3], double xi, int M, int P, double eta,
+                     double* phi_out);
+
 /* Parameters from an absolute rms error tolerance: the paper's recipe
    "Parameter selection" -- rc and kinf by inverting the Kolafa-Perram estimates
    (Eqs. (rc), (kinf), Lambert W), M = 2 kinf (even, FFT-friendly, L1/h and L2/h

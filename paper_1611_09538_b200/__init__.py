@@ -25,7 +25,8 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EDOMAIN", 3: "ENONNEUTRAL", 4: "EPARAM", 5: 
 EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_plan_query",
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
-           "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol"]
+           "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol",
+           "se1p_kspace3p_ex"]
 
 
 class SE1PError(RuntimeError):
@@ -77,6 +78,7 @@ def load(build_if_needed: bool = True):
     lib.se1p_kspace_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_real.argtypes = [vp, vp, i64, vp, d, d, vp]
     lib.se1p_real_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp]
+    lib.se1p_kspace3p_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, vp]
     lib.se1p_plan_from_tol.argtypes = [vp, d, d, d, vp]
     lib.se1p_kspace_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
     lib.se1p_real_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp, vp]
@@ -182,6 +184,18 @@ def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=N
         _check(lib.se1p_kspace_field_ex(*args, fptr))
         return out, fo
     _check(lib.se1p_kspace_ex(*args))
+    return out
+
+
+def kspace3p(x, q, L, xi, M, P, eta=None, out=None, stream=None, sync=True, skip_checks=False, profile=False):
+    """SE3P baseline (NEXT-4): k-space part of the triply periodic Ewald sum (tin-foil), same
+    gridding/gather as kspace() with a plain 3D FFT; P even (see se1p.h)."""
+    lib = load()
+    xp, qp, N, host, keep = _args(x, q)
+    out, _, optr, _ = _outputs(x, N, False, out, None)
+    o = _opts(host_io=host, skip_checks=skip_checks, sync=sync, profile=profile)
+    _check(lib.se1p_kspace3p_ex(ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M),
+                                int(P), _neg(eta, 0.0), optr))
     return out
 
 

@@ -303,6 +303,85 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   SE1P_CUDA_TRY(cudaGetLastError());
 }
 
+// SE3P baseline (the paper's Ex. 5): the 1P tile plan grids and
+// gathers on the extended grid; a periodic transform plan (every plane a J plane of extent
+// M_free, k = 0 dropped) does the 3D transform and the 3P scaling on the folded grid.
+static void kspace3p_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
+                          const double L[3], double xi, int M, int P, double eta, double* phi_out) {
+  if (!x || !q || !phi_out) throw Error{1, "null pointer"};
+  if (N < 1) throw Error{1, "N must be >= 1"};
+  if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
+  if (P % 2) throw Error{4, "SE3P needs an even P (the folded stencil nodes are then lattice nodes)"};
+  se1p_opts none{};
+  KParams pa = resolve(&none, L, xi, M, P, eta, -1.0, -1.0, 0);
+  const int Mf = (int)std::lround(L[0] / (L[2] / M));
+  pa.n_l = -1;   // tile plan only: no kernel planes, no upsampling
+  pa.S0 = pa.SI = Mf + P;
+  std::vector<int> r;
+  if (!fft_factor(Mf, r)) throw Error{4, "L1/h has a prime factor > 61"};
+  KParams pb = pa;
+  pb.periodic = 1;
+  pb.SJ = Mf;
+  KPlan* pl = kplan_get(pa, st);
+  KPlan* p3 = kplan_get(pb, st);
+  DevState& ds = dev_state();
+  KWork& w = ds.w;
+  const KDev& dv = pl->dv;
+  ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
+  grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
+  grow(w.grid3, w.grid3_cap, (int64_t)Mf * Mf * dv.M);
+  grow(w.planes, w.planes_cap, (int64_t)p3->n_planes * Mf * Mf);
+  grow(w.T, w.T_cap, p3->t_off_total);
+  grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
+  grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
+  const bool host_io = o && o->host_io;
+  const double *dx = x, *dq = q;
+  double* dphi = phi_out;
+  if (host_io) {
+    grow(ds.dx, ds.io_cap, 5 * N);
+    dx = ds.dx;
+    dq = ds.dx + 3 * N;
+    dphi = ds.dx + 4 * N;
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  }
+  if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, true, st);
+  StageTimer tm(o && o->reserved[0] == 1, st);
+  SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
+  // stages: bin, records, spread, fold + z-FFT, modes, inverse z-FFT + unfold, gather, finish
+  tm.mark();
+  k_bin_particles(*pl, w, dx, dq, N, st);
+  tm.mark();
+  k_records_stage(*pl, w, N, st);
+  tm.mark();
+  k_spread_tiles(*pl, w, N, st);
+  tm.mark();
+  k_fold_3p(*pl, w.grid, w.grid3, st);
+  KWork w3 = w;          // the transform stages read and write the periodic grid
+  w3.grid = w.grid3;
+  const SlabLayout L3 = single_layout(Mf, p3->n_planes);
+  k_zfft_forward(*p3, w3, w.planes, L3, nullptr, st);
+  tm.mark();
+  k_mode_stage(*p3, w3, w.planes, L3, nullptr, nullptr, 0, nullptr, nullptr, 0, st);
+  tm.mark();
+  k_zfft_inverse(*p3, w3, w.planes, L3, nullptr, st);
+  k_unfold_3p(*pl, w.grid3, w.grid, st);
+  tm.mark();
+  k_gather_tiles(*pl, w, N, st);
+  tm.mark();
+  k_gather_finish_stage(*pl, w, N, dphi, st);
+  tm.mark();
+  if (host_io) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  tm.finish();
+  if (!o || o->sync || host_io) {
+    SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+    int kerr = 0;
+    SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+  }
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
 static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
                       const double L[3], double xi, double rc, double* phi_out, double* field_out = nullptr) {
   if (!x || !q || (!phi_out && !field_out) || !L) throw Error{1, "null pointer"};
@@ -527,6 +606,15 @@ int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const dou
     se1p_opts o{};
     if (opts) o = *opts;
     real_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, rc, phi_out);
+  });
+}
+
+int se1p_kspace3p_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                     const double L[3], double xi, int M, int P, double eta, double* phi_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    kspace3p_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, phi_out);
   });
 }
 

@@ -49,7 +49,7 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   dv.h = p.L[2] / p.M;
   dv.inv_h = 1.0 / dv.h;
   dv.Mfree = (int)std::lround(p.L[0] / dv.h);
-  dv.Mt = dv.Mfree + p.P;
+  dv.Mt = p.periodic ? dv.Mfree : dv.Mfree + p.P;   // SE3P transform plan: no free-axis extension
   dv.alpha = 2.0 * p.xi * p.xi / p.eta;
   dv.L3 = p.L[2];
   dv.nbx = (int)ceil_div(dv.Mfree, kBin);
@@ -60,8 +60,8 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   dv.ntz = (int)ceil_div(p.M, kTZ);
   const int Mt = dv.Mt;
   pl->n_planes = p.M / 2 + 1;
-  pl->n_kernel = std::min(p.n_l + 1, pl->n_planes);
-  pl->LK = next_friendly(2 * Mt - 1);
+  pl->n_kernel = std::max(0, std::min(p.n_l + 1, pl->n_planes));
+  pl->LK = p.periodic ? p.SJ : next_friendly(2 * Mt - 1);
 
   std::vector<double2> tw;
   if (!fft_make(p.M, pl->fz, tw) || !fft_make(p.SJ, pl->fJ, tw) || !fft_make(pl->LK, pl->fK, tw))

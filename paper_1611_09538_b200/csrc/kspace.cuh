@@ -45,9 +45,10 @@ struct KParams {       // everything a k-space plan is keyed on
   double eta;          // resolved (> 0)
   int n_l;             // resolved (>= 0)
   int S0, SI, SJ;      // resolved padded extents
+  int periodic = 0;    // 1: SE3P transform plan (grid Mfree x Mfree x M, every plane a J plane, SJ = Mfree)
   bool operator==(const KParams& o) const {
     return L[0] == o.L[0] && L[1] == o.L[1] && L[2] == o.L[2] && xi == o.xi && M == o.M && P == o.P &&
-           eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ;
+           eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ && periodic == o.periodic;
   }
 };
 
@@ -99,6 +100,8 @@ struct KWork {                  // per-N workspace (grown on demand)
   int* scratch = nullptr;       // sort scratch (sort_scratch_ints)
   int64_t scratch_cap = 0;
   double* grid = nullptr;       // real grid Mt x Mt x M (H, then H~)
+  double* grid3 = nullptr;      // SE3P: the folded periodic grid Mfree x Mfree x M
+  int64_t grid3_cap = 0;
   double2* planes = nullptr;    // Hk: n_planes x Mt x Mt
   double2* T = nullptr;         // 2D pass workspace
   int64_t grid_cap = 0, planes_cap = 0, T_cap = 0;
@@ -137,5 +140,8 @@ void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& 
 void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
                     cudaStream_t st);
 void k_gather(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
+// SE3P (se3p.cu): fold the extended grid of the 1P tile plan onto the periodic grid and back
+void k_fold_3p(const KPlan& ext, const double* grid_ext, double* grid_per, cudaStream_t st);
+void k_unfold_3p(const KPlan& ext, const double* grid_per, double* grid_ext, cudaStream_t st);
 
 }  // namespace se1p

@@ -163,7 +163,8 @@ __global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const 
     if (kernel_class) {
       m = khat[((int64_t)n * W + a) * W + y];
     } else {
-      m = pn.x * exJ[a] * exJ[y] / (k2J[a] + k2J[y] + pn.y);
+      const double den = k2J[a] + k2J[y] + pn.y;   // 0 only at k = 0 of an SE3P plan: mode dropped
+      m = den > 0.0 ? pn.x * exJ[a] * exJ[y] / den : 0.0;
     }
     double2 v = out[c * SW + a];
     out[c * SW + a] = make_double2(v.x * m, v.y * m);
