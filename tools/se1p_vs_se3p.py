@@ -15,7 +15,9 @@ from se1p_synth import make_system  # noqa: E402
 XI = 4.0
 # (N, L, M and n_l at 1e-5, M and n_l at 1e-9) -- tab:params
 ROWS = [(20000, 5.43, 52, 7, 68, 10), (40000, 6.84, 64, 9, 82, 11), (60000, 7.83, 76, 10, 94, 13),
-        (80000, 8.62, 88, 10, 104, 14), (100000, 9.29, 96, 12, 114, 15)]
+        (80000, 8.62, 88, 10, 104, 14), (100000, 9.29, 96, 12, 114, 15),
+        # B200-scale rows at the same density, h and M/n_l as the table (extrapolated, not the paper's)
+        (500000, 15.874, 152, 20, 200, 29), (2000000, 25.198, 240, 32, 320, 47)]
 
 
 def timed(fn, reps=5):

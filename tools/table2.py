@@ -14,6 +14,16 @@ from se1p_synth import make_system  # noqa: E402
 P, xi, L = 12, 1.0, (1.0, 1.0, 1.0)
 
 
+def _factors(n):
+    f, d = [], 2
+    while d * d <= n:
+        while n % d == 0:
+            f.append(d)
+            n //= d
+        d += 1
+    return f + ([n] if n > 1 else [])
+
+
 def fft_ms(x, q, M, n_l, S, Nt):
     kw = dict(n_local=n_l, S0=S, SI=S, Ntilde=Nt, skip_checks=True, profile=True)
     acc = 0.0
@@ -29,16 +39,18 @@ x, q = make_system(20000, L, 3)
 x, q = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
 rows = {}
 for s in (2, 4):
-    for M in (16, 32, 48, 64, 80, 96, 112, 128):
+    for M in (16, 32, 48, 64, 80, 96, 112, 128, 192, 256):
         Mt = M + P
         S = -(-s * Mt // 1)
-        info = se1p.plan_info(L, xi * M / 16, M, P, n_local=8 if M > 16 else M // 2, S0=S, SI=S)
-        Nt = info["Ntilde"]
+        # J modes of the AFT unpadded (s = 1, as in the paper): the FFT-friendly extent >= M~
+        Nt = next(n for n in range(Mt, 2 * Mt) if all(f in (2, 3, 5) for f in _factors(n)))
+        info = se1p.plan_info(L, xi * M / 16, M, P, n_local=8 if M > 16 else M // 2, S0=S, SI=S, Ntilde=Nt)
         t_aft = fft_ms(x, q, M, min(8, M // 2), S, Nt)
         t_plain = fft_ms(x, q, M, M // 2, S, Nt)
         rows[(s, M)] = t_plain / t_aft
         print(json.dumps({"s": s, "M": M, "Mt": Mt, "S": S, "Ntilde": Nt, "LK": info["LK"], "aft_ms": t_aft,
                           "plain_ms": t_plain, "ratio": t_plain / t_aft}), flush=True)
-print("M    " + " ".join(f"{M:6d}" for M in (16, 32, 48, 64, 80, 96, 112, 128)))
+MS = (16, 32, 48, 64, 80, 96, 112, 128, 192, 256)
+print("M    " + " ".join(f"{M:6d}" for M in MS))
 for s in (2, 4):
-    print(f"s={s}  " + " ".join(f"{rows[(s, M)]:6.2f}" for M in (16, 32, 48, 64, 80, 96, 112, 128)))
+    print(f"s={s}  " + " ".join(f"{rows[(s, M)]:6.2f}" for M in MS))
