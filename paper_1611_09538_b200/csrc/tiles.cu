@@ -41,6 +41,13 @@ constexpr int kCW = 16;                          // consumer warps
 #ifndef SE1P_EXP_WARPS
 #define SE1P_EXP_WARPS 8
 #endif
+// z extent of the gather's DMMA blocks: 4 (m16n8k4), 8 (m16n8k8) or 16 (m16n8k16)
+#ifndef SE1P_GATHER_KZ
+#define SE1P_GATHER_KZ 8
+#endif
+#ifndef SE1P_GATHER_KZ_FIELD
+#define SE1P_GATHER_KZ_FIELD 4
+#endif
 #ifndef SE1P_EXP_WARPS_FIELD
 #define SE1P_EXP_WARPS_FIELD 4
 #endif
@@ -133,6 +140,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // bits of the 8-node z blocks covering tile offsets [lo, hi), hi > lo
 __device__ __forceinline__ int zbits(int lo, int hi) { return ((1 << ((hi + 7) >> 3)) - 1) & ~((1 << (lo >> 3)) - 1); }
 
+// the same for 4-node blocks (the gather's m16n8k4 granularity)
+__device__ __forceinline__ int zbits4(int lo, int hi) { return ((1 << ((hi + 3) >> 2)) - 1) & ~((1 << (lo >> 2)) - 1); }
+
 // z tiles (extent TZ) hit by the stencil nodes a, a+1, ..., a+P-1 (mod M), a in [0,M): first the
 // tiles of [a, min(a+P,M)), then those of the wrapped part [0, a+P-M) not already listed.
 // zslot gives the canonical position of tile tz (-1: not hit); k_gather_finish walks the same list.
@@ -158,6 +168,21 @@ __device__ __forceinline__ int zmask_of(int d, int P, int M, int jmax) {
   if (lo2 < jmax) zm |= zbits(lo2, min(lo2 + P, jmax));
   return zm;
 }
+__device__ __forceinline__ int zbits16(int lo, int hi) { return ((1 << ((hi + 15) >> 4)) - 1) & ~((1 << (lo >> 4)) - 1); }
+__device__ __forceinline__ int zmask16_of(int d, int P, int M, int jmax) {
+  int zm = 0;
+  if (d < P) zm |= zbits16(0, min(P - d, jmax));
+  const int lo2 = M - d;
+  if (lo2 < jmax) zm |= zbits16(lo2, min(lo2 + P, jmax));
+  return zm;
+}
+__device__ __forceinline__ int zmask4_of(int d, int P, int M, int jmax) {
+  int zm = 0;
+  if (d < P) zm |= zbits4(0, min(P - d, jmax));
+  const int lo2 = M - d;
+  if (lo2 < jmax) zm |= zbits4(lo2, min(lo2 + P, jmax));
+  return zm;
+}
 
 // FIELD (gather only): also the field E = -grad phi at the particles -- the gradient of the
 // gather (Eq. (force_se1p)): d/dx_p e^{-alpha (node - x_p)^2} = 2 alpha (node - x_p) w.
@@ -167,6 +192,7 @@ __global__ void __launch_bounds__(n_threads(FIELD), 1) k_tiles(const TileArgs A)
   constexpr int RSE = exp_stride(TZ, FIELD);
   constexpr int kEW = n_exp_warps(FIELD), kThreads = n_threads(FIELD), kRec = rec_len(FIELD);
   constexpr int NC = FIELD ? 4 : 1;   // gather outputs per particle: phi (and d/dx, d/dy, d/dz)
+  constexpr int KZ = FIELD ? SE1P_GATHER_KZ_FIELD : SE1P_GATHER_KZ;   // gather DMMA z extent
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
@@ -543,7 +569,11 @@ auto reduce = [&](int b, int rt) {
         if (ox >= -3 && ox <= P - 1 && oy >= -3 && oy <= P - 1) {
           int d = Z0 - s.w;
           if (d < 0) d += M;
-          const int zm = zmask_of(d, P, M, jmax);
+          // z blocks of SE1P_GATHER_KZ nodes: a 24-node window meets 6-7 4-node, 3-4 8-node or
+          // 2-3 16-node blocks (89%, 77%, 60% of the issued work inside the stencil); measured,
+          // the instruction count binds, not the DMMA work: at C5 KZ = 4 / 16 are 34% / 14% slower
+          // than 8 for the potential; the field (twice the DMMAs per list entry) gains 5% at 4
+          const int zm = KZ == 4 ? zmask4_of(d, P, M, jmax) : (KZ == 16 ? zmask16_of(d, P, M, jmax) : zmask_of(d, P, M, jmax));
           rel = zm != 0;
           e = p | (zm << 8);
         }
@@ -602,6 +632,44 @@ auto reduce = [&](int b, int rt) {
         const double* z1 = r1 + tig;
         double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
         double u0[4] = {0.0, 0.0, 0.0, 0.0}, u1[4] = {0.0, 0.0, 0.0, 0.0};   // field: wz' H~
+        if (KZ == 16) {
+#pragma unroll
+        for (int zq = 0; zq < NZB / 2; ++zq)
+          if ((zm >> zq) & 1) {
+            double a[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              a[2 * i] = z0[zoff(16 * zq + 4 * i)];
+              a[2 * i + 1] = z1[zoff(16 * zq + 4 * i)];
+            }
+            dmma_16x8x16(t0, a, hB[2 * zq][0][0], hB[2 * zq][0][1], hB[2 * zq + 1][0][0], hB[2 * zq + 1][0][1]);
+            dmma_16x8x16(t1, a, hB[2 * zq][1][0], hB[2 * zq][1][1], hB[2 * zq + 1][1][0], hB[2 * zq + 1][1][1]);
+            if (FIELD) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                a[2 * i] = z0[zoffd(TZ, 16 * zq + 4 * i)];
+                a[2 * i + 1] = z1[zoffd(TZ, 16 * zq + 4 * i)];
+              }
+              dmma_16x8x16(u0, a, hB[2 * zq][0][0], hB[2 * zq][0][1], hB[2 * zq + 1][0][0], hB[2 * zq + 1][0][1]);
+              dmma_16x8x16(u1, a, hB[2 * zq][1][0], hB[2 * zq][1][1], hB[2 * zq + 1][1][0], hB[2 * zq + 1][1][1]);
+            }
+          }
+        } else if (KZ == 4) {
+#pragma unroll
+        for (int zb = 0; zb < NZB; ++zb)
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+            if ((zm >> (2 * zb + s)) & 1) {
+              const double a[2] = {z0[zoff(8 * zb + 4 * s)], z1[zoff(8 * zb + 4 * s)]};
+              dmma_16x8x4(t0, a, hB[zb][0][s]);
+              dmma_16x8x4(t1, a, hB[zb][1][s]);
+              if (FIELD) {
+                const double ad[2] = {z0[zoffd(TZ, 8 * zb + 4 * s)], z1[zoffd(TZ, 8 * zb + 4 * s)]};
+                dmma_16x8x4(u0, ad, hB[zb][0][s]);
+                dmma_16x8x4(u1, ad, hB[zb][1][s]);
+              }
+            }
+        } else {
 #pragma unroll
         for (int zb = 0; zb < NZB; ++zb) {
           if ((zm >> zb) & 1) {
@@ -615,6 +683,7 @@ auto reduce = [&](int b, int rt) {
               dmma_16x8x8(u1, ad, hB[zb][1][0], hB[zb][1][1]);
             }
           }
+        }
         }
         // phi_p = sum_cols wx wy T; field: d/dx uses wx' = 2 alpha (node_x - x_p) wx, d/dy likewise,
         // d/dz the wz'-transformed U (the particles' positions sit in their raw records)

@@ -25,6 +25,13 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b0), "d"(b1));
 }
 
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], const double (&a)[2], double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(b0));
+}
+
 __device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8], double b0, double b1, double b2,
                                              double b3) {
   asm volatile(

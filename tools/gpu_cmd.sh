@@ -1,2 +1,2 @@
-timeout 900 python tools/se1p_vs_se3p.py > gpurun_out/se1p_vs_se3p.log 2>&1; tail -15 gpurun_out/se1p_vs_se3p.log
-timeout 600 python tools/table2.py > gpurun_out/table2.log 2>&1; tail -4 gpurun_out/table2.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for m in tiles field; do timeout 300 python tools/stage_times.py C5 $m; done
