@@ -84,7 +84,7 @@ struct TileArgs {
 };
 
 struct TileSmem {
-  int off_lists, off_acc, off_raw, off_exp, total;
+  int off_lists, off_rel, off_acc, off_raw, off_exp, total;
 };
 
 __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather, bool field = false) {
@@ -93,6 +93,9 @@ __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gathe
   o = (o + 15) & ~15;
   s.off_lists = o;
   o += kCW * (BM + 32) * 4;
+  o = (o + 15) & ~15;
+  s.off_rel = o;   // per batch particle: consumer-warp mask (16 bits) | z-block mask << 16
+  o += NB * BM * 4;
   o = (o + 15) & ~15;
   s.off_acc = o;
   if (gather) o += NB * BM * (kCW + 1) * (field ? 4 : 1) * 8;
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(n_threads(FIELD), 1) k_tiles(const TileArgs A)
   int* cnt = reinterpret_cast<int*>(freeb + kMaxNB);
   double* f1 = reinterpret_cast<double*>(cnt + kMaxNB);
   int* lists = reinterpret_cast<int*>(smem + L.off_lists);
+  int* relm = reinterpret_cast<int*>(smem + L.off_rel);
   double* acc = reinterpret_cast<double*>(smem + L.off_acc);
   double* raws = reinterpret_cast<double*>(smem + L.off_raw);
   double* exps = reinterpret_cast<double*>(smem + L.off_exp);
@@ -370,6 +374,23 @@ auto reduce = [&](int b, int rt) {
         for (int p = 8 * ew + (lane >> 2); p < cn; p += 8 * kEW) {
           const double* r = rb + p * kRec;
           const int4 s = *reinterpret_cast<const int4*>(r);
+          if (kind == 0) {
+            // which consumer warps (4 x 4 column blocks of 4 x 4 columns) the stencil meets, and its
+            // z blocks: computed once here instead of by each of the 16 consumer warps
+            const int bx0 = max(fdiv(s.x - X0, 4), 0), bx1 = min(fdiv(s.x - X0 + P - 1, 4), 3);
+            const int by0 = max(fdiv(s.y - Y0, 4), 0), by1 = min(fdiv(s.y - Y0 + P - 1, 4), 3);
+            int d = Z0 - s.w;
+            if (d < 0) d += M;
+            const int zm = !GATHER ? zmask_of(d, P, M, jmax)
+                                   : (KZ == 4 ? zmask4_of(d, P, M, jmax)
+                                              : (KZ == 16 ? zmask16_of(d, P, M, jmax) : zmask_of(d, P, M, jmax)));
+            int wm = 0;
+            if (zm != 0 && bx0 <= bx1 && by0 <= by1) {
+              const int xb = ((1 << (bx1 + 1)) - 1) & ~((1 << bx0) - 1);
+              for (int by = by0; by <= by1; ++by) wm |= xb << (4 * by);
+            }
+            relm[b * BM + p] = wm | (zm << 16);
+          }
           const int ax = kind < 2 ? kind : 2;
           const double A0 = (ax == 0 && !GATHER) ? r[4] * r[2] : r[4 + 2 * ax];   // gridding: q in wx
           const double E = r[5 + 2 * ax];
@@ -512,23 +533,12 @@ auto reduce = [&](int b, int rt) {
         if (lane == 0 && bprev >= 0) mbar_arrive(&empty[bprev]);
         break;
       }
-      const double* rb = raws + b * BM * kRec;
       int n = held;
       for (int p0 = 0; p0 < cn; p0 += 32) {
         const int p = p0 + lane;
-        bool rel = false;
-        int e = 0;
-        if (p < cn) {
-          const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
-          const int ox = X0b - s.x, oy = Y0b - s.y;
-          if (ox >= -3 && ox <= P - 1 && oy >= -3 && oy <= P - 1) {
-            int d = Z0 - s.w;
-            if (d < 0) d += M;
-            const int zm = zmask_of(d, P, M, jmax);
-            rel = zm != 0;
-            e = p | (b << kEntB) | (zm << kEntZ);
-          }
-        }
+        const int r = p < cn ? relm[b * BM + p] : 0;   // expander-computed relevance (see above)
+        const bool rel = (r >> w) & 1;
+        const int e = p | (b << kEntB) | ((r >> 16) << kEntZ);
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
         if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
         n += __popc(bal);
@@ -559,25 +569,15 @@ auto reduce = [&](int b, int rt) {
     const double* eb = exps + b * ES;
     // particles of the batch meeting this warp's 4 x 4 column block (order preserving)
     int n = 0;
+    // z blocks of KZ nodes: a 24-node window meets 6-7 4-node, 3-4 8-node or 2-3 16-node blocks
+    // (89%, 77%, 60% of the issued work inside the stencil); measured, the instruction count binds,
+    // not the DMMA work: at C5 KZ = 4 / 16 are 34% / 14% slower than 8 for the potential; the
+    // field (twice the DMMAs per list entry) gains 5% at 4
     for (int p0 = 0; p0 < cn; p0 += 32) {
       const int p = p0 + lane;
-      bool rel = false;
-      int e = 0;
-      if (p < cn) {
-        const int4 s = *reinterpret_cast<const int4*>(rb + p * kRec);
-        const int ox = X0b - s.x, oy = Y0b - s.y;
-        if (ox >= -3 && ox <= P - 1 && oy >= -3 && oy <= P - 1) {
-          int d = Z0 - s.w;
-          if (d < 0) d += M;
-          // z blocks of SE1P_GATHER_KZ nodes: a 24-node window meets 6-7 4-node, 3-4 8-node or
-          // 2-3 16-node blocks (89%, 77%, 60% of the issued work inside the stencil); measured,
-          // the instruction count binds, not the DMMA work: at C5 KZ = 4 / 16 are 34% / 14% slower
-          // than 8 for the potential; the field (twice the DMMAs per list entry) gains 5% at 4
-          const int zm = KZ == 4 ? zmask4_of(d, P, M, jmax) : (KZ == 16 ? zmask16_of(d, P, M, jmax) : zmask_of(d, P, M, jmax));
-          rel = zm != 0;
-          e = p | (zm << 8);
-        }
-      }
+      const int r = p < cn ? relm[b * BM + p] : 0;   // expander-computed relevance
+      const bool rel = (r >> w) & 1;
+      const int e = p | ((r >> 16) << 8);
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
       if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
       n += __popc(bal);
