@@ -18,9 +18,23 @@
 namespace se1p {
 
 static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // columns (2 per FFT)
-static int rows_for(int W) { int r = 98304 / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
-static int cols_for(int W) { return W > 400 ? 4 : 8; }
-constexpr int kFftThreads = 256;   // threads per block of the FFT passes
+// shared-memory budget of a row-pass block and columns per column-pass block (build knobs, see
+// tools/exp_variant.sh)
+#ifndef SE1P_ROW_SMEM
+#define SE1P_ROW_SMEM 49152   // measured: 96 KB -> 48 KB is -7% (C5) / -8% (C4) on the mode stage
+#endif
+#ifndef SE1P_COLS_SMALL
+#define SE1P_COLS_SMALL 8
+#endif
+#ifndef SE1P_COLS_LARGE
+#define SE1P_COLS_LARGE 4
+#endif
+#ifndef SE1P_FFT_THREADS
+#define SE1P_FFT_THREADS 256
+#endif
+static int rows_for(int W) { int r = SE1P_ROW_SMEM / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
+static int cols_for(int W) { return W > 400 ? SE1P_COLS_LARGE : SE1P_COLS_SMALL; }
+constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT passes
 
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
 // Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if

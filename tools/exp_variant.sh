@@ -5,7 +5,7 @@ for v in "$@"; do
   SE1P_NVCC_EXTRA="$v" timeout 300 python -c "from paper_1611_09538_b200 import build as b; b.build(force=True)" || continue
   echo "== [$v]"
   timeout 200 python tools/stage_times.py C5 tiles
-  timeout 200 python tools/stage_times.py C5 field
+  [ -z "$NO_FIELD" ] && timeout 200 python tools/stage_times.py C5 field
   timeout 200 python tools/stage_times.py C4 tiles
   if [ -n "$RUN_PARITY" ]; then timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_field.py -x -q 2>&1 | tail -2; fi
 done > gpurun_out/exp_$tag.log 2>&1
