@@ -58,7 +58,7 @@ constexpr int kMaxNB = 4;
 // particle position (112 B)
 __host__ __device__ constexpr int rec_len(bool field) { return field ? 14 : 10; }
 constexpr int kMaxP = 64;
-constexpr int kEntB = 7, kEntZ = 9;              // gridding list entry: p (7 bits), buffer (2), z mask
+constexpr int kEntZ = 16;                        // gridding list entry: smem row offset (16 bits), z mask
 
 // Expanded row: 16-entry window segments wx, wy, wz[0:16), wz[16:32) at offsets 0, 17, 34, 51
 // (17 apart: when 8 particles x 4 segments are written by one warp, the 32 lanes fall into
@@ -507,7 +507,7 @@ auto reduce = [&](int b, int rt) {
         const double* rz[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const double* r = exps + ((e[j] >> kEntB) & 3) * ES + (e[j] & ((1 << kEntB) - 1)) * RSE;
+          const double* r = exps + (e[j] & 0xffff);   // the entry holds its expanded row's offset
           const double wq = r[kEX + cx];
           a[2 * j] = wq * r[kEY + cy];
           a[2 * j + 1] = wq * r[kEY + cy + 2];
@@ -525,7 +525,7 @@ auto reduce = [&](int b, int rt) {
       const int cn = cnt[b];
       if (cn < 0) {
         if (held > 0) {   // flush the carried entries, padded to 16
-          if (lane < 16 - held) wl[held + lane] = dummy;
+          if (lane < 16 - held) wl[held + lane] = BM * RSE;   // the all-zero row of buffer 0
           __syncwarp();
           ksteps(0, 16);
         }
@@ -538,7 +538,7 @@ auto reduce = [&](int b, int rt) {
         const int p = p0 + lane;
         const int r = p < cn ? relm[b * BM + p] : 0;   // expander-computed relevance (see above)
         const bool rel = (r >> w) & 1;
-        const int e = p | (b << kEntB) | ((r >> 16) << kEntZ);
+        const int e = (b * ES + p * RSE) | ((r >> 16) << kEntZ);
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
         if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
         n += __popc(bal);
@@ -547,7 +547,7 @@ auto reduce = [&](int b, int rt) {
       int kend = n & ~15;
       if (kend < held) {   // fewer than 16 entries and some carried: flush everything (padded)
         kend = (n + 15) & ~15;
-        if (lane < kend - n) wl[n + lane] = dummy;
+        if (lane < kend - n) wl[n + lane] = BM * RSE;
         __syncwarp();
       }
       if (!(dv.dbg & 2)) ksteps(0, kend);

@@ -1,1 +1,3 @@
-NO_FIELD=1 bash tools/exp_variant.sh modes2 "-DSE1P_ROW_SMEM=32768" "-DSE1P_ROW_SMEM=20480" "-DSE1P_ROW_SMEM=49152 -DSE1P_COLS_SMALL=4 -DSE1P_COLS_LARGE=2" "-DSE1P_ROW_SMEM=32768 -DSE1P_COLS_SMALL=4 -DSE1P_COLS_LARGE=2"
+for m in tiles; do timeout 300 python tools/stage_times.py C5 $m; done
+timeout 300 python tools/stage_times.py C4 tiles
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
