@@ -21,12 +21,18 @@ d = defaultdict(list)
 for r in rows[1:]:
     d[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
 tot = sum(sum(v) for v in d.values())
+# plan-time kernels (run once per plan, outside every timed step) and the one-off input check
+PLAN = ("k_kern_a", "k_kern_b", "k_fft_rows_inplace", "k_transpose", "k_transpose_scale_real", "k_check")
+step_tot = sum(sum(v) for k, v in d.items() if k.split()[-1].split("<")[0] not in PLAN)
 with open(f"profiles/{tag}_launches_C5_summary.txt", "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py (C5)\n")
-    f.write("cold-cache serialised launch times over every call of the run (plan, warm-up, timed, profiled, e2e)\n")
-    f.write(f"{'total ms':>9} {'n':>4} {'avg ms':>8} {'share':>6}  kernel\n")
+    f.write("cold-cache serialised launch times over every call of the run (plan, warm-up, timed, profiled, e2e);\n")
+    f.write("'step share' leaves out the plan-time kernels (marked *) -- compare it with bench.py's stages_ms\n")
+    f.write(f"{'total ms':>9} {'n':>4} {'avg ms':>8} {'share':>6} {'step share':>10}  kernel\n")
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        f.write(f"{sum(v)/1e6:9.3f} {len(v):4d} {sum(v)/len(v)/1e6:8.3f} {100*sum(v)/tot:5.1f}%  {k}\n")
+        plan = k.split()[-1].split("<")[0] in PLAN
+        ss = "" if plan else f"{100*sum(v)/step_tot:9.1f}%"
+        f.write(f"{sum(v)/1e6:9.3f} {len(v):4d} {sum(v)/len(v)/1e6:8.3f} {100*sum(v)/tot:5.1f}% {ss:>10}  {k}{' *' if plan else ''}\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
@@ -52,7 +58,12 @@ with open(f"profiles/{tag}_ncu_tiles_C5.txt", "w") as f:
         def tobytes(v):
             x, u = float(v[0].replace(",", "")), v[1]
             return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        key = "gather" if ", 1>" in name or "true" in name else "spread"
+        import re
+        targs = re.search(r"k_tiles<([^>]*)>", name)
+        args = [t.strip() for t in targs.group(1).split(",")] if targs else []
+        gather = len(args) > 1 and args[1] in ("1", "true", "(bool)1")
+        field = len(args) > 2 and args[2] in ("1", "true", "(bool)1")
+        key = ("gather_field" if field else "gather") if gather else "spread"
         traffic[key] = tobytes(vals["dram__bytes_read.sum"]) + tobytes(vals["dram__bytes_write.sum"])
 json.dump({**traffic, "source": rep, "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, C5"},
           open("profiles/traffic.json", "w"), indent=1)
