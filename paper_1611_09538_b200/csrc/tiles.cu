@@ -587,35 +587,6 @@ auto reduce = [&](int b, int rt) {
     __syncwarp();
 
     if (dv.dbg & 2) {
-    } else if (!GATHER) {
-      // C[16 cols x 8 z] += A[16 cols x 16 particles] B[16 particles x 8 z]; particle of k-slot
-      // tig + 4j is list entry k + tig + 4j (A and B agree on it)
-      const int cx = xo + (gid & 3), cy = yo + (gid >> 2);
-      for (int k = 0; k < npad; k += 16) {
-        int e[4], zm = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          e[j] = wl[k + tig + 4 * j];
-          zm |= e[j];
-        }
-        zm = (zm >> 8) & 0xff;
-        zm |= __shfl_xor_sync(0xffffffffu, zm, 1);
-        zm |= __shfl_xor_sync(0xffffffffu, zm, 2);
-        double a[8];
-        const double* rz[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double* r = eb + (e[j] & 0xff) * RSE;
-          const double wq = r[kEX + cx];
-          a[2 * j] = wq * r[kEY + cy];
-          a[2 * j + 1] = wq * r[kEY + cy + 2];
-          rz[j] = r + gid;
-        }
-#pragma unroll
-        for (int zb = 0; zb < NZB; ++zb)
-          if ((zm >> zb) & 1)
-            dmma_16x8x16(c[zb], a, rz[0][zoff(8 * zb)], rz[1][zoff(8 * zb)], rz[2][zoff(8 * zb)], rz[3][zoff(8 * zb)]);
-      }
     } else {
       // T[16 particles x 8 cols] = A[16 particles x 8 z] (wz) B[8 z x 8 cols] (H~), per col half;
       // particle of row gid (gid + 8) is list entry k + gid (k + gid + 8)

@@ -1,3 +1,1 @@
-for m in tiles; do timeout 300 python tools/stage_times.py C5 $m; done
-timeout 300 python tools/stage_times.py C4 tiles
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+NO_FIELD=1 RUN_PARITY=1 bash tools/exp_variant.sh nb "" "-DSE1P_GRID_NOBRANCH=1" "-DSE1P_GATHER_ACC2=1"
