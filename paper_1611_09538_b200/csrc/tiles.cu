@@ -48,15 +48,23 @@ constexpr int kCW = 16;                          // consumer warps
 #ifndef SE1P_GATHER_KZ_FIELD
 #define SE1P_GATHER_KZ_FIELD 4
 #endif
+#ifndef SE1P_FIELD_ONE_PASS
+#define SE1P_FIELD_ONE_PASS 0
+#endif
 #ifndef SE1P_EXP_WARPS_FIELD
 #define SE1P_EXP_WARPS_FIELD 4
 #endif
-__host__ __device__ constexpr int n_exp_warps(bool field) { return field ? SE1P_EXP_WARPS_FIELD : SE1P_EXP_WARPS; }
-__host__ __device__ constexpr int n_threads(bool field) { return (kCW + 1 + n_exp_warps(field)) * 32; }
+// Field modes of the gather (FM): 0 potential; the field E = -grad phi in two passes over the same
+// tiles, 1: phi, d/dx, d/dy (x, y window derivatives in the epilogue) and 2: d/dz (the expanders
+// write the z-derivative window 2 alpha (node - z_p) wz in place of wz); 3: all four in one pass
+// (a second z window and accumulator set).
+__host__ __device__ constexpr int n_exp_warps(int fm) { return fm == 3 ? SE1P_EXP_WARPS_FIELD : SE1P_EXP_WARPS; }
+__host__ __device__ constexpr int n_threads(int fm) { return (kCW + 1 + n_exp_warps(fm)) * 32; }
+__host__ __device__ constexpr int fm_outputs(int fm) { return fm == 0 ? 1 : (fm == 1 ? 3 : (fm == 2 ? 1 : 4)); }
 constexpr int kMaxNB = 4;
 // doubles per compact record: {s4, q, index, (A, E) per axis} (80 B); the field gather adds the
 // particle position (112 B)
-__host__ __device__ constexpr int rec_len(bool field) { return field ? 14 : 10; }
+__host__ __device__ constexpr int rec_len(int field) { return field ? 14 : 10; }
 constexpr int kMaxP = 64;
 constexpr int kEntZ = 16;                        // gridding list entry: smem row offset (16 bits), z mask
 
@@ -65,8 +73,8 @@ constexpr int kEntZ = 16;                        // gridding list entry: smem ro
 // distinct bank pairs); row stride = 4 (mod 16) doubles, so the 4 particles of a consumer
 // k-step start 4 banks apart.
 // The field gather appends the z-derivative window wz'[j] = 2 alpha (node - z_p) wz[j] at 68 and 85.
-__host__ __device__ constexpr int exp_stride(int TZ, bool field = false) {
-  return field ? (TZ == 32 ? 116 : 68) : (TZ == 32 ? 68 : 52);
+__host__ __device__ constexpr int exp_stride(int TZ, int fm = 0) {
+  return fm == 3 ? (TZ == 32 ? 116 : 68) : (TZ == 32 ? 68 : 52);
 }
 constexpr int kEX = 0, kEY = 17, kEZ = 34;
 __host__ __device__ constexpr int zoff(int j) { return kEZ + j + (j >= 16 ? 1 : 0); }   // wz[j]
@@ -87,7 +95,7 @@ struct TileSmem {
   int off_lists, off_rel, off_acc, off_raw, off_exp, total;
 };
 
-__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather, bool field = false) {
+__host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gather, int fm = 0) {
   TileSmem s;
   int o = 4 * kMaxNB * 8 + kMaxNB * 4 + kMaxP * 8;   // barriers, counts, f1
   o = (o + 15) & ~15;
@@ -98,13 +106,13 @@ __host__ __device__ inline TileSmem tile_smem(int BM, int NB, int TZ, bool gathe
   o += NB * BM * 4;
   o = (o + 15) & ~15;
   s.off_acc = o;
-  if (gather) o += NB * BM * (kCW + 1) * (field ? 4 : 1) * 8;
+  if (gather) o += NB * BM * (kCW + 1) * fm_outputs(fm) * 8;
   o = (o + 127) & ~127;
   s.off_raw = o;
-  o += NB * BM * rec_len(field) * 8;
+  o += NB * BM * rec_len(fm) * 8;
   o = (o + 127) & ~127;
   s.off_exp = o;
-  o += NB * (BM + 1) * exp_stride(TZ, field) * 8;
+  o += NB * (BM + 1) * exp_stride(TZ, fm) * 8;
   s.total = o;
   return s;
 }
@@ -189,17 +197,20 @@ __device__ __forceinline__ int zmask4_of(int d, int P, int M, int jmax) {
 
 // FIELD (gather only): also the field E = -grad phi at the particles -- the gradient of the
 // gather (Eq. (force_se1p)): d/dx_p e^{-alpha (node - x_p)^2} = 2 alpha (node - x_p) w.
-template <int TZ, bool GATHER, bool FIELD = false>
-__global__ void __launch_bounds__(n_threads(FIELD), 1) k_tiles(const TileArgs A) {
+template <int TZ, bool GATHER, int FM = 0>
+__global__ void __launch_bounds__(n_threads(FM), 1) k_tiles(const TileArgs A) {
   constexpr int NZB = TZ / 8;
-  constexpr int RSE = exp_stride(TZ, FIELD);
-  constexpr int kEW = n_exp_warps(FIELD), kThreads = n_threads(FIELD), kRec = rec_len(FIELD);
-  constexpr int NC = FIELD ? 4 : 1;   // gather outputs per particle: phi (and d/dx, d/dy, d/dz)
+  constexpr bool FIELD = FM == 3;     // one-pass field: second z window and accumulators
+  constexpr int RSE = exp_stride(TZ, FM);
+  constexpr int kEW = n_exp_warps(FM), kThreads = n_threads(FM), kRec = rec_len(FM);
+  constexpr int NC = fm_outputs(FM);  // gather outputs per particle of this pass
+  constexpr int NCT = FM ? 4 : 1;     // values per gather slot: phi (and d/dx, d/dy, d/dz)
+  constexpr int COFF = FM == 2 ? 3 : 0;   // first slot value this pass writes
   constexpr int KZ = FIELD ? SE1P_GATHER_KZ_FIELD : SE1P_GATHER_KZ;   // gather DMMA z extent
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
-  const TileSmem L = tile_smem(BM, NB, TZ, GATHER, FIELD);
+  const TileSmem L = tile_smem(BM, NB, TZ, GATHER, FM);
   uint64_t* rawb = reinterpret_cast<uint64_t*>(smem);
   uint64_t* full = rawb + kMaxNB;
   uint64_t* empty = full + kMaxNB;
@@ -256,7 +267,7 @@ auto reduce = [&](int b, int rt) {
             sum += ap[v * NC + cc];
             ap[v * NC + cc] = 0.0;
           }
-          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NC + cc] = sum;
+          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NCT + COFF + cc] = sum;
         }
       } else if (hx) {
         for (int v = 0; v < kCW * NC; ++v)
@@ -437,7 +448,10 @@ auto reduce = [&](int b, int rt) {
                 v = g[c] * f1[tt];
                 g[c] *= E;
               }
-              o[8 * c + i] = v;
+              if (FM == 2 && ax == 2)   // pass 2: the z-derivative window in place of wz
+                o[8 * c + i] = 2.0 * dv.alpha * ((double)(s.z + tt) * dv.h - r[12]) * v;
+              else
+                o[8 * c + i] = v;
               if (FIELD && od) od[8 * c + i] = 2.0 * dv.alpha * ((double)(s.z + tt) * dv.h - r[12]) * v;
               if (++tc[c] == Mw) {   // periodic wrap: the stencil restarts at node 0
                 tc[c] = 0;
@@ -666,7 +680,7 @@ auto reduce = [&](int b, int rt) {
           const double* tt1 = t1 + 2 * h;
           const double wx0 = r[kEX + cx0], wx1 = r[kEX + cx0 + 1], wy0 = r[kEY + cy0], wy2 = r[kEY + cy0 + 2];
           v[h][0] = wy0 * fma(wx0, tt0[0], wx1 * tt0[1]) + wy2 * fma(wx0, tt1[0], wx1 * tt1[1]);
-          if (FIELD) {
+          if (FM == 1 || FM == 3) {
             const int ph = (h ? e1 : e0) & 0xff;
             const double* rr = rb + (ph < BM ? ph : 0) * kRec;
             const double px = rr[10], py = rr[11];
@@ -674,11 +688,13 @@ auto reduce = [&](int b, int rt) {
             const double ta = 2.0 * dv.alpha;
             const double wxd0 = ta * nx0 * wx0, wxd1 = ta * (nx0 + dv.h) * wx1;
             const double wyd0 = ta * ny0 * wy0, wyd2 = ta * (ny0 + 2.0 * dv.h) * wy2;
-            const double* uu0 = u0 + 2 * h;
-            const double* uu1 = u1 + 2 * h;
             v[h][1] = wy0 * fma(wxd0, tt0[0], wxd1 * tt0[1]) + wy2 * fma(wxd0, tt1[0], wxd1 * tt1[1]);
             v[h][2] = wyd0 * fma(wx0, tt0[0], wx1 * tt0[1]) + wyd2 * fma(wx0, tt1[0], wx1 * tt1[1]);
-            v[h][3] = wy0 * fma(wx0, uu0[0], wx1 * uu0[1]) + wy2 * fma(wx0, uu1[0], wx1 * uu1[1]);
+            if (FIELD) {
+              const double* uu0 = u0 + 2 * h;
+              const double* uu1 = u1 + 2 * h;
+              v[h][NC - 1] = wy0 * fma(wx0, uu0[0], wx1 * uu0[1]) + wy2 * fma(wx0, uu1[0], wx1 * uu1[1]);
+            }
           }
         }
 #pragma unroll
@@ -811,7 +827,7 @@ void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool
   SE1P_LAUNCH_CHECK();
 }
 
-template <int TZ, bool GATHER, bool FIELD>
+template <int TZ, bool GATHER, int FM>
 static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   TileArgs a;
   a.dv = pl.dv;
@@ -837,9 +853,9 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   int BM = 0, NB = 0;
   const int limit = 227 * 1024 - 1024;
   for (int bm : {64, 32, 16}) {   // the gather's lag-2 reduction needs NB >= 3
-    if (FIELD && bm > 32) continue;
+    if (FM == 3 && bm > 32) continue;
     for (int nb = kMaxNB; nb >= (GATHER ? 3 : 2) && !BM; --nb)
-      if (tile_smem(bm, nb, TZ, GATHER, FIELD).total <= limit) {
+      if (tile_smem(bm, nb, TZ, GATHER, FM).total <= limit) {
         BM = bm;
         NB = nb;
       }
@@ -848,28 +864,36 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
   if (!BM) throw Error{4, "tile kernels do not fit in shared memory"};
   a.BM = BM;
   a.NB = NB;
-  const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER, FIELD).total;
-  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER, FIELD>,
+  const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER, FM).total;
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_tiles<TZ, GATHER, FM>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned nblk = (unsigned)(ntx * a.nty * a.ntz);
-  k_tiles<TZ, GATHER, FIELD><<<nblk, n_threads(FIELD), smem, st>>>(a);
+  k_tiles<TZ, GATHER, FM><<<nblk, n_threads(FM), smem, st>>>(a);
   SE1P_LAUNCH_CHECK();
 }
 
-template <bool GATHER, bool FIELD>
+template <bool GATHER, int FM>
 static void dispatch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
   if (tx_hi < 0) tx_hi = (int)ceil_div(pl.dv.Mt, kTXY);
-  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, GATHER, FIELD>(pl, w, N, tx_lo, tx_hi, st);
-  else launch_tiles<16, GATHER, FIELD>(pl, w, N, tx_lo, tx_hi, st);
+  if (tile_tz(pl.dv.M) == 32) launch_tiles<32, GATHER, FM>(pl, w, N, tx_lo, tx_hi, st);
+  else launch_tiles<16, GATHER, FM>(pl, w, N, tx_lo, tx_hi, st);
 }
 
 void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
-  dispatch_tiles<false, false>(pl, w, N, tx_lo, tx_hi, st);
+  dispatch_tiles<false, 0>(pl, w, N, tx_lo, tx_hi, st);
 }
 
 void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi, bool field) {
-  if (field) dispatch_tiles<true, true>(pl, w, N, tx_lo, tx_hi, st);
-  else dispatch_tiles<true, false>(pl, w, N, tx_lo, tx_hi, st);
+  if (field) {
+#if SE1P_FIELD_ONE_PASS
+    dispatch_tiles<true, 3>(pl, w, N, tx_lo, tx_hi, st);
+#else
+    dispatch_tiles<true, 1>(pl, w, N, tx_lo, tx_hi, st);   // phi, d/dx, d/dy
+    dispatch_tiles<true, 2>(pl, w, N, tx_lo, tx_hi, st);   // d/dz
+#endif
+  } else {
+    dispatch_tiles<true, 0>(pl, w, N, tx_lo, tx_hi, st);
+  }
 }
 
 void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st, int tx_lo, int tx_hi,
