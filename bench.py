@@ -125,14 +125,18 @@ def bench_ours(args, cfg, rank, world, local):
     x = torch.from_numpy(x_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
     phi = torch.empty(cfg.N, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # single GPU: a side stream so the step can run as a captured CUDA graph (the legacy default
+    # stream cannot be captured); multi-GPU keeps torch's current stream for NCCL
+    stream = torch.cuda.Stream(device=dev) if world == 1 else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(stream)
     kw = kspace_kwargs(cfg)
     info = se1p.plan_info(cfg.L, cfg.xi, cfg.M, cfg.P, **kw)
 
     def step(xs=x, qs=q):
         if world > 1:
             return sdist.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, stream=stream, **kw)
-        se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, sync=False, skip_checks=True, **kw)
+        se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, sync=False, skip_checks=True,
+                    graph=True, **kw)
         return phi
 
     se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, **kw)   # plan + workspace, validated inputs
@@ -173,11 +177,13 @@ def bench_ours(args, cfg, rank, world, local):
     xh = torch.from_numpy(x_np).pin_memory()
     qh = torch.from_numpy(q_np).pin_memory()
     ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
+    xd = torch.empty_like(x)          # device input buffers the user reuses every step
+    qd = torch.empty_like(q)
     ke = max(3, args.steps // 2)
 
     def e2e_step():
-        xd = xh.to(dev, non_blocking=True)
-        qd = qh.to(dev, non_blocking=True)
+        xd.copy_(xh, non_blocking=True)
+        qd.copy_(qh, non_blocking=True)
         ph.copy_(step(xd, qd), non_blocking=True)
 
     e2e_step()

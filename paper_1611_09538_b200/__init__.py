@@ -108,7 +108,7 @@ def _check(code):
 
 
 def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0,
-          reference_kernels=False):
+          reference_kernels=False, graph=False):
     o = Opts()
     o.Ntilde = int(Ntilde or 0)
     o.S0 = int(S0 or 0)
@@ -119,7 +119,20 @@ def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=
     o.reserved[0] = 1 if profile else 0
     o.reserved[1] = int(stop_after)
     o.reserved[2] = 1 if reference_kernels else 0
+    o.reserved[3] = 1 if graph else 0
     return o
+
+
+_graph_streams = {}
+
+
+def _graph_stream(x):
+    """A per-device side stream for graph capture (the legacy default stream cannot be captured)."""
+    import torch
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    if dev not in _graph_streams:
+        _graph_streams[dev] = torch.cuda.Stream(device=dev)
+    return _graph_streams[dev]
 
 
 def _Larr(L):
@@ -170,21 +183,31 @@ def _outputs(x, N, field, out, field_out):
 
 def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
            out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0,
-           reference_kernels=False, field=False, field_out=None):
+           reference_kernels=False, field=False, field_out=None, graph=False):
     """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1).
     field=True returns (phi^F, E^F) with E^F = -grad phi^F, [N,3] (forces q E).
+    graph=True captures the device stages as a CUDA graph on the first call and replays it on later
+    calls with the same parameters and buffers (pass `out`/`field_out` to keep the buffers fixed).
     reference_kernels=True selects the simple v1 gridding/gather kernels (A/B testing)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
-    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels)
+    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels, graph)
+    side = None
+    if graph and not host and stream is None:
+        import torch
+        side, cur = _graph_stream(x), torch.cuda.current_stream(x.device)
+        side.wait_stream(cur)
+        stream = side
     args = (ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), int(M), int(P),
             _neg(eta, 0.0), _neg(s0), _neg(sf), -1 if n_local is None else int(n_local), optr)
     if field:
         _check(lib.se1p_kspace_field_ex(*args, fptr))
-        return out, fo
-    _check(lib.se1p_kspace_ex(*args))
-    return out
+    else:
+        _check(lib.se1p_kspace_ex(*args))
+    if side is not None:
+        cur.wait_stream(side)
+    return (out, fo) if field else out
 
 
 def kspace3p(x, q, L, xi, M, P, eta=None, out=None, stream=None, sync=True, skip_checks=False, profile=False):

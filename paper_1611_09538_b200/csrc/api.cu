@@ -43,9 +43,12 @@ static DevState& dev_state() {
   return g_dev[d & 63];
 }
 
+static uint64_t g_ws_generation = 1;   // bumped on every workspace reallocation (graphs bake pointers)
+
 template <typename T>
 static void grow(T*& p, int64_t& cap, int64_t need) {
   if (need <= cap) return;
+  ++g_ws_generation;
   if (p) cudaFree(p);
   p = nullptr;
   cap = 0;
@@ -218,6 +221,53 @@ struct StageTimer {
   }
 };
 
+// CUDA graphs of the k-space call (opts->reserved[3] == 1): the stage sequence is captured once per
+// (plan, N, pointers, stream, workspace generation) and replayed -- one launch instead of ~30.
+struct GraphEntry {
+  KParams prm;
+  int64_t N;
+  const void *x, *q, *phi, *field;
+  cudaStream_t st;
+  uint64_t gen;
+  int launches;
+  cudaGraphExec_t exec;
+};
+static std::vector<GraphEntry> g_graphs;
+
+template <class F>
+static void run_graphed(const KParams& prm, int64_t N, const void* x, const void* q, const void* phi,
+                        const void* field, cudaStream_t st, F&& stages) {
+  for (auto& g : g_graphs)
+    if (g.prm == prm && g.N == N && g.x == x && g.q == q && g.phi == phi && g.field == field && g.st == st &&
+        g.gen == g_ws_generation) {
+      SE1P_CUDA_TRY(cudaGraphLaunch(g.exec, st));
+      g_launches = g.launches;
+      return;
+    }
+  if (st == 0) throw Error{1, "graph mode needs a non-default stream"};
+  cudaGraph_t graph = nullptr;
+  SE1P_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int l0 = g_launches;
+  try {
+    stages();
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    throw;
+  }
+  SE1P_CUDA_TRY(cudaStreamEndCapture(st, &graph));
+  cudaGraphExec_t exec = nullptr;
+  SE1P_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  if (g_graphs.size() >= 8) {
+    cudaGraphExecDestroy(g_graphs.front().exec);
+    g_graphs.erase(g_graphs.begin());
+  }
+  g_graphs.push_back(GraphEntry{prm, N, x, q, phi, field, st, g_ws_generation, g_launches - l0, exec});
+  SE1P_CUDA_TRY(cudaGraphLaunch(exec, st));
+}
+
 static void sync_and_check(cudaStream_t st) {
   SE1P_CUDA_TRY(cudaStreamSynchronize(st));
   SE1P_CUDA_TRY(cudaGetLastError());
@@ -262,7 +312,25 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
     grow(w.gpart, w.gpart_cap, N * gather_slots(dv) * (field ? 4 : 1));
     grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
   }
+  const bool graph = o && o->reserved[3] == 1;
+  if (graph && (host_io || v1 || stop || tm.on))
+    throw Error{1, "graph mode takes device pointers and no profiling / reference kernels / early stop"};
+  if (graph) {
+    run_graphed(prm, N, dx, dq, dphi, dfield, st, [&] {
+      k_bin_particles(*pl, w, dx, dq, N, st);
+      k_records_stage(*pl, w, N, st);
+      k_spread_tiles(*pl, w, N, st);
+      const SlabLayout Lg = single_layout(dv.Mt, pl->n_planes);
+      k_zfft_forward(*pl, w, w.planes, Lg, nullptr, st);
+      k_mode_stage(*pl, w, w.planes, Lg, nullptr, nullptr, 0, nullptr, nullptr, 0, st);
+      k_zfft_inverse(*pl, w, w.planes, Lg, nullptr, st);
+      if (field) k_records_stage(*pl, w, N, st, true);
+      k_gather_tiles(*pl, w, N, st, 0, -1, field);
+      k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
+    });
+  }
   // stages (se1p_last_stage_times): bin, records, spread, zfft, modes, izfft, gather, finish
+  if (!graph) {
   tm.mark();
   k_bin_particles(*pl, w, dx, dq, N, st);
   tm.mark();
@@ -290,6 +358,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   tm.mark();
   if (!v1) k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
   tm.mark();
+  }
   if (host_io && phi_out) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   if (host_io && field)
     SE1P_CUDA_TRY(cudaMemcpyAsync(field_out, dfield, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));

@@ -235,3 +235,28 @@ def test_ragged_tiles_all_configs_of_tz():
         ref = sd.se1p_kspace(x, q, L, xi, M, P, 3, 2 * (M + P), 2 * (M + P), SJ)
         got = _gpu_kspace(x, q, L, xi, M, P, 3, 2 * (M + P), 2 * (M + P), SJ)
         assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), (M, P)
+
+
+def test_graph_mode_replays_bitwise():
+    """CUDA-graph mode (captured on the first call, replayed after): same bits as the eager path,
+    including after the inputs change in place (the graph reads the same buffers)."""
+    c = CONFIGS["C2"]
+    kw = kspace_kwargs(c)
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = _dev(x, q)
+    out = torch.empty(c.N, dtype=torch.float64, device="cuda")
+    eager = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+    g1 = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, out=out, **kw).clone()
+    assert torch.equal(g1, eager)
+    x2, q2 = make_system(c.N, c.L, c.seed + 100)
+    xd.copy_(torch.from_numpy(x2))
+    qd.copy_(torch.from_numpy(q2))
+    g2 = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, out=out, **kw).clone()
+    assert se1p.launch_count() > 5      # the captured kernels (replayed as one graph)
+    assert torch.equal(g2, se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw))
+    fo = torch.empty(c.N, 3, dtype=torch.float64, device="cuda")
+    _, e1 = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, out=out, field=True, field_out=fo, **kw)
+    _, e2 = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, field=True, **kw)
+    assert torch.equal(e1, e2)
+    with pytest.raises(se1p.SE1PError):
+        se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, profile=True, **kw)

@@ -9,9 +9,11 @@ from se1p_synth import CONFIGS, kspace_kwargs, make_system  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C5"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+field = len(sys.argv) > 3 and sys.argv[3] == "field"
 x, q = make_system(cfg.N, cfg.L, cfg.seed)
 xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
 for _ in range(reps):
-    phi = se1p.kspace(xd, qd, cfg.L, cfg.xi, cfg.M, cfg.P, skip_checks=True, **kspace_kwargs(cfg))
+    phi = se1p.kspace(xd, qd, cfg.L, cfg.xi, cfg.M, cfg.P, skip_checks=True, field=field, **kspace_kwargs(cfg))
+    phi = phi[0] if field else phi
 torch.cuda.synchronize()
 print("ok", float(phi.abs().max()))
