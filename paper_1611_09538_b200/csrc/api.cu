@@ -456,7 +456,7 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   if (!x || !q || (!phi_out && !field_out) || !L) throw Error{1, "null pointer"};
   if (N < 1) throw Error{1, "N must be >= 1"};
   if (!(xi > 0) || !(rc > 0) || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "xi, rc, L must be > 0"};
-  const RDev d = real_geometry(L, xi, rc);
+  const RDev d = real_geometry(L, xi, rc, N);
   DevState& ds = dev_state();
   KWork& w = ds.w;
   ensure_particles(w, N, d.nc[0] * d.nc[1] * d.nc[2]);

@@ -4,6 +4,7 @@ tag=$1; shift
 for v in "$@"; do
   SE1P_NVCC_EXTRA="$v" timeout 300 python -c "from paper_1611_09538_b200 import build as b; b.build(force=True)" || continue
   echo "== [$v]"
+  if [ -n "$REAL_ONLY" ]; then timeout 300 python tools/real_times.py; continue; fi
   timeout 200 python tools/stage_times.py C5 tiles
   [ -z "$NO_FIELD" ] && timeout 200 python tools/stage_times.py C5 field
   timeout 200 python tools/stage_times.py C4 tiles

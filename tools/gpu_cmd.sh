@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_field.py -x -q -k "full_size and C5" -s 2>&1 | tail -4
+timeout 300 python tools/real_times.py
+timeout 900 python -m pytest tests -m gpu -x -q -k "real or full" 2>&1 | tail -2
