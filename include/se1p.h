@@ -177,6 +177,18 @@ int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, con
 int se1p_plan_query(const se1p_opts* opts, const double L[3], double xi, int M, int P,
                     double eta, double s0, double sf, int n_local, se1p_plan_info* info);
 
+/* Multi-tier adaptive upsampling (generalises the paper's three tiers
+   s0 / s_l / 1 of Eq. (upsamplings), and its Table 2 "plain upsampled FFT"):
+   mode |k3| = 2 pi n/L3, n = 1..n_local, uses the padded extent S_modes[n-1] (each >= M~; the
+   paper's s(n) M~), k3 = 0 uses S0 (opts->S0, or s0), |k3| > 2 pi n_local/L3 the J extent.
+   n_local must be given (>= 0); S_modes holds n_local ints (host).  Other arguments, ownership
+   and errors as se1p_kspace_ex.  On this device path every upsampled mode costs the same
+   exact-convolution transform whatever its extent, so the tiers set the
+   discretisation (and error), not the run time. */
+int se1p_kspace_tiers_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
+                         int64_t N, const double L[3], double xi, int M, int P, double eta,
+                         double s0, int n_local, const int* S_modes, double* phi_out);
+
 /* SE3P baseline (the paper's Ex. 5, compares SE1P with the
    triply periodic SE3P): the k-space part of the triply periodic Ewald sum with tin-foil boundary,
      phi^F(x_m) = (4 pi/V) sum_{k != 0} e^{-k^2/4 xi^2}/k^2 sum_n q_n cos(k.(x_m - x_n)),

@@ -90,11 +90,12 @@ def ghat(kappa2, k3, R):
 
 
 def mode_extent(nprime, n_l, S0, SI, SJ):
-    """Adaptive upsampling, Eq. (upsamplings), as padded extents (reading R-5)."""
+    """Adaptive upsampling, Eq. (upsamplings), as padded extents (reading R-5).
+    SI may be a sequence: the extent of |n| = 1..n_l (multi-tier)."""
     if nprime == 0:
         return S0
     if abs(nprime) <= n_l:
-        return SI
+        return SI[abs(nprime) - 1] if hasattr(SI, "__len__") else SI
     return SJ
 
 
@@ -110,7 +111,7 @@ def se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, eta=None, return_all=False, 
         raise ValueError("square free cross-section required (M1 == M2)")
     L3 = float(L[2])
     R = math.hypot(d["Lt1"], d["Lt2"])                                   # reading R-6
-    for S in (S0, SI, SJ):
+    for S in (S0, SJ, *(SI if hasattr(SI, "__len__") else (SI,))):
         if S < Mt1:
             raise ValueError("padded extents must be >= M~")
 

@@ -26,7 +26,7 @@ EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_p
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
            "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol",
-           "se1p_kspace3p_ex"]
+           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex"]
 
 
 class SE1PError(RuntimeError):
@@ -78,6 +78,7 @@ def load(build_if_needed: bool = True):
     lib.se1p_kspace_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_real.argtypes = [vp, vp, i64, vp, d, d, vp]
     lib.se1p_real_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp]
+    lib.se1p_kspace_tiers_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, i32, vp, vp]
     lib.se1p_kspace3p_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, vp]
     lib.se1p_plan_from_tol.argtypes = [vp, d, d, d, vp]
     lib.se1p_kspace_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
@@ -183,15 +184,25 @@ def _outputs(x, N, field, out, field_out):
 
 def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
            out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0,
-           reference_kernels=False, field=False, field_out=None, graph=False):
+           reference_kernels=False, field=False, field_out=None, graph=False, S_modes=None):
     """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1).
     field=True returns (phi^F, E^F) with E^F = -grad phi^F, [N,3] (forces q E).
     graph=True captures the device stages as a CUDA graph on the first call and replays it on later
     calls with the same parameters and buffers (pass `out`/`field_out` to keep the buffers fixed).
+    S_modes: multi-tier upsampling, padded extent of modes |k3| = 2 pi n/L3, n = 1..n_local
+    (needs n_local; potential only).
     reference_kernels=True selects the simple v1 gridding/gather kernels (A/B testing)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
+    if S_modes is not None:
+        if field or n_local is None or len(S_modes) != int(n_local):
+            raise ValueError("S_modes needs n_local = len(S_modes) and the potential (field=False)")
+        o = _opts(Ntilde, S0, None, host, skip_checks, sync, profile, stop_after, reference_kernels, graph)
+        tiers = (ctypes.c_int * len(S_modes))(*[int(s) for s in S_modes])
+        _check(lib.se1p_kspace_tiers_ex(ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
+                                        int(M), int(P), _neg(eta, 0.0), _neg(s0), int(n_local), tiers, optr))
+        return out
     o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels, graph)
     side = None
     if graph and not host and stream is None:

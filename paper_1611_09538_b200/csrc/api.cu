@@ -275,11 +275,17 @@ static void sync_and_check(cudaStream_t st) {
 
 static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
                         const double L[3], double xi, int M, int P, double eta, double s0, double sf, int n_local,
-                        double* phi_out, double* field_out = nullptr) {
+                        double* phi_out, double* field_out = nullptr, const int* S_modes = nullptr) {
   if (!x || !q || (!phi_out && !field_out)) throw Error{1, "null pointer"};
   if (N < 1) throw Error{1, "N must be >= 1"};
   if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
-  const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
+  if (S_modes) {   // multi-tier upsampling
+    const int Mt = (int)std::lround(L[0] / (L[2] / M)) + P;
+    prm.SIn.assign(S_modes, S_modes + prm.n_l);
+    for (int S : prm.SIn)
+      if (S < Mt) throw Error{4, "every per-mode extent must be >= M~ = M_free + P"};
+  }
   KPlan* pl = kplan_get(prm, st);
   DevState& ds = dev_state();
   KWork& w = ds.w;
@@ -684,6 +690,18 @@ int se1p_kspace3p_ex(const se1p_opts* opts, void* stream, const double* x, const
     se1p_opts o{};
     if (opts) o = *opts;
     kspace3p_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, phi_out);
+  });
+}
+
+int se1p_kspace_tiers_ex(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                         const double L[3], double xi, int M, int P, double eta, double s0, int n_local,
+                         const int* S_modes, double* phi_out) {
+  return guarded([&] {
+    if (!S_modes) throw Error{1, "null pointer"};
+    if (n_local < 0) throw Error{1, "the tiers entry needs an explicit n_local (the length of S_modes)"};
+    se1p_opts o{};
+    if (opts) o = *opts;
+    kspace_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, M, P, eta, s0, -1.0, n_local, phi_out, nullptr, S_modes);
   });
 }
 

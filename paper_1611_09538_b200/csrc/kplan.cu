@@ -116,7 +116,7 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
     SE1P_CUDA_TRY(cudaMalloc(&pl->d_khat, sizeof(double) * (size_t)pl->n_kernel * LK * LK));
     const double scale = pl->const_gather / ((double)p.M * (double)LK * (double)LK);
     for (int n = 0; n < pl->n_kernel; ++n) {
-      const int S = (n == 0) ? p.S0 : p.SI;
+      const int S = (n == 0) ? p.S0 : ((size_t)(n - 1) < p.SIn.size() ? p.SIn[n - 1] : p.SI);
       const int H = S / 2 + 1;
       const double k3 = 2.0 * kPi * n / L3;
       const double dk = 2.0 * kPi / (S * h);

@@ -46,9 +46,11 @@ struct KParams {       // everything a k-space plan is keyed on
   int n_l;             // resolved (>= 0)
   int S0, SI, SJ;      // resolved padded extents
   int periodic = 0;    // 1: SE3P transform plan (grid Mfree x Mfree x M, every plane a J plane, SJ = Mfree)
+  std::vector<int> SIn;   // multi-tier upsampling: extent of mode n = 1..n_l (empty: SI for all)
   bool operator==(const KParams& o) const {
     return L[0] == o.L[0] && L[1] == o.L[1] && L[2] == o.L[2] && xi == o.xi && M == o.M && P == o.P &&
-           eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ && periodic == o.periodic;
+           eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ && periodic == o.periodic &&
+           SIn == o.SIn;
   }
 };
 

@@ -260,3 +260,20 @@ def test_graph_mode_replays_bitwise():
     assert torch.equal(e1, e2)
     with pytest.raises(se1p.SE1PError):
         se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, profile=True, **kw)
+
+
+def test_multi_tier_matches_oracle():
+    """Per-mode extents (se1p_kspace_tiers_ex) element-wise against the Alg. 1 oracle's tiers."""
+    L, xi, M, P, n_l = (1.0, 1.0, 1.0), 6.0, 24, 16, 4
+    Mt = M + P
+    x, q = make_system(300, L, 42)
+    tiers = [170, 120, 97, 53]
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, tiers, 2 * Mt)
+    xd, qd = _dev(x, q)
+    got = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, Ntilde=2 * Mt, S_modes=tiers).cpu().numpy()
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+    flat = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, SI=97, Ntilde=2 * Mt).cpu().numpy()
+    same = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, Ntilde=2 * Mt, S_modes=[97] * n_l).cpu().numpy()
+    assert np.array_equal(flat, same)
+    with pytest.raises(se1p.SE1PError):
+        se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, Ntilde=2 * Mt, S_modes=[Mt - 1] * n_l)

@@ -130,3 +130,30 @@ def test_alg1_field_matches_exact_field():
         errs.append(np.sqrt(np.mean((E - ref) ** 2) / np.mean(ref ** 2)))
     assert all(b < a / 20 for a, b in zip(errs, errs[1:]))
     assert errs[-1] < 1e-9
+
+
+def test_multi_tier_upsampling():
+    """Multi-tier s(n) (generalising Eq. (upsamplings)): each mode
+    |n| <= n_l padded only as far as its own image distance needs (the estimate of reading R-18 at
+    k3 = 2 pi n/L3) meets the accuracy of padding every mode to the largest extent; equal tiers
+    reproduce the single-s_l path exactly."""
+    L = (1.0, 1.0, 1.0)
+    x, q = make_system(150, L, 41)
+    xi, M, P, n_l = 6.0, 24, 16, 4
+    Mt = M + P
+    h = L[2] / M
+    ref = _kspace_exact(x, q, L, xi)
+    SJ = 2 * Mt
+    same = sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, [3 * Mt] * n_l, SJ)
+    assert np.array_equal(same, sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, 3 * Mt, SJ))
+    budget = math.log(math.sqrt(np.sum(q * q)) / 1e-12)
+    tiers = [max(Mt, int(math.ceil((L[0] + budget * L[2] / (2 * math.pi * n)) / h))) for n in range(1, n_l + 1)]
+    assert tiers == sorted(tiers, reverse=True) and tiers[0] > tiers[-1]
+    tiered = sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, tiers, SJ)
+    full = sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, tiers[0], SJ)
+    e_t = math.sqrt(np.mean((tiered - ref) ** 2))
+    e_f = math.sqrt(np.mean((full - ref) ** 2))
+    assert e_t <= 2 * e_f + 1e-13 and e_t < 1e-9, (e_t, e_f)
+    # too little padding on the slowest mode is visible
+    starved = sd.se1p_kspace(x, q, L, xi, M, P, n_l, 4 * Mt, [Mt] + tiers[1:], SJ)
+    assert math.sqrt(np.mean((starved - ref) ** 2)) > 10 * e_t
