@@ -132,12 +132,12 @@ def bench_ours(args, cfg, rank, world, local):
     kw = kspace_kwargs(cfg)
     info = se1p.plan_info(cfg.L, cfg.xi, cfg.M, cfg.P, **kw)
 
-    def step(xs=x, qs=q):
+    def step(xs=x, qs=q, out=phi):
         if world > 1:
             return sdist.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, stream=stream, **kw)
-        se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, sync=False, skip_checks=True,
+        se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=out, stream=stream, sync=False, skip_checks=True,
                     graph=True, **kw)
-        return phi
+        return out
 
     se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, **kw)   # plan + workspace, validated inputs
     for _ in range(args.warmup):
@@ -173,30 +173,51 @@ def bench_ours(args, cfg, rank, world, local):
     clocks = clk.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # end-to-end through the public API: pinned host x, q -> device, the step, phi -> host
+    # end-to-end through the public API: every step copies its x, q from pinned host memory to the
+    # device, runs the step and reads phi back to pinned host memory.  Single GPU: two buffer
+    # slots and copy streams, so step i+1's H2D and step i-1's D2H run on the copy engines while
+    # step i computes (a streaming user's pipeline); multi-GPU: one slot, serial.
     xh = torch.from_numpy(x_np).pin_memory()
     qh = torch.from_numpy(q_np).pin_memory()
-    ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
-    xd = torch.empty_like(x)          # device input buffers the user reuses every step
-    qd = torch.empty_like(q)
     ke = max(3, args.steps // 2)
+    nslot = 2 if world == 1 else 1
+    slots = [dict(x=torch.empty_like(x), q=torch.empty_like(q), phi=torch.empty_like(phi),
+                  ph=torch.empty(cfg.N, dtype=torch.float64).pin_memory(),
+                  loaded=torch.cuda.Event(), computed=torch.cuda.Event(), read=torch.cuda.Event())
+             for _ in range(nslot)]
+    h2d = torch.cuda.Stream(device=dev) if world == 1 else stream
+    d2h = torch.cuda.Stream(device=dev) if world == 1 else stream
 
-    def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        qd.copy_(qh, non_blocking=True)
-        ph.copy_(step(xd, qd), non_blocking=True)
+    def e2e_run(n):
+        for i in range(n):
+            s = slots[i % nslot]
+            h2d.wait_event(s["computed"])        # the slot's previous step has consumed its inputs
+            with torch.cuda.stream(h2d):
+                s["x"].copy_(xh, non_blocking=True)
+                s["q"].copy_(qh, non_blocking=True)
+            s["loaded"].record(h2d)
+            stream.wait_event(s["loaded"])
+            stream.wait_event(s["read"])          # the slot's previous phi has reached the host
+            out = step(s["x"], s["q"], s["phi"])
+            s["computed"].record(stream)
+            d2h.wait_event(s["computed"])
+            with torch.cuda.stream(d2h):
+                s["ph"].copy_(out, non_blocking=True)
+            s["read"].record(d2h)
+        stream.wait_stream(d2h)
 
-    e2e_step()
+    e2e_run(nslot)                                # capture each slot's graph
     torch.cuda.synchronize(dev)
     barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(ke):
-        e2e_step()
+    e2e_run(ke)
     f1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_s = max_over_ranks(f0.elapsed_time(f1) / ke) * 1e-3
+    if world == 1:
+        assert np.array_equal(slots[0]["ph"].numpy(), phi.cpu().numpy()), "e2e result differs from the device step"
 
     if world > 1:
         import torch.distributed as dist
