@@ -28,18 +28,56 @@ import math
 TILE = 16   # x extent of the gridding/gather tiles: slab bounds are multiples of it
 
 
-def slab_bounds(Mt: int, R: int) -> list:
-    """R+1 x-row bounds 0 = b_0 <= ... <= b_R = Mt, multiples of TILE (b_R = Mt), the
-    ceil(Mt/TILE) tiles split as evenly as possible (lower ranks take the extra ones)."""
+def tile_weights(Mt: int, P: int) -> list:
+    """Gridding/gather work of each 16-row x tile of the extended grid: the number of
+    (particle column, stencil row) incidences, particles uniform over the M_free = Mt - P columns
+    with stencil rows j0 .. j0+P-1, j0 = 1 .. M_free (reading R-3).  Boundary tiles are light."""
+    Mf = Mt - P
+    nt = (Mt + TILE - 1) // TILE
+    w = []
+    for t in range(nt):
+        s = 0
+        for r in range(t * TILE, min(Mt, (t + 1) * TILE)):
+            s += max(0, min(Mf, r) - max(1, r - P + 1) + 1)
+        w.append(float(s))
+    return w
+
+
+def slab_bounds(Mt: int, R: int, P=None) -> list:
+    """R+1 x-row bounds 0 = b_0 <= ... <= b_R = Mt, multiples of TILE (b_R = Mt).  Without P the
+    ceil(Mt/TILE) tiles are split as evenly as possible (lower ranks take the extra ones); with P
+    the contiguous split minimises the largest slab's tile work (tile_weights; ties: the earliest
+    bounds), since the boundary tiles carry little work."""
     if R < 1:
         raise ValueError("R >= 1")
     nt = (Mt + TILE - 1) // TILE
-    bounds = [0]
-    for r in range(R):
-        cnt = nt // R + (1 if r < nt % R else 0)
-        bounds.append(min(Mt, bounds[-1] + TILE * cnt))
-    bounds[-1] = Mt
-    return bounds
+    if P is None:
+        bounds = [0]
+        for r in range(R):
+            cnt = nt // R + (1 if r < nt % R else 0)
+            bounds.append(min(Mt, bounds[-1] + TILE * cnt))
+        bounds[-1] = Mt
+        return bounds
+    w = tile_weights(Mt, P)
+    pre = [0.0]
+    for v in w:
+        pre.append(pre[-1] + v)
+    INF = float("inf")
+    # best[k][t]: minimal max load splitting tiles [0, t) into k slabs; cut[k][t]: last cut
+    best = [[INF] * (nt + 1) for _ in range(R + 1)]
+    cut = [[0] * (nt + 1) for _ in range(R + 1)]
+    best[0][0] = 0.0
+    for k in range(1, R + 1):
+        for t in range(nt + 1):
+            for s in range(t + 1):
+                v = max(best[k - 1][s], pre[t] - pre[s])
+                if v < best[k][t] - 1e-9 * max(1.0, v):
+                    best[k][t], cut[k][t] = v, s
+    ends = [nt]
+    for k in range(R, 0, -1):
+        ends.append(cut[k][ends[-1]])
+    tiles = ends[::-1]                       # R+1 tile indices, 0 .. nt
+    return [min(Mt, TILE * t) for t in tiles[:-1]] + [Mt]
 
 
 def plane_costs(info: dict) -> list:
@@ -93,7 +131,7 @@ def make_plan(info: dict, R: int) -> DistPlan:
     Mt, n_planes = info["Mt"], info["n_planes"]
     owned = assign_planes(plane_costs(info), R)
     order = [n for r in range(R) for n in owned[r]]
-    return DistPlan(Mt, n_planes, R, slab_bounds(Mt, R), owned, order)
+    return DistPlan(Mt, n_planes, R, slab_bounds(Mt, R, info.get("P")), owned, order)
 
 
 class CudaBackend:

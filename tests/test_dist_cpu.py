@@ -115,7 +115,8 @@ def _stages(x):
 
 
 def _info(s):
-    return {"Mt": s.Mt, "n_planes": s.n_planes, "n_kernel_planes": s.n_l + 1, "LK": 2 * s.Mt, "Ntilde": s.SJ}
+    return {"Mt": s.Mt, "n_planes": s.n_planes, "n_kernel_planes": s.n_l + 1, "LK": 2 * s.Mt, "Ntilde": s.SJ,
+            "P": s.P}
 
 
 def _reference():
@@ -131,6 +132,16 @@ def test_slab_bounds_and_lpt():
     b = sdist.slab_bounds(40, 4)                   # 3 tiles over 4 ranks: one empty slab
     assert b[0] == 0 and b[-1] == 40 and all(v % 16 == 0 or v == 40 for v in b)
     assert all(b2 >= b1 for b1, b2 in zip(b, b[1:]))
+    # tile-work-weighted split (boundary tiles are light): C5's 18 tiles over 8 ranks
+    w = sdist.tile_weights(280, 24)
+    assert len(w) == 18 and w[2] == 16 * 24 and w[0] < w[2] and w[17] < w[16] < w[2]
+    assert sum(w) == 256 * 24                      # every (particle column, stencil row) once
+    b = sdist.slab_bounds(280, 8, 24)
+    loads = [sum(w[b[i] // 16:(b[i + 1] + 15) // 16]) for i in range(8)]
+    assert b[0] == 0 and b[-1] == 280 and all(v % 16 == 0 for v in b[:-1])
+    assert max(loads) <= 2.25 * 16 * 24 < max(sum(w[c // 16:(d + 15) // 16]) for c, d in
+                                               zip(sdist.slab_bounds(280, 8), sdist.slab_bounds(280, 8)[1:]))
+    assert sdist.slab_bounds(152, 1, 24) == [0, 152]
     costs = [10.0, 9.0, 1.0, 1.0, 1.0, 1.0, 1.0]
     owned = sdist.assign_planes(costs, 2)
     assert sorted(sum(owned, [])) == list(range(7))

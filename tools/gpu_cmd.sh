@@ -1,1 +1,1 @@
-timeout 600 python bench.py --steps 20 --warmup 3 --cpu-seconds 5 > gpurun_out/bg.log 2>&1; tail -3 gpurun_out/bg.log | cut -c1-300; tail -1 gpurun_out/bg.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e'], d['gpu_launches'], d['roofline']['frac'])"
+timeout 900 python -m pytest tests/test_gpu_dist.py -x -q 2>&1 | tail -3
