@@ -184,6 +184,10 @@ EDGE = [
     ("odd-P9-M18", 70, (1, 1, 1), 4.0, 18, 9, 3, 70, 56, 28, 22),
     ("P32-M48", 120, (1, 1, 1), 6.0, 48, 32, 4, 200, 160, 80, 23),
     ("P40-M64", 60, (1, 1, 1), 7.0, 64, 40, 3, 260, 208, 104, 24),
+    ("P64-max", 40, (1, 1, 1), 9.0, 64, 64, 2, 260, 260, 128, 25),
+    ("M4-P2", 30, (1, 1, 1), 1.5, 4, 2, 1, 12, 12, 6, 26),
+    ("P-equals-M", 50, (1, 1, 1), 3.0, 8, 8, 2, 40, 32, 16, 27),
+    ("flat-box-L3-0.5", 80, (1, 1, 0.5), 8.0, 16, 10, 2, 200, 160, 52, 28),
 ]
 
 
