@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "odd_and_large" 2>&1 | tail -8
+for m in tiles field; do timeout 300 python tools/stage_times.py C5 $m; done
+timeout 300 python tools/stage_times.py C4 tiles
