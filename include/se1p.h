@@ -116,8 +116,10 @@ int se1p_kspace_ex(const se1p_opts* opts, void* stream, const double* x, const d
  *                 returns every rank its slab buffer.
  *
  * se1p_kspace_slab_forward: Alg. 1 steps 2-3a (AFT step 1 P:749) restricted to the slab:
- *   bins and sorts all N particles, grids the slab's x rows (output-stationary tiles, so no
- *   reduction between ranks) and transforms them along z.  planes_out: slab buffer (caller owned).
+ *   compacts the particles whose stencils meet the slab's tiles, bins and sorts those, grids the
+ *   slab's x rows (output-stationary tiles, so no reduction between ranks) and transforms them
+ *   along z.  planes_out: slab buffer (caller owned).  Synchronises the stream once (the
+ *   compacted count sizes the sort).
  * se1p_kspace_modes: Alg. 2 steps 2-4, the scaling of Alg. 1 step 4 and Alg. 3 steps 1-3
  *    for the n_own planes plane_ids[] (global k3 indices 0..M/2) held in the
  *   split buffer `planes` described by nslab, slab_lo[0..nslab] (slab_lo[0] = 0, slab_lo[nslab] = M~).

@@ -30,6 +30,13 @@ struct DevState {
   int64_t fwd_N = -1;
   int* dmap = nullptr;          // device copies of plane maps (distributed path)
   int64_t dmap_cap = 0;
+  int64_t fwd_nrel = -1;        // particles of the slab (compacted set) of the last forward
+  int* sel = nullptr;           // [2N+1+scan scratch] flags, positions
+  int64_t sel_cap = 0;
+  int* idmap = nullptr;         // compacted index -> user index
+  int64_t idmap_cap = 0;
+  double* xsel = nullptr;       // compacted x (3n), q (n), phi partial (n)
+  int64_t xsel_cap = 0;
   double* dx = nullptr;   // host_io staging (device side)
   double* dq = nullptr;
   double* dphi = nullptr;
@@ -543,9 +550,29 @@ static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double*
   grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
   if (!(o && o->skip_checks)) check_inputs(w, x, q, N, L, true, st);
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
-  k_bin_particles(*pl, w, x, q, N, st);
-  k_records_stage(*pl, w, N, st);
-  k_spread_tiles(*pl, w, N, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
+  // only the particles whose stencils meet the slab's tiles are binned and gridded (the rest
+  // cannot touch them): rows [16 ceil(x_lo/16), 16 ceil(x_hi/16))
+  const int tlo = (int)ceil_div(x_lo, 16), thi = (int)ceil_div(x_hi, 16);
+  grow(ds.sel, ds.sel_cap, 2 * N + 2 + scan_scratch_ints(N));
+  grow(ds.idmap, ds.idmap_cap, N);
+  grow(ds.xsel, ds.xsel_cap, 5 * N);
+  int* flags = ds.sel;
+  int* pos = ds.sel + N;
+  double* xc = ds.xsel;
+  double* qc = ds.xsel + 3 * N;
+  k_slab_select(*pl, x, q, N, 16 * tlo, 16 * thi, flags, pos, pos + N + 1, xc, qc, ds.idmap, st);
+  int nrel = 0;
+  SE1P_CUDA_TRY(cudaMemcpyAsync(&nrel, pos + N, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+  if (nrel > 0) {
+    k_bin_particles(*pl, w, xc, qc, nrel, st);
+    k_records_stage(*pl, w, nrel, st);
+    k_spread_tiles(*pl, w, nrel, st, tlo, thi);
+  } else if (thi > tlo) {   // no particle meets the slab: its rows are zero
+    const int64_t r0 = 16 * (int64_t)tlo, r1 = std::min<int64_t>(16 * (int64_t)thi, dv.Mt);
+    SE1P_CUDA_TRY(cudaMemsetAsync(w.grid + r0 * dv.Mt * dv.M, 0, sizeof(double) * (r1 - r0) * dv.Mt * dv.M, st));
+  }
+  ds.fwd_nrel = nrel;
   SlabLayout Ls{};
   Ls.nslab = 1;
   Ls.nloc = pl->n_planes;
@@ -621,8 +648,17 @@ static void slab_backward_impl(const se1p_opts* o, cudaStream_t st, int64_t N, c
   Ls.xlo[0] = x_lo;
   Ls.xlo[1] = x_hi;
   k_zfft_inverse(*pl, w, (const double2*)planes_in, Ls, upload_ints(ds, slot, st), st);
-  k_gather_tiles(*pl, w, N, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
-  k_gather_finish_stage(*pl, w, N, phi_partial, st, (int)ceil_div(x_lo, 16), (int)ceil_div(x_hi, 16));
+  // the slab's particles (compacted by the forward): partials into their slots, then scattered
+  // to user order; every other particle's partial is zero
+  const int64_t nrel = ds.fwd_nrel;
+  const int tlo = (int)ceil_div(x_lo, 16), thi = (int)ceil_div(x_hi, 16);
+  SE1P_CUDA_TRY(cudaMemsetAsync(phi_partial, 0, sizeof(double) * N, st));
+  if (nrel > 0) {
+    double* phic = ds.xsel + 4 * N;
+    k_gather_tiles(*pl, w, nrel, st, tlo, thi);
+    k_gather_finish_stage(*pl, w, nrel, phic, st, tlo, thi);
+    k_scatter_partial_stage(phic, ds.idmap, nrel, phi_partial, st);
+  }
   finish_call(o, w, st);
 }
 

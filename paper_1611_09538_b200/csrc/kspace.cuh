@@ -123,6 +123,10 @@ double lambert_w0(double x);
 
 // Stages (launch on st).
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st);
+// distributed path (particles.cu): compact the particles meeting slab rows [row_lo, row_hi)
+void k_slab_select(const KPlan& pl, const double* x, const double* q, int64_t N, int row_lo, int row_hi, int* flags,
+                   int* pos, int* scan_scratch, double* xc, double* qc, int* idmap, cudaStream_t st);
+void k_scatter_partial_stage(const double* phic, const int* idmap, int64_t n, double* phi, cudaStream_t st);
 void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
 void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field = false);   // tiles.cu
 // DMMA tile kernels over x tiles [tx_lo, tx_hi) (tx_hi < 0: all), tiles of 16 grid rows

@@ -51,6 +51,53 @@ __global__ void k_permute(KDev dv, const double* __restrict__ x, const double* _
   s4[s] = make_int4(jx0, jy0, lz0, a);
 }
 
+// Distributed path: the particles whose x stencil rows [jx0, jx0 + P) meet the slab rows
+// [row_lo, row_hi) (reading R-3: jx0 = floor(x/h) + 1), compacted in their original order.
+__global__ void k_slab_flags(KDev dv, const double* __restrict__ x, int64_t N, int row_lo, int row_hi,
+                             int* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int cx = (int)floor(x[3 * i] * dv.inv_h);
+  cx = min(max(cx, 0), dv.Mfree - 1);
+  const int j0 = cx + 1;
+  flags[i] = (j0 + dv.P > row_lo && j0 < row_hi) ? 1 : 0;
+}
+
+__global__ void k_slab_compact(const double* __restrict__ x, const double* __restrict__ q, int64_t N,
+                               const int* __restrict__ flags, const int* __restrict__ pos, double* __restrict__ xc,
+                               double* __restrict__ qc, int* __restrict__ idmap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || !flags[i]) return;
+  const int p = pos[i];
+  xc[3 * (int64_t)p] = x[3 * i];
+  xc[3 * (int64_t)p + 1] = x[3 * i + 1];
+  xc[3 * (int64_t)p + 2] = x[3 * i + 2];
+  qc[p] = q[i];
+  idmap[p] = (int)i;
+}
+
+__global__ void k_scatter_partial(const double* __restrict__ phic, const int* __restrict__ idmap, int64_t n,
+                                  double* __restrict__ phi) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) phi[idmap[p]] = phic[p];
+}
+
+void k_slab_select(const KPlan& pl, const double* x, const double* q, int64_t N, int row_lo, int row_hi, int* flags,
+                   int* pos, int* scan_scratch, double* xc, double* qc, int* idmap, cudaStream_t st) {
+  const unsigned nb = (unsigned)ceil_div(N, 256);
+  k_slab_flags<<<nb, 256, 0, st>>>(pl.dv, x, N, row_lo, row_hi, flags);
+  SE1P_LAUNCH_CHECK();
+  exclusive_scan_ints(flags, N, pos, scan_scratch, st);
+  k_slab_compact<<<nb, 256, 0, st>>>(x, q, N, flags, pos, xc, qc, idmap);
+  SE1P_LAUNCH_CHECK();
+}
+
+void k_scatter_partial_stage(const double* phic, const int* idmap, int64_t n, double* phi, cudaStream_t st) {
+  if (n <= 0) return;
+  k_scatter_partial<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(phic, idmap, n, phi);
+  SE1P_LAUNCH_CHECK();
+}
+
 void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q, int64_t N, cudaStream_t st) {
   const KDev& dv = pl.dv;
   const int nbins = dv.nbx * dv.M * dv.Mfree;

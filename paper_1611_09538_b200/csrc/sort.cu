@@ -165,6 +165,11 @@ __global__ void __launch_bounds__(kSortThreads) k_rs_down(const int* __restrict_
   }
 }
 
+void exclusive_scan_ints(const int* in, int64_t n, int* out, int* scratch, cudaStream_t st) {
+  excl_scan(in, n, out, scratch, st);
+}
+int64_t scan_scratch_ints(int64_t n) { return ceil_div(n + 1, kScanTile) + 16; }
+
 int64_t sort_scratch_ints(int64_t N, int nbins) {
   const int64_t nblk = ceil_div(N, kSortTile);
   const int64_t gh = 256 * nblk + 1;

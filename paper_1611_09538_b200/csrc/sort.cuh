@@ -10,5 +10,8 @@ namespace se1p {
 void stable_bin_sort(const int* keys, int64_t N, int nbins, int* perm, int* bin_start, int* scratch,
                      cudaStream_t st);
 int64_t sort_scratch_ints(int64_t N, int nbins);
+// out[0..n]: exclusive prefix sums of in[0..n) and the total at out[n]; scratch: scan_scratch_ints(n)
+void exclusive_scan_ints(const int* in, int64_t n, int* out, int* scratch, cudaStream_t st);
+int64_t scan_scratch_ints(int64_t n);
 
 }  // namespace se1p

@@ -192,8 +192,10 @@ def kspace_emulated(x, q, plan: DistPlan, backend):
     phi = None
     for r in range(R):
         buf = torch.cat([back[owner][r] for owner in range(R)])                       # all-to-all #2
-        # the device workspace holds the sorted particle state of the last forward, which is the same
-        # for every rank (same particles and parameters)
+        # the device workspace holds the particle state of the LAST forward, and each rank's
+        # forward keeps only its slab's particles: redo rank r's forward (its planes are discarded)
+        if R > 1:
+            backend.forward(x, q, plan.bounds[r], plan.bounds[r + 1], plan.order)
         part = backend.backward(buf.reshape(plan.n_planes, plan.width(r), plan.Mt, 2), N, plan.bounds[r],
                                 plan.bounds[r + 1], plan.order)
         phi = part.clone() if phi is None else phi + part

@@ -1,2 +1,1 @@
-for m in tiles field; do timeout 300 python tools/stage_times.py C5 $m; done
-timeout 300 python tools/stage_times.py C4 tiles
+timeout 900 python -m pytest tests/test_gpu_dist.py -x -q 2>&1 | grep -E "Error|assert|error" | head -20
