@@ -259,6 +259,8 @@ auto reduce = [&](int b, int rt) {
       if (sz >= 0) {
         const int sx = tx - fdiv(s.x, kTXY), sy = ty - fdiv(s.y, kTXY);
         const int64_t i = __double_as_longlong(rb[p * kRec + 3]);   // sorted index (k_records)
+        if (sx < 0 || sx >= dv.nsxy || sy < 0 || sy >= dv.nsxy || sz >= dv.nsz || i < 0 || i >= dv.N)
+          atomicOr(dv.err, 4);                                          // bounds check: slot map
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
           double sum = 0.0;
@@ -327,6 +329,7 @@ auto reduce = [&](int b, int rt) {
     int pos = 0;   // stream position of the next record (= k BM + fill)
     for (int q0 = 0; q0 < npc; q0 += 32) {
       const int sC = sN, nC = eN - sN;
+      if (nC < 0 || sC < 0 || (int64_t)sC + nC > dv.N) atomicOr(dv.err, 1);   // bounds check: run outside [0, N)
       load_run(q0 + 32 + lane, sN, eN);   // prefetch the next 32 runs
       int incl = nC;
 #pragma unroll
@@ -557,6 +560,7 @@ auto reduce = [&](int b, int rt) {
         if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
         n += __popc(bal);
       }
+      if (lane == 0 && n > BM + 16) atomicOr(dv.err, 2);   // bounds check: list capacity BM + 32
       __syncwarp();
       int kend = n & ~15;
       if (kend < held) {   // fewer than 16 entries and some carried: flush everything (padded)
@@ -596,6 +600,7 @@ auto reduce = [&](int b, int rt) {
       if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
       n += __popc(bal);
     }
+    if (lane == 0 && n > BM) atomicOr(dv.err, 2);   // bounds check: list capacity BM + 32
     const int npad = (n + 15) & ~15;
     if (lane < npad - n) wl[n + lane] = dummy;
     __syncwarp();
