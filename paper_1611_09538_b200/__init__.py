@@ -248,14 +248,33 @@ def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False, f
     return out
 
 
-def potential(x, q, L, xi, rc, M, P, **kw):
-    """Full singly periodic potential phi = phi^F + phi^R + phi^self (Eq. (2))."""
+def _tol_params(q, L, xi, tol):
+    """(rc, M, P, kspace kwargs) from plan_from_tol for this system's Q = sum q^2."""
+    Q = float((q * q).sum())
+    plan = plan_from_tol(L, Q, xi, tol)
+    M, P, kw = kspace_args(plan)
+    return plan["rc"], M, P, kw
+
+
+def potential(x, q, L, xi, rc=None, M=None, P=None, tol=None, **kw):
+    """Full singly periodic potential phi = phi^F + phi^R + phi^self (Eq. (2)).
+    Either rc, M, P (and kspace keywords) or tol: the parameters from plan_from_tol (NEXT-2)."""
+    if tol is not None:
+        rc, M, P, kw2 = _tol_params(q, L, xi, tol)
+        kw = {**kw2, **kw}
+    if rc is None or M is None or P is None:
+        raise ValueError("give rc, M, P or tol")
     return kspace(x, q, L, xi, M, P, **kw) + real(x, q, L, xi, rc)
 
 
-def energy_forces(x, q, L, xi, rc, M, P, **kw):
+def energy_forces(x, q, L, xi, rc=None, M=None, P=None, tol=None, **kw):
     """(U, phi, F): the electrostatic energy U = 1/2 sum_n q_n phi_n, the potentials and the forces
-    F_n = q_n E_n, E = E^F + E^R (Eq. (2) and its gradient)."""
+    F_n = q_n E_n, E = E^F + E^R (Eq. (2) and its gradient).  rc, M, P or tol as in potential()."""
+    if tol is not None:
+        rc, M, P, kw2 = _tol_params(q, L, xi, tol)
+        kw = {**kw2, **kw}
+    if rc is None or M is None or P is None:
+        raise ValueError("give rc, M, P or tol")
     pk, ek = kspace(x, q, L, xi, M, P, field=True, **kw)
     pr, er = real(x, q, L, xi, rc, field=True)
     phi, E = pk + pr, ek + er

@@ -30,3 +30,19 @@ def test_planned_gpu_potential_meets_tol(L, N, xi, tol):
     err = math.sqrt(np.mean((phi[t] - ref) ** 2))
     print(f"planned M={M} P={P} rc={p['rc']:.3f}: abs rms {err:.2e} (tol {tol:.0e})")
     assert err <= tol
+
+
+def test_potential_and_forces_from_tol():
+    """potential(..., tol=) and energy_forces(..., tol=) pick the planner's parameters."""
+    L, xi, tol = (1.0, 1.0, 1.0), 8.0, 1e-8
+    x, q = make_system(3000, L, 18)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    phi = se1p.potential(xd, qd, L, xi, tol=tol).cpu().numpy()
+    t = sample_targets(3000, 128, 18)
+    ref = oracle.phi_exact(x, q, L, t)
+    assert math.sqrt(np.mean((phi[t] - ref) ** 2)) <= tol
+    U, phi2, F = se1p.energy_forces(xd, qd, L, xi, tol=tol)
+    assert torch.max(torch.abs(phi2.cpu() - torch.from_numpy(phi))) <= 1e-12 * np.max(np.abs(phi))
+    Eref = oracle.field_exact(x, q, L, t)
+    err = math.sqrt(np.mean(((F.cpu().numpy()[t] / q[t, None]) - Eref) ** 2))
+    assert err <= 100 * tol      # the field's error constant is larger (P:602)
