@@ -290,7 +290,7 @@ def kernel_traffic(which):
         return None
 
 
-def bench_reference(args, cfg, rank):
+def bench_reference(args, cfg, rank, world=1):
     if rank != 0:
         return None
     cores = len(os.sched_getaffinity(0))
@@ -310,10 +310,12 @@ def bench_reference(args, cfg, rank):
     value = m / dt
     sample = f"{m} seeded targets per step of {cfg.name} (exact Ewald1P, all {cfg.N} sources)"
     return {"impl": "reference", "metric": "SE1P k-space particles/sec (fp64)", "value": value,
-            "unit": "particles/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "unit": "particles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded uniform neutral charges, se1p_synth.py)",
-            "config": {"workload": cfg.name, "N": cfg.N},
+            "config": {"workload": f"{cfg.name}: N={cfg.N} L={list(cfg.L)} xi={cfg.xi} M={cfg.M} P={cfg.P} "
+                                   f"(the exact Ewald1P potential of the same system, on {cores} host cores)",
+                       "N": cfg.N, "parallelism": "CPU oracle (rank 0 only)"},
             "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -323,7 +325,7 @@ def main():
     rank, world, local = dist_env()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
-        line = bench_reference(args, cfg, rank)
+        line = bench_reference(args, cfg, rank, world)
         if line is not None:
             print(json.dumps(line), flush=True)
         return
