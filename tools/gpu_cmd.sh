@@ -1,1 +1,3 @@
-python tools/profile_one.py C5 1 > /dev/null && ncu --clock-control none --set full -k regex:"k_colpass|k_rowfwd" -c 4 -o gpurun_out/fftprof python tools/profile_one.py C5 1 > gpurun_out/fftprof.log 2>&1; tail -2 gpurun_out/fftprof.log
+for m in tiles field; do timeout 300 python tools/stage_times.py C5 $m; done
+timeout 300 python tools/stage_times.py C4 tiles
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
