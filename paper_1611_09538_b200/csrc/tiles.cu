@@ -261,16 +261,26 @@ auto reduce = [&](int b, int rt) {
         const int64_t i = __double_as_longlong(rb[p * kRec + 3]);   // sorted index (k_records)
         if (sx < 0 || sx >= dv.nsxy || sy < 0 || sy >= dv.nsxy || sz >= dv.nsz || i < 0 || i >= dv.N)
           atomicOr(dv.err, 4);                                          // bounds check: slot map
+        double sum[NC];
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
-          double sum = 0.0;
+          sum[cc] = 0.0;
 #pragma unroll
           for (int v = 0; v < kCW; ++v) {
-            sum += ap[v * NC + cc];
+            sum[cc] += ap[v * NC + cc];
             ap[v * NC + cc] = 0.0;
           }
-          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NCT + COFF + cc] = sum;
         }
+        if (FM == 1) {   // column moments -> d/dx, d/dy: 2 alpha (h S + delta phi)
+          const double ta = 2.0 * dv.alpha;
+          const double dxp = ((double)X0 - 0.5 * P) * dv.h - rb[p * kRec + 10];
+          const double dyp = ((double)Y0 - 0.5 * P) * dv.h - rb[p * kRec + 11];
+          sum[1] = ta * fma(dv.h, sum[1], dxp * sum[0]);
+          sum[2] = ta * fma(dv.h, sum[2], dyp * sum[0]);
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NCT + COFF + cc] = sum[cc];
       } else if (hx) {
         for (int v = 0; v < kCW * NC; ++v)
           if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
@@ -684,8 +694,18 @@ auto reduce = [&](int b, int rt) {
           const double* tt0 = t0 + 2 * h;
           const double* tt1 = t1 + 2 * h;
           const double wx0 = r[kEX + cx0], wx1 = r[kEX + cx0 + 1], wy0 = r[kEY + cy0], wy2 = r[kEY + cy0 + 2];
-          v[h][0] = wy0 * fma(wx0, tt0[0], wx1 * tt0[1]) + wy2 * fma(wx0, tt1[0], wx1 * tt1[1]);
-          if (FM == 1 || FM == 3) {
+          const double A0 = fma(wx0, tt0[0], wx1 * tt0[1]), A1 = fma(wx0, tt1[0], wx1 * tt1[1]);
+          v[h][0] = fma(wy0, A0, wy2 * A1);
+          if (FM == 1) {
+            // x, y derivatives: with node - x_p = (tile column) h + delta_x, delta_x = (X0 - P/2) h - x_p
+            // per particle and tile, sum (node - x_p) wx wy T = h S_x + delta_x phi; the column moments
+            // S_x = sum cx wx wy T, S_y likewise go through the reduction, delta in the slot reduce
+            const double cxa = (double)cx0, cya = (double)cy0;
+            v[h][1] = fma(wy0, fma(cxa * wx0, tt0[0], (cxa + 1.0) * wx1 * tt0[1]),
+                          wy2 * fma(cxa * wx0, tt1[0], (cxa + 1.0) * wx1 * tt1[1]));
+            v[h][2] = fma(cya * wy0, A0, (cya + 2.0) * wy2 * A1);
+          }
+          if (FM == 3) {
             const int ph = (h ? e1 : e0) & 0xff;
             const double* rr = rb + (ph < BM ? ph : 0) * kRec;
             const double px = rr[10], py = rr[11];
