@@ -1,4 +1,5 @@
-# round-1 evidence refresh (tag r01d): bench line, reference arm, launch list, full tile capture
+# Evidence refresh for profiles/ (bench line, reference arm, launch list, full tile capture);
+# then: python tools/summarize_profiles.py gpurun_out/r1u_launches.csv gpurun_out/r1u_tiles.ncu-rep <tag>
 set -x
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
 timeout 600 python bench.py --steps 20 --warmup 3 --cpu-seconds 10 > gpurun_out/r1u_bench.log 2>&1
