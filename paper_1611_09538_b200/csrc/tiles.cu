@@ -13,17 +13,22 @@
 //     a run = one x band, one z cell, the tile's y range) z-major, 32 runs at a time: a warp scan
 //     places them in the batch stream and every lane moves its run's records with one bulk copy
 //     (cp.async.bulk, SASS UBLKCP) into a ring of NB batches of BM records (mbarrier `raw`,
-//     transaction bytes).  Gather: also reduces finished batches' per-warp partials.
+//     transaction bytes).
 //   expanders (kEW warps): per batch, the tile windows wx[16], wy[16], wz[TZ] of every particle
 //     (zero outside the stencil, z wraps periodically, gridding folds q into wx) in 16-entry
-//     segments (one FGG recurrence each, started by binary powering of E); then `full`.
+//     segments (one FGG recurrence each, started by binary powering of E), and per particle the
+//     mask of consumer warps its stencil meets with its z-block mask; then `full`.  Gather: they
+//     also reduce finished batches' per-warp partials into the slots (lag 2, then `freeb`).
 //   consumers (16 warps): warp w owns the 4 x 4 column block (4 (w&3), 4 (w>>2)) over all TZ
-//     nodes; per batch it lists the particles meeting its block (order preserving) and runs
+//     nodes; per batch it lists the particles whose mask names it (order preserving) and runs
 //       gridding  C[16 cols x 8 z]        += A[16 cols x 16 particles] B[16 particles x 8 z]
 //                 A = (q wx) wy, B = wz                                   (m16n8k16)
 //       gather    T[16 particles x 8 cols] = A[16 particles x 8 z] (wz) B[8 z x 8 cols] (H~)
 //                 per col half, then phi_p += sum_cols wx wy T             (m16n8k8)
 //     skipping 8-node z blocks no particle of the k-step reaches; then arrives on `empty`.
+//   Field modes (FM, gather only): 1 phi and the x, y column moments, 2 d/dz through the
+//   z-derivative window (two passes), 3 all four in one pass (build knob).
+// Device-side bounds checks set bits of an error word (1 runs, 2 lists, 4 slots, 8 slot map).
 // No floating-point atomics: gridding writes its tile once; the gather writes one partial per
 // (particle, tile) into a fixed slot and k_gather_finish sums the slots in a fixed order, so
 // results are bitwise reproducible.
