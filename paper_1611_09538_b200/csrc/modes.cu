@@ -41,19 +41,22 @@ constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT 
 // null) of the plane buffer in layout L (kspace.cuh, slab_row).
 // Two real z columns per complex FFT (columns 2r and 2r+1 of the block as z_r = col_2r + i col_2r+1):
 // their spectra separate as A[n] = (Z[n] + conj Z[M-n])/2, B[n] = (Z[n] - conj Z[M-n])/(2i).
-__global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
+// CB (columns per block) is a template constant and M's log2 (or -1) is passed, so the index
+// splits below are shifts, not integer divisions by runtime values.
+template <int CB>
+__global__ void k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   const int S = M + 1;   // padded row stride: the transposed accesses below stay conflict-free
-  const int CH = CB / 2;
+  constexpr int CH = CB / 2;
   double2* buf = sm;
   double2* tmp = sm + CH * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   const double* src = grid + ((int64_t)x * Mt + y0) * M;
   double* bd = reinterpret_cast<double*>(buf);
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
-    const int c = idx / M, k = idx - c * M;
+    const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
     bd[2 * ((c >> 1) * S + k) + (c & 1)] = (y0 + c < Mt) ? src[idx] : 0.0;
   }
   __syncthreads();
@@ -71,12 +74,13 @@ __global__ void k_zfwd(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
 
 // Inverse: the Hermitian spectra a, b of columns 2r, 2r+1 combine into W[n] = a[n] + i b[n],
 // W[M-n] = conj a[n] + i conj b[n]; the complex inverse FFT gives col_2r + i col_2r+1.
-__global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const double2* __restrict__ tw,
+template <int CB>
+__global__ void k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
   const int S = M + 1;   // padded row stride (conflict-free transposed accesses)
-  const int CH = CB / 2;
+  constexpr int CH = CB / 2;
   double2* buf = sm;
   double2* tmp = sm + CH * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
@@ -92,7 +96,7 @@ __global__ void k_zinv(int Mt, int M, int nplanes, int CB, FftDesc fz, const dou
   double2* out = fft_rows<1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   double* dst = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
-    const int c = idx / M, k = idx - c * M;
+    const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
     if (y0 + c < Mt) {
       const double2 v = out[(c >> 1) * S + k];
       dst[idx] = (c & 1) ? v.y : v.x;
@@ -137,9 +141,18 @@ __global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const d
   const int i = S.slot(blockIdx.y), x0 = blockIdx.x * RB;
   const int nr = min(RB, Mt - x0);
   const double2* src = T + base + (int64_t)blockIdx.y * Mt * W + (int64_t)x0 * W;
-  for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
-    const int r = idx / W;
-    buf[idx] = (r < nr) ? src[idx] : make_double2(0.0, 0.0);
+  {
+    int r = threadIdx.x / W;   // flat loop, row split carried incrementally (no division per entry)
+    const int dr = blockDim.x / W;
+    for (int idx = threadIdx.x, y = threadIdx.x - r * W; idx < RB * W; idx += blockDim.x) {
+      buf[idx] = (r < nr) ? src[idx] : make_double2(0.0, 0.0);
+      r += dr;
+      y += blockDim.x - dr * W;
+      if (y >= W) {
+        y -= W;
+        ++r;
+      }
+    }
   }
   __syncthreads();
   double2* out = fft_rows<1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
@@ -151,7 +164,8 @@ __global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const d
 
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
 // kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
-__global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const double2* __restrict__ tw,
+template <int CB>
+__global__ void k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
                           double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
                           const double2* __restrict__ pl, PlaneSel S) {
@@ -170,8 +184,10 @@ __global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const 
   double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
   double2* oth = (out == buf) ? tmp : buf;
   const double2 pn = pl[n];
-  for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
-    const int c = idx / W, a = idx - c * W;
+  // flat loop over the CB x W entries with the (c, a) split carried incrementally (no division)
+  int c = threadIdx.x / W, a = threadIdx.x - c * W;
+  const int dc = blockDim.x / W, da = blockDim.x - dc * W;
+  for (; c < CB;) {
     const int y = min(y0 + c, W - 1);
     double m;
     if (kernel_class) {
@@ -182,6 +198,12 @@ __global__ void k_colpass(int Mt, int W, int64_t base, int CB, FftDesc f, const 
     }
     double2 v = out[c * SW + a];
     out[c * SW + a] = make_double2(v.x * m, v.y * m);
+    c += dc;
+    a += da;
+    if (a >= W) {
+      a -= W;
+      ++c;
+    }
   }
   __syncthreads();
   double2* res = fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
@@ -195,27 +217,69 @@ static void set_smem(const void* fn, size_t bytes) {
   SE1P_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+static int log2_or_neg(int n) {
+  int s = 0;
+  while ((1 << s) < n) ++s;
+  return (1 << s) == n ? s : -1;
+}
+
+template <int CB>
+static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
+                        int rows, cudaStream_t st) {
+  const int M = pl.dv.M, Mt = pl.dv.Mt;
+  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
+  set_smem((const void*)k_zfwd<CB>, smem);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
+  k_zfwd<CB><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, w.grid,
+                                              planes, L, slot_of);
+  SE1P_LAUNCH_CHECK();
+}
+
+template <int CB>
+static void zinv_launch(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
+                        int rows, cudaStream_t st) {
+  const int M = pl.dv.M, Mt = pl.dv.Mt;
+  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
+  set_smem((const void*)k_zinv<CB>, smem);
+  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
+  k_zinv<CB><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, planes,
+                                              w.grid, L, slot_of);
+  SE1P_LAUNCH_CHECK();
+}
+
 void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
                     cudaStream_t st) {
-  const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
-  set_smem((const void*)k_zfwd, smem);
-  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zfwd<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, w.grid, planes, L, slot_of);
-  SE1P_LAUNCH_CHECK();
+  switch (zcols(pl.dv.M)) {
+    case 4: zfwd_launch<4>(pl, w, planes, L, slot_of, rows, st); break;
+    case 8: zfwd_launch<8>(pl, w, planes, L, slot_of, rows, st); break;
+    case 16: zfwd_launch<16>(pl, w, planes, L, slot_of, rows, st); break;
+    case 32: zfwd_launch<32>(pl, w, planes, L, slot_of, rows, st); break;
+    default: zfwd_launch<64>(pl, w, planes, L, slot_of, rows, st);
+  }
 }
 
 void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
                     cudaStream_t st) {
-  const int M = pl.dv.M, Mt = pl.dv.Mt, CB = zcols(M);
   const int rows = L.xlo[L.nslab] - L.xlo[0];
   if (rows <= 0) return;
-  const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
-  set_smem((const void*)k_zinv, smem);
-  dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zinv<<<grid, kFftThreads, smem, st>>>(Mt, M, pl.n_planes, CB, pl.fz, pl.d_tw + pl.twz, planes, w.grid, L, slot_of);
+  switch (zcols(pl.dv.M)) {
+    case 4: zinv_launch<4>(pl, w, planes, L, slot_of, rows, st); break;
+    case 8: zinv_launch<8>(pl, w, planes, L, slot_of, rows, st); break;
+    case 16: zinv_launch<16>(pl, w, planes, L, slot_of, rows, st); break;
+    case 32: zinv_launch<32>(pl, w, planes, L, slot_of, rows, st); break;
+    default: zinv_launch<64>(pl, w, planes, L, slot_of, rows, st);
+  }
+}
+
+template <int CB>
+static void colpass_launch(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
+                           int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
+  const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2);
+  set_smem((const void*)k_colpass<CB>, smc);
+  k_colpass<CB><<<dim3((unsigned)ceil_div(W, CB), nplanes), kFftThreads, smc, st>>>(
+      pl.dv.Mt, W, base, f, tw, w.T, kernel_class, pl.d_khat, pl.d_exJ, pl.d_k2J, (const double2*)pl.d_pl, S);
   SE1P_LAUNCH_CHECK();
 }
 
@@ -224,17 +288,18 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
   if (nplanes <= 0) return;
   const int Mt = pl.dv.Mt;
   const int RB = rows_for(W), CB = cols_for(W);
-  const size_t smr = 2 * (size_t)RB * W * sizeof(double2), smc = 2 * (size_t)CB * (W + 1) * sizeof(double2);
+  const size_t smr = 2 * (size_t)RB * W * sizeof(double2);
   set_smem((const void*)k_rowfwd, smr);
   set_smem((const void*)k_rowinv, smr);
-  set_smem((const void*)k_colpass, smc);
   const double2* tw = pl.d_tw + twoff;
   k_rowfwd<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), kFftThreads, smr, st>>>(Mt, W, base, RB, f, tw, planes, w.T, L, S);
   SE1P_LAUNCH_CHECK();
-  k_colpass<<<dim3((unsigned)ceil_div(W, CB), nplanes), kFftThreads, smc, st>>>(Mt, W, base, CB, f, tw, w.T, kernel_class,
-                                                                        pl.d_khat, pl.d_exJ, pl.d_k2J,
-                                                                        (const double2*)pl.d_pl, S);
-  SE1P_LAUNCH_CHECK();
+  switch (CB) {
+    case 2: colpass_launch<2>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+    case 4: colpass_launch<4>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+    case 16: colpass_launch<16>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+    default: colpass_launch<8>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
+  }
   k_rowinv<<<dim3((unsigned)ceil_div(Mt, RB), nplanes), kFftThreads, smr, st>>>(Mt, W, base, RB, f, tw, w.T, planes, L, S);
   SE1P_LAUNCH_CHECK();
 }

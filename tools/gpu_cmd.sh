@@ -1,1 +1,2 @@
-RUN_PARITY=1 NO_FIELD=1 bash tools/exp_variant.sh cw "" "-DSE1P_COLPASS_WARP=1 -DSE1P_COLS_LARGE=8" "-DSE1P_COLPASS_WARP=0"
+for c in C5 C4; do timeout 300 python tools/stage_times.py $c tiles; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
