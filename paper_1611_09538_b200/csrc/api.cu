@@ -246,7 +246,7 @@ static void run_graphed(const KParams& prm, int64_t N, const void* x, const void
                         const void* field, cudaStream_t st, F&& stages) {
   for (auto& g : g_graphs)
     if (g.prm == prm && g.N == N && g.x == x && g.q == q && g.phi == phi && g.field == field && g.st == st &&
-        g.gen == g_ws_generation) {
+        g.gen == g_ws_generation + kplan_generation()) {
       SE1P_CUDA_TRY(cudaGraphLaunch(g.exec, st));
       g_launches = g.launches;
       return;
@@ -271,7 +271,8 @@ static void run_graphed(const KParams& prm, int64_t N, const void* x, const void
     cudaGraphExecDestroy(g_graphs.front().exec);
     g_graphs.erase(g_graphs.begin());
   }
-  g_graphs.push_back(GraphEntry{prm, N, x, q, phi, field, st, g_ws_generation, g_launches - l0, exec});
+  g_graphs.push_back(GraphEntry{prm, N, x, q, phi, field, st, g_ws_generation + kplan_generation(), g_launches - l0,
+                                exec});
   SE1P_CUDA_TRY(cudaGraphLaunch(exec, st));
 }
 
@@ -845,9 +846,13 @@ void se1p_release(void) {
   KWork& w = ds.w;
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
-                  (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap})
+                  (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap, (void*)w.grid3, (void*)ds.sel,
+                  (void*)ds.idmap, (void*)ds.xsel})
     if (p) cudaFree(p);
   ds = DevState{};
+  for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);   // they bake the freed pointers
+  g_graphs.clear();
+  ++g_ws_generation;
 }
 
 const char* se1p_last_error(void) { return g_err.c_str(); }

@@ -38,6 +38,9 @@ static double scaling(double kap2, double k3sq, double eta, double xi, double R)
 }
 
 static std::vector<std::unique_ptr<KPlan>> g_plans;
+static uint64_t g_plan_generation = 1;   // bumped whenever a plan is built or freed (graphs bake its pointers)
+
+uint64_t kplan_generation() { return g_plan_generation; }
 
 static KPlan* build(const KParams& p, cudaStream_t st) {
   auto t0 = std::chrono::steady_clock::now();
@@ -145,6 +148,7 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
 KPlan* kplan_get(const KParams& p, cudaStream_t st) {
   for (auto& q : g_plans)
     if (q->prm == p) return q.get();
+  ++g_plan_generation;
   if (g_plans.size() >= 16) {
     KPlan* old = g_plans.front().get();
     cudaFree(old->d_tw);
@@ -159,6 +163,7 @@ KPlan* kplan_get(const KParams& p, cudaStream_t st) {
 }
 
 void kplan_release_all() {
+  ++g_plan_generation;
   for (auto& q : g_plans) {
     cudaFree(q->d_tw);
     cudaFree(q->d_khat);

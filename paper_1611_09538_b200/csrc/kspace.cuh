@@ -118,6 +118,7 @@ struct KWork {                  // per-N workspace (grown on demand)
 
 KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached
 void kplan_release_all();
+uint64_t kplan_generation();   // changes whenever a plan is built or freed
 void plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out);   // planner.cu
 double lambert_w0(double x);
 

@@ -264,6 +264,10 @@ def test_graph_mode_replays_bitwise():
     assert torch.equal(e1, e2)
     with pytest.raises(se1p.SE1PError):
         se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, profile=True, **kw)
+    # release frees workspace, plans and graphs; the next graph call re-captures
+    se1p.release()
+    g3 = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, graph=True, out=out, **kw).clone()
+    assert torch.equal(g3, se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw))
 
 
 def test_multi_tier_matches_oracle():
