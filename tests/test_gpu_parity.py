@@ -285,3 +285,47 @@ def test_multi_tier_matches_oracle():
     assert np.array_equal(flat, same)
     with pytest.raises(se1p.SE1PError):
         se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, Ntilde=2 * Mt, S_modes=[Mt - 1] * n_l)
+
+
+def test_random_configurations_match_oracle():
+    """Seeded random valid configurations (M, P, box aspect, xi, n_l, extents, N): element-wise
+    parity with the Alg. 1 oracle -- catches index/tiling assumptions the named cases miss."""
+    rng = np.random.default_rng(2024)
+    checked = 0
+    while checked < 12:
+        M = int(rng.choice([8, 10, 12, 14, 16, 20, 24, 30, 32, 36, 40, 48]))
+        P = int(rng.integers(2, min(M, 28) + 1))
+        L3 = float(rng.choice([0.5, 1.0, 1.5, 2.0]))
+        m1 = int(rng.choice([M // 2, M, (3 * M) // 2])) if M % 2 == 0 else M
+        h = L3 / M
+        L = (m1 * h, m1 * h, L3)
+        xi = float(rng.uniform(2.0, 9.0)) / max(L)
+        eta = P * xi ** 2 * h ** 2 / (0.95 ** 2 * math.pi)
+        if not (0.05 < eta < 0.95):
+            continue
+        Mt = m1 + P
+        n_l = int(rng.integers(0, M // 2 + 1))
+        S0 = int(Mt * rng.uniform(2.5, 4.0))
+        SI = int(Mt * rng.uniform(1.0, 3.0)) if n_l else Mt
+        SJ = int(rng.integers(Mt, 2 * Mt))
+        while not all(f in (2, 3, 5, 7) for f in _factors(SJ)):
+            SJ += 1
+        if not all(f in (2, 3, 5, 7) for f in _factors(M)):
+            continue
+        N = int(rng.integers(2, 400))
+        x, q = make_system(N, L, int(rng.integers(1, 10 ** 6)))
+        ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+        got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+        err = np.max(np.abs(got - ref))
+        assert err <= 1e-11 * np.max(np.abs(ref)), (M, P, L, xi, n_l, S0, SI, SJ, N, err)
+        checked += 1
+
+
+def _factors(n):
+    f, d = [], 2
+    while d * d <= n:
+        while n % d == 0:
+            f.append(d)
+            n //= d
+        d += 1
+    return f + ([n] if n > 1 else [])
