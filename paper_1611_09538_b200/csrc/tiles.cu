@@ -285,7 +285,7 @@ auto reduce = [&](int b, int rt) {
         }
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc)
-          A.gpart[(i * nslot + (sx * dv.nsxy + sy) * dv.nsz + sz) * NCT + COFF + cc] = sum[cc];
+          A.gpart[(int64_t)(((sx * dv.nsxy + sy) * dv.nsz + sz) * NCT + COFF + cc) * dv.N + i] = sum[cc];
       } else if (hx) {
         for (int v = 0; v < kCW * NC; ++v)
           if (ap[v] != 0.0) atomicOr(dv.err, 8);   // consumer listed a particle the slot map lacks
@@ -776,7 +776,9 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
   const int nx = fdiv(st.x + P - 1, kTXY) - fdiv(st.x, kTXY) + 1;
   const int ny = fdiv(st.y + P - 1, kTXY) - fdiv(st.y, kTXY) + 1;
   const int nz = zcount(st.w, P, dv.M, TZ);
-  const double* g = gpart + p * dv.nslot * NC;
+  // slot-major partials [slot][value][particle]: a tile's consecutive particles write, and the
+  // finish's consecutive threads read, consecutive addresses
+  const double* g = gpart + p;
   double s[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) s[c] = 0.0;
@@ -786,7 +788,7 @@ __global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int*
     for (int b = 0; b < ny; ++b)
       for (int z = 0; z < nz; ++z)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) s[c] += g[((a * dv.nsxy + b) * dv.nsz + z) * NC + c];
+        for (int c = 0; c < NC; ++c) s[c] += g[(int64_t)(((a * dv.nsxy + b) * dv.nsz + z) * NC + c) * N];
   }
   const int64_t u = perm[p];
   if (phi) phi[u] = s[0];
