@@ -849,6 +849,9 @@ void se1p_release(void) {
                   (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap, (void*)w.grid3, (void*)ds.sel,
                   (void*)ds.idmap, (void*)ds.xsel})
     if (p) cudaFree(p);
+  if (w.side) cudaStreamDestroy(w.side);
+  if (w.ev_fork) cudaEventDestroy(w.ev_fork);
+  if (w.ev_join) cudaEventDestroy(w.ev_join);
   ds = DevState{};
   for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);   // they bake the freed pointers
   g_graphs.clear();

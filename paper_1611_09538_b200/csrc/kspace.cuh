@@ -114,6 +114,8 @@ struct KWork {                  // per-N workspace (grown on demand)
   double* red = nullptr;        // reductions (neutrality check)
   int* flag = nullptr;
   double* host_x = nullptr;     // staging for host_io
+  cudaStream_t side = nullptr;  // second stream of the mode stage (kernel planes beside J planes)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached

@@ -29,6 +29,9 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 #ifndef SE1P_COLS_LARGE
 #define SE1P_COLS_LARGE 4
 #endif
+#ifndef SE1P_MODES_TWO_STREAMS
+#define SE1P_MODES_TWO_STREAMS 1
+#endif
 #ifndef SE1P_FFT_THREADS
 #define SE1P_FFT_THREADS 256
 #endif
@@ -312,8 +315,26 @@ void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& 
   const int Mt = pl.dv.Mt;
   if (!glK) nK = pl.n_kernel;
   if (!glJ) nJ = pl.n_planes - pl.n_kernel;
-  mode_class(pl, w, planes, L, PlaneSel{glK, liK, 0}, nK, pl.LK, pl.fK, pl.twK, 0, 1, st);
   const int64_t baseJ = (int64_t)nK * Mt * pl.LK;
+#if SE1P_MODES_TWO_STREAMS
+  // the two plane classes are independent (disjoint planes and T regions) and each pass is
+  // latency bound: the kernel planes run on a second stream beside the J planes
+  if (nK > 0 && nJ > 0) {
+    if (!w.side) {
+      SE1P_CUDA_TRY(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
+      SE1P_CUDA_TRY(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
+      SE1P_CUDA_TRY(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
+    }
+    SE1P_CUDA_TRY(cudaEventRecord(w.ev_fork, st));
+    SE1P_CUDA_TRY(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+    mode_class(pl, w, planes, L, PlaneSel{glK, liK, 0}, nK, pl.LK, pl.fK, pl.twK, 0, 1, w.side);
+    mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
+    SE1P_CUDA_TRY(cudaEventRecord(w.ev_join, w.side));
+    SE1P_CUDA_TRY(cudaStreamWaitEvent(st, w.ev_join, 0));
+    return;
+  }
+#endif
+  mode_class(pl, w, planes, L, PlaneSel{glK, liK, 0}, nK, pl.LK, pl.fK, pl.twK, 0, 1, st);
   mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
 }
 

@@ -1,1 +1,2 @@
-NO_FIELD=1 bash tools/exp_variant.sh m3 "" "-DSE1P_COLS_SMALL=4 -DSE1P_COLS_LARGE=2" "-DSE1P_COLS_SMALL=16 -DSE1P_COLS_LARGE=8" "-DSE1P_ROW_SMEM=32768" "-DSE1P_ROW_SMEM=65536"
+RUN_PARITY=1 NO_FIELD=1 bash tools/exp_variant.sh ts "" "-DSE1P_MODES_TWO_STREAMS=0"
+timeout 300 python tools/graph_times.py 2>&1 | tail -5
