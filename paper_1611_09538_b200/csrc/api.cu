@@ -852,6 +852,8 @@ void se1p_release(void) {
   if (w.side) cudaStreamDestroy(w.side);
   if (w.ev_fork) cudaEventDestroy(w.ev_fork);
   if (w.ev_join) cudaEventDestroy(w.ev_join);
+  if (w.side2) cudaStreamDestroy(w.side2);
+  if (w.ev_join2) cudaEventDestroy(w.ev_join2);
   ds = DevState{};
   for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);   // they bake the freed pointers
   g_graphs.clear();

@@ -116,6 +116,8 @@ struct KWork {                  // per-N workspace (grown on demand)
   double* host_x = nullptr;     // staging for host_io
   cudaStream_t side = nullptr;  // second stream of the mode stage (kernel planes beside J planes)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr; // third stream (second half of the J planes)
+  cudaEvent_t ev_join2 = nullptr;
 };
 
 KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached

@@ -30,7 +30,7 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 #define SE1P_COLS_LARGE 4
 #endif
 #ifndef SE1P_MODES_TWO_STREAMS
-#define SE1P_MODES_TWO_STREAMS 1
+#define SE1P_MODES_TWO_STREAMS 2   // 1: kernel planes beside J planes; 2: and the J planes in two halves
 #endif
 #ifndef SE1P_FFT_THREADS
 #define SE1P_FFT_THREADS 256
@@ -328,7 +328,23 @@ void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& 
     SE1P_CUDA_TRY(cudaEventRecord(w.ev_fork, st));
     SE1P_CUDA_TRY(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
     mode_class(pl, w, planes, L, PlaneSel{glK, liK, 0}, nK, pl.LK, pl.fK, pl.twK, 0, 1, w.side);
-    mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
+#if SE1P_MODES_TWO_STREAMS > 1
+    if (nJ >= 8) {   // the J planes in two halves on two streams
+      if (!w.side2) {
+        SE1P_CUDA_TRY(cudaStreamCreateWithFlags(&w.side2, cudaStreamNonBlocking));
+        SE1P_CUDA_TRY(cudaEventCreateWithFlags(&w.ev_join2, cudaEventDisableTiming));
+      }
+      SE1P_CUDA_TRY(cudaStreamWaitEvent(w.side2, w.ev_fork, 0));
+      const int nJ1 = nJ / 2;
+      mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ1, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
+      const PlaneSel S2{glJ ? glJ + nJ1 : nullptr, liJ ? liJ + nJ1 : nullptr, pl.n_kernel + nJ1};
+      mode_class(pl, w, planes, L, S2, nJ - nJ1, pl.prm.SJ, pl.fJ, pl.twJ, baseJ + (int64_t)nJ1 * Mt * pl.prm.SJ, 0,
+                 w.side2);
+      SE1P_CUDA_TRY(cudaEventRecord(w.ev_join2, w.side2));
+      SE1P_CUDA_TRY(cudaStreamWaitEvent(st, w.ev_join2, 0));
+    } else
+#endif
+      mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
     SE1P_CUDA_TRY(cudaEventRecord(w.ev_join, w.side));
     SE1P_CUDA_TRY(cudaStreamWaitEvent(st, w.ev_join, 0));
     return;
