@@ -1,2 +1,2 @@
-B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
-$B > gpurun_out/r1v_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file gpurun_out/r1v_launches.csv $B > gpurun_out/r1v_ncu1.log 2>&1; tail -1 gpurun_out/r1v_ncu1.log
+REAL_ONLY=1 bash tools/exp_variant.sh rc "" "-DSE1P_REAL_CHUNKED=0"
+timeout 900 python -m pytest tests -m gpu -x -q -k "real or full or field or planner" 2>&1 | tail -2
