@@ -6,9 +6,15 @@
 // cells cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell (u mod nc_z)
 // shifted by floor(u/nc_z) L3; a cell whose box lies farther than rc from the target is skipped.
 // Every image within rc is visited exactly once, for any rc.
+#include <vector>
+
 #include "kspace.cuh"
 #include "real.cuh"
 #include "sort.cuh"
+
+#ifndef SE1P_REAL_TABLE
+#define SE1P_REAL_TABLE 1
+#endif
 
 // Cell width rc/D, D in 1..4 chosen for ~32 particles per cell (measured at C3/C4/C5: D = 3/4/2
 // best, -45% / -57% / -33% against D = 1)
@@ -78,6 +84,27 @@ __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restr
           const double dx = pt.x - ps.x, dy = pt.y - ps.y, dz = pt.z - (ps.z + shift);
           const double r2 = dx * dx + dy * dy + dz * dz;
           if (r2 <= rc2) {
+#if SE1P_REAL_TABLE
+            // erfc(xi r) from the local polynomial of r's interval (no erfc, exp or division)
+            const double rinv = rsqrt(r2), r = r2 * rinv;
+            const int it = min((int)(r * d.inv_dr), kTabN - 1);
+            const double u = r - ((double)it + 0.5) * d.dr;
+            const double* cf = d.tab + it * (kTabDeg + 1);
+            double pv = __ldg(cf + kTabDeg), dv = 0.0;
+#pragma unroll
+            for (int k = kTabDeg - 1; k >= 0; --k) {
+              if (FIELD) dv = fma(dv, u, pv);
+              pv = fma(pv, u, __ldg(cf + k));
+            }
+            const double ec = pv * rinv;
+            acc = fma(ps.w, ec, acc);
+            if (FIELD) {   // dv = d/dr erfc(xi r) = -(2 xi/sqrt(pi)) e^{-xi^2 r^2}
+              const double g = ps.w * (ec - dv) * (rinv * rinv);
+              ex = fma(g, dx, ex);
+              ey = fma(g, dy, ey);
+              ez = fma(g, dz, ez);
+            }
+#else
             const double r = sqrt(r2);
             const double ec = erfc(d.xi * r) / r;
             acc = fma(ps.w, ec, acc);
@@ -88,6 +115,7 @@ __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restr
               ey = fma(g, dy, ey);
               ez = fma(g, dz, ez);
             }
+#endif
           }
         }
       }
@@ -120,8 +148,60 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
   return d;
 }
 
-void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
+// Taylor coefficients of erfc(xi r) about the interval midpoints r_i = (i + 1/2) dr:
+// d^n/dx^n erfc(x) = (-1)^n (2/sqrt(pi)) H_{n-1}(x) e^{-x^2} (physicists' Hermite polynomials),
+// evaluated in long double; term n carries xi^n/n!.  Interval half-width xi dr/2 <= 0.013 for
+// xi rc <= 6.6, so the degree-10 remainder is below 1e-25 relative to the leading term.
+static std::vector<double> erfc_table(double xi, double rc) {
+  std::vector<double> t((size_t)kTabN * (kTabDeg + 1));
+  const long double dr = (long double)rc / kTabN, two_over_sqrtpi = 1.128379167095512573896158903121545172L;
+  for (int i = 0; i < kTabN; ++i) {
+    const long double x0 = (long double)xi * ((long double)i + 0.5L) * dr;
+    const long double g = two_over_sqrtpi * expl(-x0 * x0);
+    long double hm1 = 0.0L, h = 1.0L;   // H_{-1} (unused), H_0
+    t[(size_t)i * (kTabDeg + 1)] = (double)erfcl(x0);
+    long double xin = 1.0L, fact = 1.0L;
+    for (int n = 1; n <= kTabDeg; ++n) {
+      xin *= (long double)xi;
+      fact *= (long double)n;
+      // coefficient of u^n: (-1)^n (2/sqrt(pi)) H_{n-1}(x0) e^{-x0^2} xi^n / n!
+      const long double c = ((n & 1) ? -1.0L : 1.0L) * g * h * xin / fact;
+      t[(size_t)i * (kTabDeg + 1) + n] = (double)c;
+      const long double hn = 2.0L * x0 * h - 2.0L * (long double)(n - 1) * hm1;   // H_n
+      hm1 = h;
+      h = hn;
+    }
+  }
+  return t;
+}
+
+struct TabCache {
+  double xi = 0, rc = 0;
+  double* dev = nullptr;
+};
+static TabCache g_tab[64];
+
+void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out) {
+  RDev d = d0;
+#if SE1P_REAL_TABLE
+  {
+    int dev = 0;
+    SE1P_CUDA_TRY(cudaGetDevice(&dev));
+    TabCache& tc = g_tab[dev & 63];
+    if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
+      const std::vector<double> t = erfc_table(d.xi, d.rc);
+      if (!tc.dev) SE1P_CUDA_TRY(cudaMalloc(&tc.dev, sizeof(double) * t.size()));
+      SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
+      SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+      tc.xi = d.xi;
+      tc.rc = d.rc;
+    }
+    d.tab = tc.dev;
+    d.dr = d.rc / kTabN;
+    d.inv_dr = kTabN / d.rc;
+  }
+#endif
   const int ncell = d.nc[0] * d.nc[1] * d.nc[2];
   const unsigned nb = (unsigned)ceil_div(N, 256);
   k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);

@@ -14,7 +14,11 @@ struct RDev {
   int K;          // periodic-axis cell reach
   int Kx, Ky;     // free-axis cell reach (cells are >= rc/D wide)
   double xi, rc;
+  // erfc(xi r) on [0, rc] as kTabN local Taylor polynomials of degree kTabDeg in r - r_mid
+  const double* tab = nullptr;
+  double inv_dr = 0.0, dr = 0.0;
 };
+constexpr int kTabN = 256, kTabDeg = 10;
 
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
