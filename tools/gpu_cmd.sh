@@ -1,2 +1,2 @@
-REAL_ONLY=1 bash tools/exp_variant.sh rf "" "-DSE1P_REAL_F32_REJECT=0"
-timeout 900 python -m pytest tests -m gpu -x -q -k "real or full or field or planner" 2>&1 | tail -2
+timeout 900 python tools/se1p_vs_se3p.py > gpurun_out/se1p_vs_se3p.log 2>&1; tail -15 gpurun_out/se1p_vs_se3p.log
+timeout 600 python tools/table2.py > gpurun_out/table2.log 2>&1; tail -3 gpurun_out/table2.log
