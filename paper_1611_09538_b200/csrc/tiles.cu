@@ -66,7 +66,7 @@ constexpr int kCW = 16;                          // consumer warps
 __host__ __device__ constexpr int n_exp_warps(int fm) { return fm == 3 ? SE1P_EXP_WARPS_FIELD : SE1P_EXP_WARPS; }
 __host__ __device__ constexpr int n_threads(int fm) { return (kCW + 1 + n_exp_warps(fm)) * 32; }
 __host__ __device__ constexpr int fm_outputs(int fm) { return fm == 0 ? 1 : (fm == 1 ? 3 : (fm == 2 ? 1 : 4)); }
-constexpr int kMaxNB = 4;
+constexpr int kMaxNB = 6;
 // doubles per compact record: {s4, q, index, (A, E) per axis} (80 B); the field gather adds the
 // particle position (112 B)
 __host__ __device__ constexpr int rec_len(int field) { return field ? 14 : 10; }
@@ -894,6 +894,16 @@ static void launch_tiles(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx
     if (BM) break;
   }
   if (!BM) throw Error{4, "tile kernels do not fit in shared memory"};
+  {   // experiment override (tools/): batch size and ring depth, if they fit
+    const char* eb = getenv(GATHER ? "SE1P_GATHER_BM" : "SE1P_SPREAD_BM");
+    const char* en = getenv(GATHER ? "SE1P_GATHER_NB" : "SE1P_SPREAD_NB");
+    const int bm = eb ? atoi(eb) : BM, nb = en ? atoi(en) : NB;
+    if ((eb || en) && bm >= 16 && bm <= 128 && nb >= (GATHER ? 3 : 2) && nb <= kMaxNB &&
+        tile_smem(bm, nb, TZ, GATHER, FM).total <= limit) {
+      BM = bm;
+      NB = nb;
+    }
+  }
   a.BM = BM;
   a.NB = NB;
   const size_t smem = (size_t)tile_smem(BM, NB, TZ, GATHER, FM).total;

@@ -1,2 +1,3 @@
-timeout 900 python tools/se1p_vs_se3p.py > gpurun_out/se1p_vs_se3p.log 2>&1; tail -15 gpurun_out/se1p_vs_se3p.log
-timeout 600 python tools/table2.py > gpurun_out/table2.log 2>&1; tail -3 gpurun_out/table2.log
+for v in "SE1P_GATHER_BM=56 SE1P_GATHER_NB=5" "SE1P_GATHER_BM=52 SE1P_GATHER_NB=5" "SE1P_SPREAD_BM=60 SE1P_SPREAD_NB=5"; do
+  echo "== [$v]"; env $v timeout 200 python tools/stage_times.py C5 tiles; env $v timeout 200 python tools/stage_times.py C4 tiles
+done
