@@ -85,7 +85,10 @@ typedef struct se1p_plan_info {
 } se1p_plan_info;
 
 /* k-space potential phi^F (Alg. 1 OUTPUT): no real-space and no self term.
-     M        grid points along the periodic axis; h = L[2]/M, free-axis counts L[0]/h, L[1]/h
+     M        grid points along the periodic axis; h = L[2]/M.  The free axes are solved on the
+              square [0, max(L[0],L[1]))^2, whose side must be an integer multiple of h; a
+              rectangular box is embedded in it (phi^F is free-space in x, y, so
+              the embedding does not change it; reading R-19).
      P        Gaussian support points per dimension
      eta      <= 0 -> P xi^2 h^2/(0.95^2 pi) (Eq. (comp_eta))
      s0, sf   upsampling factors of k3 = 0 and of the I modes (Eq. (upsamplings));
@@ -198,15 +201,16 @@ int se1p_kspace_tiers_ex(const se1p_opts* opts, void* stream, const double* x, c
    truncated to P^3 nodes, h = L[2]/M, eta as in se1p_kspace), a plain 3D FFT of the
    M_free x M_free x M periodic grid (no upsampling) and the scaling e^{-(1-eta)k^2/4xi^2}/k^2
    (k = 0 dropped).  P must be even; x, y in [0,L1) x [0,L2) (any z).  Same pointers, ownership,
-   opts and errors as se1p_kspace_ex. */
+   opts and errors as se1p_kspace_ex; L1 != L2 -> SE1P_EPARAM (the periodic cross-section must be
+   square in this build). */
 int se1p_kspace3p_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
                      int64_t N, const double L[3], double xi, int M, int P, double eta,
                      double* phi_out);
 
 /* Parameters from an absolute rms error tolerance: the paper's recipe
    "Parameter selection" -- rc and kinf by inverting the Kolafa-Perram estimates
-   (Eqs. (rc), (kinf), Lambert W), M = 2 kinf (even, FFT-friendly, L1/h and L2/h
-   integers), P the smallest even integer with A e^{-c^2 pi P/2} <= tol (Eq.
+   (Eqs. (rc), (kinf), Lambert W), M = 2 kinf (even, FFT-friendly, max(L1,L2)/h
+   integer), P the smallest even integer with A e^{-c^2 pi P/2} <= tol (Eq.
    (approximation_error_oneterm), c = 0.95), eta, s_l from e^{-2 pi s_l} < tol
    (P:697), n_l = ceil(M/10), s0 = 1 + sqrt(2).  Host-only (no device
    work).  Non-cubic boxes: DESIGN.md reading R-18.  Q = sum q_n^2; xi is the caller's choice
@@ -214,12 +218,12 @@ int se1p_kspace3p_ex(const se1p_opts* opts, void* stream, const double* x, const
    of tol (real space tol/2, k-space truncation and aliasing tol/10, window tol/100) and M is
    raised until eta <= 0.8 (reading R-18), so the measured rms error meets tol.
    Errors: SE1P_EINVAL (null, Q/xi/L <= 0, tol not in (0,1)), SE1P_EPARAM (no admissible M <=
-   8192, non-square cross-section). */
+   8192). */
 typedef struct se1p_tol_plan {
   double xi, tol, Q;
   double rc;                 /* real-space cutoff, Eq. (rc)                                  */
   double kinf;               /* Eq. (kinf) (unrounded)                                       */
-  int M, P, Mfree, Mt;       /* periodic points, support, L1/h, M~ = Mfree + P               */
+  int M, P, Mfree, Mt;       /* periodic points, support, max(L1,L2)/h, M~ = Mfree + P      */
   double h, eta;
   int n_local;               /* n_l                                                          */
   double s_l, s0;            /* upsampling factors                                           */

@@ -140,9 +140,16 @@ static int extent_from_factor(double s, int Mt) { return (int)std::ceil(s * Mt -
 //          same for any S, so the planner takes a generous S
 //   SJ     given, else the smallest FFT-friendly extent with Ntilde h - L >= 23 L3/(2 pi (n_l+1))
 //          (aliasing distance of the first J mode for a 1e-10 estimate, SURVEY c-6)
-static KParams resolve(const se1p_opts* o, const double L[3], double xi, int M, int P, double eta, double s0,
-                       double sf, int n_local) {
-  if (!L || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "box lengths must be positive"};
+//
+// A rectangular free cross-section (L1 != L2, embed = true) is solved on the square domain
+// [0, max(L1,L2))^2: phi^F is the free-space solution in x, y, so it does not depend
+// on L1, L2 once every particle lies inside the grid's domain, and the truncated kernel's R
+// (reading R-6) covers the larger square.  The particle checks still use the user's box.
+static KParams resolve(const se1p_opts* o, const double Lu[3], double xi, int M, int P, double eta, double s0,
+                       double sf, int n_local, bool embed = true) {
+  if (!Lu || !(Lu[0] > 0) || !(Lu[1] > 0) || !(Lu[2] > 0)) throw Error{1, "box lengths must be positive"};
+  const double Lsq = std::max(Lu[0], Lu[1]);
+  const double L[3] = {embed ? Lsq : Lu[0], embed ? Lsq : Lu[1], Lu[2]};
   if (!(xi > 0)) throw Error{1, "xi must be positive"};
   if (M < 2) throw Error{1, "M must be >= 2"};
   KParams p{};
@@ -157,7 +164,6 @@ static KParams resolve(const se1p_opts* o, const double L[3], double xi, int M, 
   const long M1 = std::lround(m1), M2 = std::lround(m2);
   if (std::fabs(m1 - M1) > 1e-9 * m1 || std::fabs(m2 - M2) > 1e-9 * m2)
     throw Error{4, "L1/h and L2/h must be integers (h = L3/M)"};
-  if (M1 != M2) throw Error{4, "this build requires a square free cross-section (L1/h == L2/h)"};
   if (M % 2) throw Error{4, "M must be even (Hermitian half along z)"};
   if (P < 2 || P > M || P > (int)M1 + P || P > 64) throw Error{4, "P must satisfy 2 <= P <= min(M, 64)"};
   const int Mt = (int)M1 + P;
@@ -289,7 +295,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
   KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
   if (S_modes) {   // multi-tier upsampling
-    const int Mt = (int)std::lround(L[0] / (L[2] / M)) + P;
+    const int Mt = (int)std::lround(prm.L[0] / (L[2] / M)) + P;
     prm.SIn.assign(S_modes, S_modes + prm.n_l);
     for (int S : prm.SIn)
       if (S < Mt) throw Error{4, "every per-mode extent must be >= M~ = M_free + P"};
@@ -396,7 +402,8 @@ static void kspace3p_impl(const se1p_opts* o, cudaStream_t st, const double* x, 
   if (N > (int64_t)2000000000) throw Error{1, "N too large for int32 indices"};
   if (P % 2) throw Error{4, "SE3P needs an even P (the folded stencil nodes are then lattice nodes)"};
   se1p_opts none{};
-  KParams pa = resolve(&none, L, xi, M, P, eta, -1.0, -1.0, 0);
+  if (L && L[0] != L[1]) throw Error{4, "SE3P in this build requires a square periodic cross-section (L1 == L2)"};
+  KParams pa = resolve(&none, L, xi, M, P, eta, -1.0, -1.0, 0, false);
   const int Mf = (int)std::lround(L[0] / (L[2] / M));
   pa.n_l = -1;   // tile plan only: no kernel planes, no upsampling
   pa.S0 = pa.SI = Mf + P;

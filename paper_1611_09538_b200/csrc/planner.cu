@@ -51,7 +51,7 @@ void plan_from_tol(const double L[3], double Q, double xi, double E, se1p_tol_pl
   if (!L || !o) throw Error{1, "null pointer"};
   if (!(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0) || !(Q > 0) || !(xi > 0) || !(E > 0) || !(E < 1))
     throw Error{1, "L, Q, xi must be > 0 and 0 < tol < 1"};
-  const double V = L[0] * L[1] * L[2], L3 = L[2], c = 0.95;
+  const double V = L[0] * L[1] * L[2], L3 = L[2], c = 0.95, Lsq = std::max(L[0], L[1]);
   *o = se1p_tol_plan{};
   o->xi = xi;
   o->tol = E;
@@ -73,16 +73,15 @@ void plan_from_tol(const double L[3], double Q, double xi, double E, se1p_tol_pl
   int M = 2 * (int)std::ceil(o->kinf - 1e-12);
   for (;; M += 2) {
     if (M > 8192) throw Error{4, "no admissible M <= 8192 (L1/h and L2/h integers, eta < 1)"};
-    const double m1 = L[0] * M / L3, m2 = L[1] * M / L3;
-    if (std::fabs(m1 - std::lround(m1)) > 1e-9 * m1 || std::fabs(m2 - std::lround(m2)) > 1e-9 * m2) continue;
+    const double m1 = Lsq * M / L3;   // the square domain the solve runs on (api.cu resolve)
+    if (std::fabs(m1 - std::lround(m1)) > 1e-9 * m1) continue;
     if (!friendly(M) || M < P) continue;   // P <= M (Thm 1)
     const double hm = L3 / M;
     if (P * xi * xi * hm * hm / (c * c * kPi) <= eta_max) break;
   }
   o->M = M;
   o->h = L3 / M;
-  o->Mfree = (int)std::lround(L[0] / o->h);
-  if (std::lround(L[1] / o->h) != o->Mfree) throw Error{4, "this build requires a square free cross-section"};
+  o->Mfree = (int)std::lround(Lsq / o->h);
   o->P = P;
   o->Mt = o->Mfree + P;
   o->eta = P * xi * xi * o->h * o->h / (c * c * kPi);
@@ -94,11 +93,11 @@ void plan_from_tol(const double L[3], double Q, double xi, double E, se1p_tol_pl
   // of each set binds: k3 = 2 pi/L3 for the I planes, 2 pi (n_l+1)/L3 for the J planes.
   const double budget = std::max(0.0, std::log(std::sqrt(Q) / EF));
   const double dI = budget * L3 / (2.0 * kPi), dJ = dI / (o->n_local + 1);
-  o->s_l = std::max({1.0, std::log(1.0 / EF) / (2.0 * kPi), (L[0] + dI) / (o->Mt * o->h)});   // (choose_sl) P:697
+  o->s_l = std::max({1.0, std::log(1.0 / EF) / (2.0 * kPi), (Lsq + dI) / (o->Mt * o->h)});   // (choose_sl) P:697
   o->SI = (int)std::ceil(o->s_l * o->Mt - 1e-9);
   o->s0 = 1.0 + std::sqrt(2.0);
   o->S0 = (int)std::ceil(o->s0 * o->Mt - 1e-9);
-  o->Ntilde = next_friendly(std::max(o->Mt, (int)std::ceil((L[0] + dJ) / o->h - 1e-9)));
+  o->Ntilde = next_friendly(std::max(o->Mt, (int)std::ceil((Lsq + dJ) / o->h - 1e-9)));
   o->est_real = std::sqrt(Q * o->rc / (2.0 * V)) / (xi * o->rc * xi * o->rc) * std::exp(-xi * xi * o->rc * o->rc);
   const double ki = M / 2.0;   // the grid resolves |k3| <= 2 pi (M/2)/L3
   o->est_fourier = xi / (kPi * kPi) * std::pow(ki, -1.5) * std::sqrt(Q) * std::exp(-std::pow(kPi * ki / (xi * L3), 2));

@@ -87,6 +87,33 @@ def test_full_potential_vs_exact_oracle(cfg):
     assert oracle.rel_rms(phi, ref) <= 1e-9
 
 
+@pytest.mark.parametrize("L", [(1.0, 0.625, 1.0), (0.5, 1.0, 1.0)])
+def test_rectangular_cross_section(L):
+    """L1 != L2 runs on the square embedding [0, max(L1,L2))^2 (reading R-19): element-wise equal
+    to Alg. 1 on the square box for the same particles, and the full potential matches the exact
+    sum, which does not depend on L1, L2 (Eq. (2))."""
+    x, q = make_system(120, L, 21)
+    Lsq = (1.0, 1.0, 1.0)
+    ref = sd.se1p_kspace(x, q, Lsq, 4.0, 16, 16, 2, 110, 64, 32)
+    got = _gpu_kspace(x, q, L, 4.0, 16, 16, 2, 110, 64, 32)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+    xd, qd = _dev(x, q)
+    phi = (se1p.kspace(xd, qd, L, 4.0, 16, 16, n_local=2, S0=110, SI=64, Ntilde=32)
+           + se1p.real(xd, qd, L, 4.0, 1.158)).cpu().numpy()
+    assert oracle.rel_rms(phi, oracle.phi_exact(x, q, L)) <= 1e-9
+    assert np.max(np.abs(oracle.phi_exact(x, q, L) - oracle.phi_exact(x, q, Lsq))) <= 1e-12 * np.max(np.abs(phi))
+    # a particle outside the user's box (inside the square) is still refused
+    xb = x.copy()
+    xb[5, 0 if L[0] < L[1] else 1] = 0.9
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace(torch.from_numpy(xb).cuda(), qd, L, 4.0, 16, 16)
+    assert e.value.code == 2
+    # SE3P keeps the square requirement (its cross-section is periodic)
+    with pytest.raises(se1p.SE1PError) as e:
+        se1p.kspace3p(xd, qd, L, 4.0, 16, 8)
+    assert e.value.code == 4
+
+
 def test_real_space_vs_oracle():
     for L, xi, rc, N, seed in [((1, 1, 1), 4.0, 1.158, 100, 1), ((1, 1, 1), 8.0, 0.594, 500, 2),
                                ((1, 1, 2), 12.0, 0.401, 800, 3), ((2, 2, 2), 30.0, 0.1, 3000, 5),

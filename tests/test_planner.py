@@ -70,9 +70,11 @@ def test_lambert_region_and_errors():
         with pytest.raises(se1p.SE1PError) as e:
             se1p.plan_from_tol(*args)
         assert e.value.code == 1
-    with pytest.raises(se1p.SE1PError) as e:
-        se1p.plan_from_tol((1.0, 2.0, 1.0), 1.0, 4.0, 1e-6)   # non-square cross-section
-    assert e.value.code == 4
+    # rectangular cross-section: planned on the square [0, max(L1, L2))^2 (reading R-19)
+    r = se1p.plan_from_tol((1.0, 2.0, 1.0), 1.0, 4.0, 1e-6)
+    s = se1p.plan_from_tol((2.0, 2.0, 1.0), 1.0, 4.0, 1e-6)
+    assert r["Mfree"] == round(2.0 / r["h"]) and r["Mt"] == r["Mfree"] + r["P"]
+    assert (r["M"], r["P"], r["Mfree"], r["Ntilde"]) == (s["M"], s["P"], s["Mfree"], s["Ntilde"])
 
 
 # (L, N, normalise Q to 1, xi, tol): the paper's Table 1 systems and unit boxes
