@@ -31,6 +31,7 @@
 #ifndef SE1P_H
 #define SE1P_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -251,6 +252,17 @@ int se1p_debug_copy(int which, double* host_dst, int64_t count);
 
 /* Free all plans and workspaces of the current device. */
 void se1p_release(void);
+
+/* Device-memory hook (SURVEY.md 8(b) "Ownership": the Python layer routes the library's memory
+   to torch's caching allocator).  Every plan, workspace and table the library allocates from now
+   on comes from alloc(bytes, ctx) (must return device memory of the current device, >= 256-byte
+   aligned, or NULL -> SE1P_ENOMEM) and goes back through release(ptr, ctx).  Before a pointer is
+   released the library synchronises the device, so the hook may reuse it at once.  The call
+   first frees everything allocated so far (se1p_release, through the allocator that made it),
+   then installs the hook; alloc = release = NULL restores cudaMalloc / cudaFree.  Not to be
+   called while another thread is inside the library.  Returns SE1P_OK, or SE1P_EINVAL if
+   exactly one of alloc, release is NULL (nothing changes then). */
+int se1p_set_allocator(void* (*alloc)(size_t bytes, void* ctx), void (*release)(void* ptr, void* ctx), void* ctx);
 
 const char* se1p_last_error(void);
 const char* se1p_version(void);

@@ -26,7 +26,7 @@ EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_p
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
            "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol",
-           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex"]
+           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex", "se1p_set_allocator"]
 
 
 class SE1PError(RuntimeError):
@@ -90,6 +90,8 @@ def load(build_if_needed: bool = True):
     lib.se1p_version.restype = ctypes.c_char_p
     lib.se1p_debug_copy.argtypes = [i32, vp, i64]
     lib.se1p_debug_copy.restype = i32
+    lib.se1p_set_allocator.argtypes = [vp, vp, vp]
+    lib.se1p_set_allocator.restype = i32
     ip = ctypes.POINTER(ctypes.c_int)
     lib.se1p_kspace_slab_forward.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32,
                                              i32, i32, ip, vp]
@@ -392,6 +394,40 @@ def debug_stage(x, q, L, xi, M, P, stage, **kw):
 
 def release():
     load().se1p_release()
+
+
+_ALLOC_T = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_RELEASE_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+_allocator_refs = None   # the installed callbacks (kept alive while the library may call them)
+
+
+def _torch_alloc(nbytes, _ctx):
+    try:
+        import torch
+        return torch.cuda.caching_allocator_alloc(int(nbytes))
+    except Exception:   # noqa: BLE001 -- NULL tells the library (SE1P_ENOMEM)
+        return None
+
+
+def _torch_release(ptr, _ctx):
+    import torch
+    torch.cuda.caching_allocator_delete(int(ptr))
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device memory (plans, workspaces, tables) through torch's caching
+    allocator (include/se1p.h se1p_set_allocator; SURVEY.md 8(b) "Ownership"), or back to
+    cudaMalloc with enable=False.  Frees everything the library holds first."""
+    global _allocator_refs
+    lib = load()
+    if enable:
+        refs = (_ALLOC_T(_torch_alloc), _RELEASE_T(_torch_release))
+        _check(lib.se1p_set_allocator(ctypes.cast(refs[0], ctypes.c_void_p), ctypes.cast(refs[1], ctypes.c_void_p),
+                                      None))
+        _allocator_refs = refs
+    else:
+        _check(lib.se1p_set_allocator(None, None, None))
+        _allocator_refs = None
 
 
 def version():

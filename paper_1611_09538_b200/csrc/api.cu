@@ -52,17 +52,46 @@ static DevState& dev_state() {
 
 static uint64_t g_ws_generation = 1;   // bumped on every workspace reallocation (graphs bake pointers)
 
+// se1p_set_allocator hook (null: cudaMalloc / cudaFree)
+static void* (*g_alloc_fn)(size_t, void*) = nullptr;
+static void (*g_release_fn)(void*, void*) = nullptr;
+static void* g_alloc_ctx = nullptr;
+
+void* dev_alloc(size_t bytes) {
+  bytes = std::max<size_t>(bytes, 8);
+  void* p = nullptr;
+  if (g_alloc_fn) {
+    p = g_alloc_fn(bytes, g_alloc_ctx);
+    if (!p) throw Error{5, "allocator hook returned null (" + std::to_string(bytes) + " bytes)"};
+    return p;
+  }
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{5, "cudaMalloc failed (" + std::to_string(bytes) + " bytes)"};
+  }
+  return p;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  if (g_release_fn) {
+    // the hook's memory may be handed out again at once: no library kernel may still use it
+    // (cudaFree synchronises implicitly; frees are rare -- growth, eviction, release)
+    cudaDeviceSynchronize();
+    g_release_fn(p, g_alloc_ctx);
+    return;
+  }
+  cudaFree(p);
+}
+
 template <typename T>
 static void grow(T*& p, int64_t& cap, int64_t need) {
   if (need <= cap) return;
   ++g_ws_generation;
-  if (p) cudaFree(p);
+  dev_free(p);
   p = nullptr;
   cap = 0;
-  if (cudaMalloc(&p, sizeof(T) * (size_t)std::max<int64_t>(need, 1)) != cudaSuccess) {
-    cudaGetLastError();
-    throw Error{5, "cudaMalloc failed (" + std::to_string(sizeof(T) * need) + " bytes)"};
-  }
+  dev_alloc(p, (size_t)std::max<int64_t>(need, 1));
   cap = need;
 }
 
@@ -855,7 +884,8 @@ void se1p_release(void) {
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
                   (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap, (void*)w.grid3, (void*)ds.sel,
                   (void*)ds.idmap, (void*)ds.xsel})
-    if (p) cudaFree(p);
+    dev_free(p);
+  real_release_tables(d);
   if (w.side) cudaStreamDestroy(w.side);
   if (w.ev_fork) cudaEventDestroy(w.ev_fork);
   if (w.ev_join) cudaEventDestroy(w.ev_join);
@@ -865,6 +895,19 @@ void se1p_release(void) {
   for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);   // they bake the freed pointers
   g_graphs.clear();
   ++g_ws_generation;
+}
+
+int se1p_set_allocator(void* (*alloc)(size_t, void*), void (*release)(void*, void*), void* ctx) {
+  if ((alloc == nullptr) != (release == nullptr)) {
+    g_err = "se1p_set_allocator: alloc and release must both be set or both be null";
+    return 1;
+  }
+  se1p_release();   // everything allocated so far goes back through the allocator that made it
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_alloc_fn = alloc;
+  g_release_fn = release;
+  g_alloc_ctx = ctx;
+  return 0;
 }
 
 const char* se1p_last_error(void) { return g_err.c_str(); }

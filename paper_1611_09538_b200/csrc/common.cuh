@@ -39,6 +39,13 @@ struct Error {
 
 void count_launch();
 
+// Device memory of the library (workspaces, plans, tables): cudaMalloc/cudaFree, or the hook
+// installed by se1p_set_allocator (include/se1p.h).  dev_alloc throws Error{5} on failure.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+template <typename T>
+inline void dev_alloc(T*& p, size_t count) { p = static_cast<T*>(dev_alloc(sizeof(T) * count)); }
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

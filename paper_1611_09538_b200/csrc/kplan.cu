@@ -71,7 +71,7 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
     throw Error{4, "FFT extent has a prime factor > 61"};
   // descriptor offsets (twoff/rootoff) index the combined table directly
   pl->twz = pl->twJ = pl->twK = 0;
-  SE1P_CUDA_TRY(cudaMalloc(&pl->d_tw, sizeof(double2) * tw.size()));
+  dev_alloc(pl->d_tw, tw.size());
   SE1P_CUDA_TRY(cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
 
   const double h = dv.h, xi = p.xi, eta = p.eta, L3 = p.L[2];
@@ -97,9 +97,9 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
                                 std::exp(-(1.0 - eta) * k3 * k3 / (4.0 * xi * xi)),
                             k3 * k3);
     }
-    SE1P_CUDA_TRY(cudaMalloc(&pl->d_exJ, sizeof(double) * SJ));
-    SE1P_CUDA_TRY(cudaMalloc(&pl->d_k2J, sizeof(double) * SJ));
-    SE1P_CUDA_TRY(cudaMalloc(&pl->d_pl, sizeof(double2) * pl->n_planes));
+    dev_alloc(pl->d_exJ, SJ);
+    dev_alloc(pl->d_k2J, SJ);
+    dev_alloc(pl->d_pl, 2 * (size_t)pl->n_planes);   // (e^{...} C_J, k3^2) pairs
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_exJ, ex.data(), sizeof(double) * SJ, cudaMemcpyHostToDevice));
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_k2J, k2.data(), sizeof(double) * SJ, cudaMemcpyHostToDevice));
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_pl, plv.data(), sizeof(double2) * pl->n_planes, cudaMemcpyHostToDevice));
@@ -109,14 +109,14 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   {
     std::vector<double> f1(p.P);
     for (int t = 0; t < p.P; ++t) f1[t] = std::exp(-dv.alpha * h * h * (double)t * (double)t);
-    SE1P_CUDA_TRY(cudaMalloc(&pl->d_f1, sizeof(double) * p.P));
+    dev_alloc(pl->d_f1, p.P);
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_f1, f1.data(), sizeof(double) * p.P, cudaMemcpyHostToDevice));
   }
 
   // kernel planes: k3 = 0 (extent S0) and 0 < k3 <= 2 pi n_l/L3 (extent SI)
   {
     const int LK = pl->LK;
-    SE1P_CUDA_TRY(cudaMalloc(&pl->d_khat, sizeof(double) * (size_t)pl->n_kernel * LK * LK));
+    dev_alloc(pl->d_khat, (size_t)pl->n_kernel * LK * LK);
     const double scale = pl->const_gather / ((double)p.M * (double)LK * (double)LK);
     for (int n = 0; n < pl->n_kernel; ++n) {
       const int S = (n == 0) ? p.S0 : ((size_t)(n - 1) < p.SIn.size() ? p.SIn[n - 1] : p.SI);
@@ -132,10 +132,10 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
           sig[(size_t)m2 * H + m1] = v;
         }
       double* d_sig = nullptr;
-      SE1P_CUDA_TRY(cudaMalloc(&d_sig, sizeof(double) * sig.size()));
+      dev_alloc(d_sig, sig.size());
       SE1P_CUDA_TRY(cudaMemcpy(d_sig, sig.data(), sizeof(double) * sig.size(), cudaMemcpyHostToDevice));
       build_kernel_spectrum(*pl, S, d_sig, pl->d_khat + (size_t)n * LK * LK, scale, st);
-      cudaFree(d_sig);
+      dev_free(d_sig);
     }
   }
   pl->t_off_total = (int64_t)pl->n_kernel * Mt * pl->LK + (int64_t)(pl->n_planes - pl->n_kernel) * Mt * p.SJ;
@@ -151,12 +151,12 @@ KPlan* kplan_get(const KParams& p, cudaStream_t st) {
   ++g_plan_generation;
   if (g_plans.size() >= 16) {
     KPlan* old = g_plans.front().get();
-    cudaFree(old->d_tw);
-    cudaFree(old->d_khat);
-    cudaFree(old->d_exJ);
-    cudaFree(old->d_k2J);
-    cudaFree(old->d_pl);
-    cudaFree(old->d_f1);
+    dev_free(old->d_tw);
+    dev_free(old->d_khat);
+    dev_free(old->d_exJ);
+    dev_free(old->d_k2J);
+    dev_free(old->d_pl);
+    dev_free(old->d_f1);
     g_plans.erase(g_plans.begin());
   }
   return build(p, st);
@@ -165,12 +165,12 @@ KPlan* kplan_get(const KParams& p, cudaStream_t st) {
 void kplan_release_all() {
   ++g_plan_generation;
   for (auto& q : g_plans) {
-    cudaFree(q->d_tw);
-    cudaFree(q->d_khat);
-    cudaFree(q->d_exJ);
-    cudaFree(q->d_k2J);
-    cudaFree(q->d_pl);
-    cudaFree(q->d_f1);
+    dev_free(q->d_tw);
+    dev_free(q->d_khat);
+    dev_free(q->d_exJ);
+    dev_free(q->d_k2J);
+    dev_free(q->d_pl);
+    dev_free(q->d_f1);
   }
   g_plans.clear();
 }

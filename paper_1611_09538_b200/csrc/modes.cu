@@ -423,9 +423,9 @@ void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* 
   const int Mt = pl.dv.Mt, LK = pl.LK, H = S / 2 + 1;
   double* tmp = nullptr;
   double2 *A = nullptr, *B = nullptr;
-  SE1P_CUDA_TRY(cudaMalloc(&tmp, sizeof(double) * (size_t)Mt * H));
-  SE1P_CUDA_TRY(cudaMalloc(&A, sizeof(double2) * (size_t)LK * LK));
-  SE1P_CUDA_TRY(cudaMalloc(&B, sizeof(double2) * (size_t)LK * LK));
+  dev_alloc(tmp, (size_t)Mt * H);
+  dev_alloc(A, (size_t)LK * LK);
+  dev_alloc(B, (size_t)LK * LK);
   SE1P_CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * (size_t)LK * LK, st));
   k_kern_a<<<(unsigned)ceil_div((int64_t)Mt * H, 128), 128, 0, st>>>(S, Mt, d_sig, tmp);
   SE1P_LAUNCH_CHECK();
@@ -445,9 +445,9 @@ void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* 
   k_transpose_scale_real<<<(unsigned)ceil_div((int64_t)LK * LK, 256), 256, 0, st>>>(LK, scale, B, khat_out);
   SE1P_LAUNCH_CHECK();
   SE1P_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFree(tmp);
-  cudaFree(A);
-  cudaFree(B);
+  dev_free(tmp);
+  dev_free(A);
+  dev_free(B);
 }
 
 }  // namespace se1p

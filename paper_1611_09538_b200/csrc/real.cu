@@ -181,6 +181,12 @@ struct TabCache {
 };
 static TabCache g_tab[64];
 
+void real_release_tables(int dev) {
+  TabCache& tc = g_tab[dev & 63];
+  if (tc.dev) dev_free(tc.dev);
+  tc = TabCache{};
+}
+
 void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out) {
   RDev d = d0;
@@ -191,7 +197,7 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     TabCache& tc = g_tab[dev & 63];
     if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
       const std::vector<double> t = erfc_table(d.xi, d.rc);
-      if (!tc.dev) SE1P_CUDA_TRY(cudaMalloc(&tc.dev, sizeof(double) * t.size()));
+      if (!tc.dev) dev_alloc(tc.dev, t.size());
       SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
       SE1P_CUDA_TRY(cudaStreamSynchronize(st));
       tc.xi = d.xi;

@@ -23,5 +23,6 @@ constexpr int kTabN = 256, kTabDeg = 10;
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out = nullptr);
+void real_release_tables(int dev);   // the cached erfc table of device dev
 
 }  // namespace se1p

@@ -62,3 +62,14 @@ def test_no_cpu_fallback_without_library(tmp_path, monkeypatch):
     with pytest.raises(ImportError):
         se1p.load(build_if_needed=False)
     importlib.reload(se1p)
+
+
+def test_set_allocator_rejects_half_a_hook():
+    """se1p_set_allocator (include/se1p.h): exactly one of alloc/release null -> SE1P_EINVAL,
+    checked before any device work (so it runs without a GPU)."""
+    import ctypes
+    import paper_1611_09538_b200 as se1p
+    lib = se1p.load()
+    cb = se1p._ALLOC_T(lambda n, c: None)
+    assert lib.se1p_set_allocator(ctypes.cast(cb, ctypes.c_void_p), None, None) == 1
+    assert b"both" in lib.se1p_last_error()
