@@ -390,14 +390,14 @@ auto reduce = [&](int b, int rt) {
     auto reduce_batch = [&](int j) {
       const int bj = j % NB;
       mbar_wait(&empty[bj], (unsigned)((j / NB) & 1));
-      reduce(bj, tid - (kCW + 1) * 32);
+      if (!(dv.dbg & 4)) reduce(bj, tid - (kCW + 1) * 32);
       __syncwarp();
       if (lane == 0) mbar_arrive(&freeb[bj]);
     };
     for (int b = 0, ph = 0, j = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0), ++j) {
       mbar_wait(&rawb[b], (unsigned)ph);
       const int cn = cnt[b];
-      if (cn > 0 && kind < NSEG) {
+      if (cn > 0 && kind < NSEG && !((dv.dbg & 8) && kind > 0)) {
         const double* rb = raws + b * BM * kRec;
         double* eb = exps + b * ES;
         for (int p = 8 * ew + (lane >> 2); p < cn; p += 8 * kEW) {
@@ -593,15 +593,17 @@ auto reduce = [&](int b, int rt) {
       if (lane == 0 && bprev >= 0) mbar_arrive(&empty[bprev]);
       bprev = b;
     }
-  } else
+  } else {
+  // Gather, batches in order.  As in gridding, list entries left over after the last full k-step
+  // of a batch are carried into the next batch's list (an entry names its buffer: p | zmask << 8
+  // | buffer << 16), so k-steps are padded only at the end of the tile; a batch is released
+  // (empty -> the expanders reduce it) once no carried entry refers to it.
+  int held = 0, bprev = -1;
   for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
     mbar_wait(&full[b], (unsigned)ph);
     const int cn = cnt[b];
-    if (cn < 0) break;
-    const double* rb = raws + b * BM * kRec;
-    const double* eb = exps + b * ES;
     // particles of the batch meeting this warp's 4 x 4 column block (order preserving)
-    int n = 0;
+    int n = held;
     // z blocks of KZ nodes: a 24-node window meets 6-7 4-node, 3-4 8-node or 2-3 16-node blocks
     // (89%, 77%, 60% of the issued work inside the stencil); measured, the instruction count binds,
     // not the DMMA work: at C5 KZ = 4 / 16 are 34% / 14% slower than 8 for the potential; the
@@ -610,15 +612,26 @@ auto reduce = [&](int b, int rt) {
       const int p = p0 + lane;
       const int r = p < cn ? relm[b * BM + p] : 0;   // expander-computed relevance
       const bool rel = (r >> w) & 1;
-      const int e = p | ((r >> 16) << 8);
+      const int e = p | ((r >> 16) << 8) | (b << 16);
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
       if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = e;
       n += __popc(bal);
     }
-    if (lane == 0 && n > BM) atomicOr(dv.err, 2);   // bounds check: list capacity BM + 32
-    const int npad = (n + 15) & ~15;
-    if (lane < npad - n) wl[n + lane] = dummy;
+    if (lane == 0 && n > BM + 16) atomicOr(dv.err, 2);   // bounds check: list capacity BM + 32
     __syncwarp();
+    int npad = n & ~15;
+    if (cn < 0 || npad < held) {   // the end, or fewer than 16 with carried ones: flush all (padded)
+      npad = (n + 15) & ~15;
+      if (lane < npad - n) wl[n + lane] = dummy;
+      __syncwarp();
+    }
+    // the carried entries (< 16) all sit in the first k-step: the previous batch is released
+    // right after it (at once if nothing was carried), so the ring keeps its prefetch depth
+    bool pend = bprev >= 0;
+    if (pend && held == 0) {
+      if (lane == 0) mbar_arrive(&empty[bprev]);
+      pend = false;
+    }
 
     if (dv.dbg & 2) {
     } else {
@@ -631,8 +644,9 @@ auto reduce = [&](int b, int rt) {
         zm |= __shfl_xor_sync(0xffffffffu, zm, 4);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 8);
         zm |= __shfl_xor_sync(0xffffffffu, zm, 16);
-        const double* r0 = eb + (e0 & 0xff) * RSE;
-        const double* r1 = eb + (e1 & 0xff) * RSE;
+        const int b0 = (e0 >> 16) & 7, b1 = (e1 >> 16) & 7;
+        const double* r0 = exps + b0 * ES + (e0 & 0xff) * RSE;
+        const double* r1 = exps + b1 * ES + (e1 & 0xff) * RSE;
         const double* z0 = r0 + tig;
         const double* z1 = r1 + tig;
         double t0[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
@@ -712,7 +726,7 @@ auto reduce = [&](int b, int rt) {
           }
           if (FM == 3) {
             const int ph = (h ? e1 : e0) & 0xff;
-            const double* rr = rb + (ph < BM ? ph : 0) * kRec;
+            const double* rr = raws + ((h ? b1 : b0) * BM + (ph < BM ? ph : 0)) * kRec;
             const double px = rr[10], py = rr[11];
             const double nx0 = ((double)(X0 + cx0) - 0.5 * P) * dv.h - px, ny0 = ((double)(Y0 + cy0) - 0.5 * P) * dv.h - py;
             const double ta = 2.0 * dv.alpha;
@@ -738,15 +752,32 @@ auto reduce = [&](int b, int rt) {
           const int pa = e0 & 0xff, pb = e1 & 0xff;
 #pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
-            if (pa < BM) acc[((b * BM + pa) * (kCW + 1) + w) * NC + cc] = v[0][cc];
-            if (pb < BM) acc[((b * BM + pb) * (kCW + 1) + w) * NC + cc] = v[1][cc];
+            if (pa < BM) acc[((b0 * BM + pa) * (kCW + 1) + w) * NC + cc] = v[0][cc];
+            if (pb < BM) acc[((b1 * BM + pb) * (kCW + 1) + w) * NC + cc] = v[1][cc];
           }
+        }
+        if (pend) {
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[bprev]);
+          pend = false;
         }
       }
       __threadfence_block();
     }
+    if (pend) {   // (debug mode: no k-steps ran)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[bprev]);
+    }
+    const int rest = n > npad ? n - npad : 0;   // carry the rest (all from this batch)
+    const int mv = lane < rest ? wl[npad + lane] : 0;
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
+    if (lane < rest) wl[lane] = mv;
+    __syncwarp();
+    held = rest;
+    if (cn < 0) break;
+    bprev = b;
+  }
   }
 
   if (!GATHER) {
