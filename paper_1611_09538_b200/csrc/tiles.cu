@@ -359,7 +359,7 @@ auto reduce = [&](int b, int rt) {
         if (!have) acquire();
         const int blo = k * BM, bhi = blo + BM;
         const int lo = max(rlo, blo), hi = min(rhi, bhi);
-        if (hi > lo) {
+        if (hi > lo && !(dv.dbg & 16)) {
           const unsigned bytes = (unsigned)((hi - lo) * kRec * 8);
           mbar_expect_tx(&rawb[b], bytes);
           bulk_g2s(raws + (b * BM + (lo - blo)) * kRec, A.rec + (int64_t)(sC + (lo - rlo)) * kRec, bytes, &rawb[b]);
