@@ -142,9 +142,43 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
       : "memory");
   return ok != 0;
 }
+// SE1P_MBAR_WAIT: 0 try_wait (the hardware may suspend the warp until the phase flips),
+// 1 test_wait spin (no suspension), 2 try_wait with a suspend-time hint (ns)
+#ifndef SE1P_MBAR_WAIT
+#define SE1P_MBAR_WAIT 0
+#endif
+#ifndef SE1P_MBAR_HINT_NS
+#define SE1P_MBAR_HINT_NS 64
+#endif
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "n"(SE1P_MBAR_HINT_NS)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+#if SE1P_MBAR_WAIT == 1
+  while (!mbar_test_wait(b, parity)) {
+  }
+#elif SE1P_MBAR_WAIT == 2
+  while (!mbar_try_wait_hint(b, parity)) {
+  }
+#else
   while (!mbar_try_wait(b, parity)) {
   }
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -251,7 +285,6 @@ __global__ void __launch_bounds__(n_threads(FM), 1) k_tiles(const TileArgs A) {
     for (int k = tid; k < NB * BM * (kCW + 1) * NC; k += kThreads) acc[k] = 0.0;
   __syncthreads();
 
-  const int nslot = dv.nslot;
 // gather: sum the per-warp partials of batch buffer b into the particles' slots (expander warps)
 auto reduce = [&](int b, int rt) {
     const int c = cnt[b];
