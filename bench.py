@@ -319,7 +319,7 @@ def bench_reference(args, cfg, rank, world=1):
     sample = f"{m} seeded targets per step of {cfg.name} (exact Ewald1P, all {cfg.N} sources)"
     return {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "particles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded uniform neutral charges, se1p_synth.py)",
             "config": {"workload": f"{cfg.name}: N={cfg.N} L={list(cfg.L)} xi={cfg.xi} M={cfg.M} P={cfg.P} "
                                    f"(the exact Ewald1P potential of the same system, on {cores} host cores)",
