@@ -111,7 +111,7 @@ def _check(code):
 
 
 def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0,
-          reference_kernels=False, graph=False):
+          graph=False):
     o = Opts()
     o.Ntilde = int(Ntilde or 0)
     o.S0 = int(S0 or 0)
@@ -121,7 +121,6 @@ def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=
     o.sync = int(bool(sync))
     o.reserved[0] = 1 if profile else 0
     o.reserved[1] = int(stop_after)
-    o.reserved[2] = 1 if reference_kernels else 0
     o.reserved[3] = 1 if graph else 0
     return o
 
@@ -186,26 +185,25 @@ def _outputs(x, N, field, out, field_out):
 
 def kspace(x, q, L, xi, M, P, eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None,
            out=None, stream=None, sync=True, skip_checks=False, profile=False, stop_after=0,
-           reference_kernels=False, field=False, field_out=None, graph=False, S_modes=None):
+           field=False, field_out=None, graph=False, S_modes=None):
     """phi^F = phi^{F,k3!=0} + phi^{F,k3=0} at every particle (Alg. 1).
     field=True returns (phi^F, E^F) with E^F = -grad phi^F, [N,3] (forces q E).
     graph=True captures the device stages as a CUDA graph on the first call and replays it on later
     calls with the same parameters and buffers (pass `out`/`field_out` to keep the buffers fixed).
     S_modes: multi-tier upsampling, padded extent of modes |k3| = 2 pi n/L3, n = 1..n_local
-    (needs n_local; potential only).
-    reference_kernels=True selects the simple v1 gridding/gather kernels (A/B testing)."""
+    (needs n_local; potential only)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
     if S_modes is not None:
         if field or n_local is None or len(S_modes) != int(n_local):
             raise ValueError("S_modes needs n_local = len(S_modes) and the potential (field=False)")
-        o = _opts(Ntilde, S0, None, host, skip_checks, sync, profile, stop_after, reference_kernels, graph)
+        o = _opts(Ntilde, S0, None, host, skip_checks, sync, profile, stop_after, graph)
         tiers = (ctypes.c_int * len(S_modes))(*[int(s) for s in S_modes])
         _check(lib.se1p_kspace_tiers_ex(ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
                                         int(M), int(P), _neg(eta, 0.0), _neg(s0), int(n_local), tiers, optr))
         return out
-    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, reference_kernels, graph)
+    o = _opts(Ntilde, S0, SI, host, skip_checks, sync, profile, stop_after, graph)
     side = None
     if graph and not host and stream is None:
         import torch

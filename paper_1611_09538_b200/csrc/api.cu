@@ -109,6 +109,14 @@ static void ensure_particles(KWork& w, int64_t N, int nbins) {
   }
 }
 
+// gather partial slots, records and the sweep kernels' overhang buffer and item table
+static void ensure_sweep(KWork& w, const KDev& dv, int64_t N, int nvals) {
+  grow(w.gpart, w.gpart_cap, N * gather_slots(dv) * nvals);
+  grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
+  grow(w.over, w.over_cap, sweep_overhang_doubles(dv));
+  grow(w.items, w.items_cap, sweep_items_max(dv));
+}
+
 // ------------------------------------------------------------------ input checks
 __global__ void k_check(const double* __restrict__ x, const double* __restrict__ q, int64_t N, double L0, double L1,
                         double* __restrict__ red, int* __restrict__ flag) {
@@ -355,15 +363,11 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   StageTimer tm(o && o->reserved[0] == 1, st);
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   const int stop = o ? o->reserved[1] : 0;
-  const bool v1 = o && o->reserved[2] == 1;   // reference (v1) gridding/gather kernels
-  if (field && v1) throw Error{1, "the field is computed by the tile kernels only"};
-  if (!v1) {
-    grow(w.gpart, w.gpart_cap, N * gather_slots(dv) * (field ? 4 : 1));
-    grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
-  }
+  if (o && o->reserved[2]) throw Error{1, "opts->reserved[2] is unused and must be 0"};
+  ensure_sweep(w, dv, N, field ? 4 : 1);
   const bool graph = o && o->reserved[3] == 1;
-  if (graph && (host_io || v1 || stop || tm.on))
-    throw Error{1, "graph mode takes device pointers and no profiling / reference kernels / early stop"};
+  if (graph && (host_io || stop || tm.on))
+    throw Error{1, "graph mode takes device pointers and no profiling / early stop"};
   if (graph) {
     run_graphed(prm, N, dx, dq, dphi, dfield, st, [&] {
       k_bin_particles(*pl, w, dx, dq, N, st);
@@ -373,7 +377,6 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
       k_zfft_forward(*pl, w, w.planes, Lg, nullptr, st);
       k_mode_stage(*pl, w, w.planes, Lg, nullptr, nullptr, 0, nullptr, nullptr, 0, st);
       k_zfft_inverse(*pl, w, w.planes, Lg, nullptr, st);
-      if (field) k_records_stage(*pl, w, N, st, true);
       k_gather_tiles(*pl, w, N, st, 0, -1, field);
       k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
     });
@@ -383,10 +386,9 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   tm.mark();
   k_bin_particles(*pl, w, dx, dq, N, st);
   tm.mark();
-  if (!v1) k_records_stage(*pl, w, N, st);
+  k_records_stage(*pl, w, N, st);
   tm.mark();
-  if (v1) k_spread(*pl, w, N, st);
-  else k_spread_tiles(*pl, w, N, st);
+  k_spread_tiles(*pl, w, N, st);
   tm.mark();
   if (stop == 1) return sync_and_check(st);
   const SlabLayout L1 = single_layout(dv.Mt, pl->n_planes);
@@ -399,13 +401,9 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   k_zfft_inverse(*pl, w, w.planes, L1, nullptr, st);
   tm.mark();
   if (stop == 4) return sync_and_check(st);
-  if (v1) k_gather(*pl, w, N, dphi, st);
-  else {
-    if (field) k_records_stage(*pl, w, N, st, true);   // field records add the position
-    k_gather_tiles(*pl, w, N, st, 0, -1, field);
-  }
+  k_gather_tiles(*pl, w, N, st, 0, -1, field);
   tm.mark();
-  if (!v1) k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
+  k_gather_finish_stage(*pl, w, N, dphi, st, 0, -1, dfield);
   tm.mark();
   }
   if (host_io && phi_out) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
@@ -451,8 +449,7 @@ static void kspace3p_impl(const se1p_opts* o, cudaStream_t st, const double* x, 
   grow(w.grid3, w.grid3_cap, (int64_t)Mf * Mf * dv.M);
   grow(w.planes, w.planes_cap, (int64_t)p3->n_planes * Mf * Mf);
   grow(w.T, w.T_cap, p3->t_off_total);
-  grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
-  grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
+  ensure_sweep(w, dv, N, 1);
   const bool host_io = o && o->host_io;
   const double *dx = x, *dq = q;
   double* dphi = phi_out;
@@ -583,8 +580,7 @@ static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double*
   const KDev& dv = pl->dv;
   ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
   grow(w.grid, w.grid_cap, (int64_t)dv.Mt * dv.Mt * dv.M);
-  grow(w.gpart, w.gpart_cap, N * gather_slots(dv));
-  grow(w.rec, w.cap_rec, N * (int64_t)rec_doubles(dv.P));
+  ensure_sweep(w, dv, N, 1);
   if (!(o && o->skip_checks)) check_inputs(w, x, q, N, L, true, st);
   SE1P_CUDA_TRY(cudaMemsetAsync(w.flag + 1, 0, sizeof(int), st));
   // only the particles whose stencils meet the slab's tiles are binned and gridded (the rest
@@ -862,11 +858,6 @@ int se1p_debug_copy(int which, double* host_dst, int64_t count) {
     } else if (which == 1) {
       if (count > 2 * w.planes_cap) throw Error{1, "plane buffer smaller than requested"};
       SE1P_CUDA_TRY(cudaMemcpy(host_dst, w.planes, sizeof(double) * count, cudaMemcpyDeviceToHost));
-    } else if (which == 2) {
-      if (count > 32 || !w.prof) throw Error{1, "no phase counters (run with profiling counters on)"};
-      unsigned long long h[32];
-      SE1P_CUDA_TRY(cudaMemcpy(h, w.prof, sizeof h, cudaMemcpyDeviceToHost));
-      for (int64_t i = 0; i < count; ++i) host_dst[i] = (double)h[i];
     } else {
       throw Error{1, "unknown buffer"};
     }
@@ -883,7 +874,7 @@ void se1p_release(void) {
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
                   (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap, (void*)w.grid3, (void*)ds.sel,
-                  (void*)ds.idmap, (void*)ds.xsel})
+                  (void*)ds.idmap, (void*)ds.xsel, (void*)w.over, (void*)w.items})
     dev_free(p);
   real_release_tables(d);
   if (w.side) cudaStreamDestroy(w.side);

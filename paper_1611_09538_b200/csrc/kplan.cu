@@ -56,11 +56,6 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   dv.alpha = 2.0 * p.xi * p.xi / p.eta;
   dv.L3 = p.L[2];
   dv.nbx = (int)ceil_div(dv.Mfree, kBin);
-  dv.nby = (int)ceil_div(dv.Mfree, kBin);
-  dv.nbz = (int)ceil_div(p.M, kTZ);
-  dv.ntx = (int)ceil_div(dv.Mt, kTX);
-  dv.nty = (int)ceil_div(dv.Mt, kTY);
-  dv.ntz = (int)ceil_div(p.M, kTZ);
   const int Mt = dv.Mt;
   pl->n_planes = p.M / 2 + 1;
   pl->n_kernel = std::max(0, std::min(p.n_l + 1, pl->n_planes));

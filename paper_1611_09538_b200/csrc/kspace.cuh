@@ -7,9 +7,7 @@
 
 namespace se1p {
 
-// Tile of the v1 (reference) gridding kernel on the extended grid (free x, free y, periodic z).
-constexpr int kTX = 8, kTY = 8, kTZ = 16;
-// Particle bins: xy columns of kBin x kBin cells, z-sorted by cell inside a column.
+// Particle bins: x bands of kBin cells; inside a band by periodic stencil start, then y cell.
 constexpr int kBin = 4;
 
 // Layout of a k3-plane buffer: rows x in [xlo[0], xlo[nslab]) split into
@@ -59,12 +57,8 @@ struct KDev {
   int M, P, Mfree, Mt;          // grid: Mt x Mt (free, extended) x M (periodic)
   double h, inv_h, alpha;       // alpha = 2 xi^2 / eta (window exponent)
   double L3;
-  int nbx, nby, nbz;            // bins: xy columns of kBin x kBin cells (nbz: v1 z-chunks of kTZ)
-  int ntx, nty, ntz;            // tiles over the Mt x Mt x M grid (v1 kernels)
-  int nty2;                     // 16-wide tiles of the DMMA kernels
+  int nbx;                      // bins: x bands of kBin cells
   int nsxy, nsz, nslot;         // gather partial slots per particle
-  unsigned long long* prof;     // optional phase counters of the tile kernels (nullptr = off)
-  int dbg;                      // debug experiment bits of the tile kernels (0 = normal)
   int* err;                     // device error word of the tile kernels (bounds checks)
   int64_t N;
 };
@@ -107,10 +101,12 @@ struct KWork {                  // per-N workspace (grown on demand)
   double2* planes = nullptr;    // Hk: n_planes x Mt x Mt
   double2* T = nullptr;         // 2D pass workspace
   int64_t grid_cap = 0, planes_cap = 0, T_cap = 0;
-  unsigned long long* prof = nullptr;   // 32 phase counters of the tile kernels (debug)
-  bool prof_on = false;
-  double* gpart = nullptr;      // gather partials [N][nslot]
+  double* gpart = nullptr;      // gather partials [slot][value][N]
   int64_t gpart_cap = 0;
+  double* over = nullptr;       // gridding overhang [chunk][Mt][Mt][P-1] (sweep.cu)
+  int64_t over_cap = 0;
+  int* items = nullptr;         // sweep work items + work counter
+  int64_t items_cap = 0;
   double* red = nullptr;        // reductions (neutrality check)
   int* flag = nullptr;
   double* host_x = nullptr;     // staging for host_io
@@ -132,9 +128,8 @@ void k_bin_particles(const KPlan& pl, KWork& w, const double* x, const double* q
 void k_slab_select(const KPlan& pl, const double* x, const double* q, int64_t N, int row_lo, int row_hi, int* flags,
                    int* pos, int* scan_scratch, double* xc, double* qc, int* idmap, cudaStream_t st);
 void k_scatter_partial_stage(const double* phic, const int* idmap, int64_t n, double* phi, cudaStream_t st);
-void k_spread(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st);          // v1 (reference kernels)
-void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field = false);   // tiles.cu
-// DMMA tile kernels over x tiles [tx_lo, tx_hi) (tx_hi < 0: all), tiles of 16 grid rows
+void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field = false);   // sweep.cu
+// z-aligned DMMA column sweeps over x tiles [tx_lo, tx_hi) (tx_hi < 0: all), tiles of 16 grid rows
 void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1);
 // field: also E = -grad phi (3 doubles per particle, user order) -- the gradient of the gather
 void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo = 0, int tx_hi = -1,
@@ -143,14 +138,14 @@ void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi_out
                            int tx_hi = -1, double* field = nullptr);
 int64_t gather_slots(const KDev& dv);
 void slot_geometry(KDev& dv);
-int tile_tz(int M);
+int64_t sweep_overhang_doubles(const KDev& dv);
+int64_t sweep_items_max(const KDev& dv);
 void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
                     cudaStream_t st);
 void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* glK, const int* liK,
                   int nK, const int* glJ, const int* liJ, int nJ, cudaStream_t st);
 void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
                     cudaStream_t st);
-void k_gather(const KPlan& pl, KWork& w, int64_t N, double* phi_out, cudaStream_t st);
 // SE3P (se3p.cu): fold the extended grid of the 1P tile plan onto the periodic grid and back
 void k_fold_3p(const KPlan& ext, const double* grid_ext, double* grid_per, cudaStream_t st);
 void k_unfold_3p(const KPlan& ext, const double* grid_per, double* grid_ext, cudaStream_t st);

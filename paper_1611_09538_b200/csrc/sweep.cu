@@ -1,0 +1,969 @@
+// sweep.cu -- gridding (Alg. 1 step 2, Eq. (spread_1p)) and gather (Alg. 1 step 6,
+// Eq. (se1p_complete_discretized)) as z-aligned column sweeps on the FP64 tensor
+// pipe (mma.sync m16n8k8 f64 -> SASS DMMA; tcgen05.mma has no f64 kind).  See tiles.cuh.
+//
+// Work item = (16 x 16 column tile of the extended free grid, chunk [Z0, Z0+Ck) of the periodic
+// axis).  Persistent CTAs fetch items heavy-first from a work counter.  Inside an item the CTA
+// sweeps the stencil-start layers a = Z0 .. Z0+Ck-1 in order.  A "group" is the set of candidate
+// particles whose periodic stencil starts at node a (bins: x band, a, y cell, so a group is one
+// contiguous run of the sorted order per x band).  Every particle of a group has its P z-weights
+// on the SAME nodes a .. a+P-1, so in the frame of the group the z-window is dense:
+//   gridding  C[16 cols x 8 z] += A[16 cols x 8 particles] B[8 particles x 8 z]   per 8-node block
+//             A = (q wx) wy, B = wz (relative to a): no z block is partly outside the stencil,
+//   gather    T[16 cols x 8 particles] += H~[16 cols x 8 z] wz^T[8 z x 8 particles],
+//             phi_p += sum_cols wx wy T.
+// The z window depends on the particle only, so k_records stores it with the particle's record
+// (Fast Gaussian Gridding factors, for the free axes).  Roles (21 warps):
+//   producer (1 warp): fetches items, walks their groups (one candidate run per x band: bin_start)
+//     and cuts them into batches of <= BM candidates, whose records (with the z windows) it moves
+//     into a ring of NB shared-memory slots with bulk copies (cp.async.bulk, SASS UBLKCP;
+//     completion by transaction bytes on the slot's mbarrier).
+//   expanders (4 warps): per candidate the tile's x and y windows from the FGG factors -- the
+//     record holds per free axis A = e^{-alpha d0^2}, E = e^{-2 alpha h d0} (node t weighs
+//     A E^t f1[t]) with E^-1 and E^8 for short power trees -- and the 16-bit mask of consumer
+//     warps whose 4 x 4 column block the stencil meets; then `full`.  Gather: they also sum the
+//     consumers' per-warp partials of finished batches into the particle's slot (fixed order).
+//   consumers (16 warps): warp w owns the 4 x 4 column block (w & 3, w >> 2) of the tile; per
+//     batch it lists (ballot) the candidates meeting it and runs 8-particle k-steps.  Entries left
+//     over (< 8) are carried into the next batch of the same group; a group's last batch pads.
+//     Gridding accumulates each group's frame (16 cols x 8 NZB nodes) in a per-warp ring of
+//     positions in shared memory (load frame, k-steps, store frame); position u is complete once
+//     group u is done, and completed 8-position blocks are written to the grid.  The P-1 positions
+//     past the chunk end go to an overhang buffer that k_overhang adds to the next chunk.
+// No floating-point atomics: each grid point is written by one warp; the gather's partials go
+// to fixed slots summed in a fixed order (k_gather_finish) -> bitwise reproducible.
+#include <cstdint>
+#include <vector>
+
+#include "tiles.cuh"
+
+namespace se1p {
+
+constexpr int kCW = 16;                 // consumer warps (16 blocks of 4 x 4 columns)
+constexpr int kEG = 2;                  // expander groups (alternate batches)
+constexpr int kGW = 4;                  // warps per expander group
+constexpr int kSW = kEG * kGW;          // expander warps
+constexpr int kSweepThreads = (kCW + 1 + kSW) * 32;
+constexpr int kMaxNB = 4;
+// batch ring depth (shared-memory slots): even, so that a row slot is always reused by the
+// expander group that filled it
+constexpr int kNB = 4;
+constexpr int kMaxP = 64;
+
+// header flags of a batch
+constexpr int kFirst = 1, kLast = 2, kItemEnd = 4, kKernelEnd = 8;
+
+__host__ __device__ constexpr int sw_nzb(int P) { return P <= 16 ? 2 : (P <= 24 ? 3 : (P <= 32 ? 4 : 8)); }
+// record (k_records): {jx0, jy0}, q, x: A E E^-1 E^8, y: A E E^-1 E^8, d0 x y z, sorted index, pad,
+// then the z window wz[0 .. 8 NZB) (zero past P); stride = 8 (mod 16) doubles so that the
+// consumers' loads of 4 or 8 records spread over the banks
+constexpr int kRq = 1, kRx = 2, kRy = 6, kRd = 10, kRi = 13, kRz = 16;
+__host__ __device__ constexpr int rec_stride(int NZB) { return kRz + 8 * NZB + ((NZB & 1) ? 0 : 8); }
+// rows: x[0:16) y[0:16) (XOR-swizzled, see xy_key), then the z window (copied from the record);
+// stride 8 (mod 16) doubles
+constexpr int kZ = 32;
+__host__ __device__ constexpr int row_stride(int NZB) { return kZ + 8 * NZB + ((NZB & 1) ? 0 : 8); }
+constexpr int kNR = 2;   // record ring depth (batches): released once expanded
+// gridding ring: R positions (>= 8 NZB + 8), column stride S = 4 (mod 16) doubles
+__host__ __device__ constexpr int sw_R(int NZB) { return 8 * NZB + 8; }
+__host__ __device__ constexpr int sw_S(int NZB) { return sw_R(NZB) + ((4 - sw_R(NZB)) % 16 + 16) % 16; }
+__host__ __device__ constexpr int sw_nc(int FM) { return FM == 1 ? 3 : 1; }   // gather outputs per pass
+// node i (0..15) of free axis ax of the row of ring slot e sits at 16 ax + 8 (i >> 3) + ((i & 7) ^ key),
+// key = ((e >> 1) & 3) | (ax << 2): the 2 axes of 8 consecutive candidates, stored by one half-warp
+// (row stride 8 mod 16, BM a multiple of 8), then hit 16 distinct bank pairs
+__host__ __device__ __forceinline__ int xy_key(int e, int ax) { return ((e >> 1) & 3) | (ax << 2); }
+
+struct SweepArgs {
+  KDev dv;
+  const double* rec;
+  const int* bin_start;
+  const double* f1;
+  double* grid;       // gridding: H (written); gather: H~ (read)
+  double* over;       // gridding: overhang [nzc][Mt][Mt][P-1]
+  double* gpart;      // gather partials [slot][value][N]
+  const int* items;   // packed items (tx | ty << 10 | zc << 20), heavy first
+  int* counter;       // work counter (zeroed by k_items)
+  int n_items, C, nzc, BM, NB;
+};
+
+struct SweepSmem {
+  int off_meta, off_lists, off_raw, off_rows, off_acc, off_ring, total;
+};
+
+// barriers: full, empty, (unused) [kMaxNB], rawb, rawfree [kNR]; headers hdr [kMaxNB], bhdr [kNR]
+constexpr int kSmemHead = (3 * kMaxNB + 2 * kNR) * 8 + (kMaxNB + kNR) * 16;
+
+__host__ __device__ inline SweepSmem sweep_smem(int BM, int NB, int NZB, bool gather, int FM) {
+  SweepSmem s;
+  int o = kSmemHead + kMaxP * 8;                              // + f1
+  o = (o + 15) & ~15;
+  s.off_meta = o;
+  o += (NB * BM + 1) * 16;
+  s.off_lists = o;
+  o += kCW * (BM + 24) * 4;
+  o = (o + 127) & ~127;
+  s.off_raw = o;
+  o += kNR * BM * rec_stride(NZB) * 8;
+  s.off_rows = o;
+  o += (NB * BM + 1) * row_stride(NZB) * 8;
+  s.off_acc = o;
+  if (gather) o += (NB * BM + 1) * kCW * sw_nc(FM) * 8;
+  o = (o + 127) & ~127;
+  s.off_ring = o;
+  if (!gather) o += kCW * 16 * sw_S(NZB) * 8;
+  s.total = o;
+  return s;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// consumers' waits for a batch: try_wait with a suspend-time hint (ns; 0: the hardware default), so
+// waiting warps leave the issue slots to the expanders
+#ifndef SE1P_SWEEP_WAIT_NS
+#define SE1P_SWEEP_WAIT_NS 0
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "n"(SE1P_SWEEP_WAIT_NS > 0 ? SE1P_SWEEP_WAIT_NS : 1)
+      : "memory");
+  return ok != 0;
+}
+// SE1P_SWEEP_WATCHDOG (debug builds): report and trap a wait that never completes
+#ifndef SE1P_SWEEP_WATCHDOG
+#define SE1P_SWEEP_WATCHDOG 0
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, int tag = 0) {
+#if SE1P_SWEEP_WATCHDOG
+  const long long t0 = clock64();
+  while (!mbar_try_wait(b, parity)) {
+    if (clock64() - t0 > 4000000000ll) {
+      printf("sweep watchdog: block %d warp %d tag %d parity %u\n", blockIdx.x, threadIdx.x >> 5, tag, parity);
+      __trap();
+    }
+  }
+#else
+  (void)tag;
+  while (!mbar_try_wait(b, parity)) {
+  }
+#endif
+}
+
+template <bool GATHER, int FM, int NZB>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
+  constexpr int RD = rec_stride(NZB), RS = row_stride(NZB), R = sw_R(NZB), S = sw_S(NZB);
+  constexpr int NC = sw_nc(FM);                   // values this pass writes per particle
+  constexpr int NCT = FM ? 4 : 1;                 // values per gather slot
+  constexpr int COFF = FM == 2 ? 3 : 0;           // first slot value of this pass
+  constexpr int ACS = kCW * NC;                   // acc doubles per candidate
+  extern __shared__ __align__(128) unsigned char smem[];
+  const KDev& dv = A.dv;
+  const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
+  const SweepSmem L = sweep_smem(BM, NB, NZB, GATHER, FM);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxNB;
+  uint64_t* rawb = empty + kMaxNB + kMaxNB;
+  uint64_t* rawfree = rawb + kNR;
+  int4* hdr = reinterpret_cast<int4*>(rawfree + kNR);
+  int4* bhdr = hdr + kMaxNB;
+  double* f1 = reinterpret_cast<double*>(smem + kSmemHead);
+  int4* meta = reinterpret_cast<int4*>(smem + L.off_meta);
+  int* lists = reinterpret_cast<int*>(smem + L.off_lists);
+  double* raw = reinterpret_cast<double*>(smem + L.off_raw);
+  double* rows = reinterpret_cast<double*>(smem + L.off_rows);
+  double* acc = reinterpret_cast<double*>(smem + L.off_acc);
+  double* ring = reinterpret_cast<double*>(smem + L.off_ring);
+  const int dummy = NB * BM;   // the all-zero slot
+
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int b = 0; b < kMaxNB; ++b) {
+      mbar_init(&full[b], kGW);
+      mbar_init(&empty[b], kCW);
+    }
+    for (int r = 0; r < kNR; ++r) {
+      mbar_init(&rawb[r], 1);
+      mbar_init(&rawfree[r], kGW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = tid; k < kMaxP; k += kSweepThreads) f1[k] = k < P ? A.f1[k] : 0.0;
+  for (int k = tid; k < RS; k += kSweepThreads) rows[dummy * RS + k] = 0.0;
+  if (tid < 4) reinterpret_cast<int*>(&meta[dummy])[tid] = 0;
+  if (!GATHER)
+    for (int k = tid; k < kCW * 16 * S; k += kSweepThreads) ring[k] = 0.0;
+  __syncthreads();
+
+  auto item_geom = [&](int it, int& X0, int& Y0, int& Z0, int& Ck, int& zc) {
+    const int pk = A.items[it];
+    const int tx = pk & 1023, ty = (pk >> 10) & 1023;
+    zc = pk >> 20;
+    X0 = tx * kTXY;
+    Y0 = ty * kTXY;
+    Z0 = zc * A.C;
+    Ck = min(A.C, M - Z0);
+  };
+
+  if (w == kCW) {
+    // ================================================================ producer
+    int k = 0;   // batch sequence number
+    auto acquire = [&](int b) {   // record slot b free: its previous batch expanded
+      if (k >= kNR) mbar_wait(&rawfree[b], (unsigned)(((k - kNR) / kNR) & 1), 100 + k);
+    };
+    auto post = [&](int b, int4 h) {   // after every lane's copies: header, then the arrival
+      __syncwarp();
+      if (lane == 0) {
+        bhdr[b] = h;
+        mbar_arrive(&rawb[b]);
+      }
+      __syncwarp();
+      ++k;
+    };
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(A.counter, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= A.n_items) {   // one end marker per expander group
+        for (int gq = 0; gq < kEG; ++gq) {
+          const int b = k % kNR;
+          acquire(b);
+          post(b, make_int4(-1, gq, 0, kKernelEnd));
+        }
+        break;
+      }
+      int X0, Y0, Z0, Ck, zc;
+      item_geom(it, X0, Y0, Z0, Ck, zc);
+      // candidate runs of layer a: x bands covering cells [X0 - P, X0 + 14], y cells [cy0, cy1]
+      const int b0 = max(0, fdiv(X0 - P, kBin)), b1 = min(dv.nbx - 1, fdiv(X0 + kTXY - 2, kBin));
+      const int cy0 = max(0, Y0 - P), cy1 = min(dv.Mfree - 1, Y0 + kTXY - 2);
+      const int nruns = (cy1 >= cy0) ? max(0, b1 - b0 + 1) : 0;
+      // run bounds of layer u + 1 are loaded while layer u's batches are issued
+      auto load_runs = [&](int u, int& s0, int& e0) {
+        s0 = e0 = 0;
+        if (u < Ck && lane < nruns) {
+          const int row = ((b0 + lane) * M + Z0 + u) * dv.Mfree;
+          s0 = __ldg(A.bin_start + row + cy0);
+          e0 = __ldg(A.bin_start + row + cy1 + 1);
+        }
+      };
+      int sN, eN;
+      load_runs(0, sN, eN);
+      for (int u = 0; u < Ck; ++u) {
+        const int s0 = sN, len = eN - sN;
+        load_runs(u + 1, sN, eN);
+        if (len < 0 || s0 < 0 || (int64_t)s0 + len > dv.N) atomicOr(dv.err, 1);
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int pre = incl - len;
+        for (int lo = 0; lo < tot; lo += BM) {
+          const int b = k % kNR;
+          acquire(b);
+          const int cnt = min(BM, tot - lo);
+          const int a0 = max(pre, lo), a1 = min(pre + len, lo + cnt);
+          if (a1 > a0) {
+            const unsigned bytes = (unsigned)((a1 - a0) * RD * 8);
+            mbar_expect_tx(&rawb[b], bytes);
+            bulk_g2s(raw + ((int64_t)b * BM + (a0 - lo)) * RD, A.rec + ((int64_t)s0 + (a0 - pre)) * RD, bytes,
+                     &rawb[b]);
+          }
+          post(b, make_int4(it, u, cnt, (lo == 0 ? kFirst : 0) | (lo + BM >= tot ? kLast : 0)));
+        }
+      }
+      const int b = k % kNR;
+      acquire(b);
+      post(b, make_int4(it, Ck, 0, kItemEnd));
+    }
+    return;
+  }
+
+  if (w > kCW) {
+    // ================================================================ expanders
+    // group gi expands batches k = gi, gi + kEG, ...; record slot k % kNR = gi; with kNB even the
+    // row slot k % kNB returns to the same group, which first reduces (gather) its previous batch
+    const int ew = w - kCW - 1, gi = ew / kGW, gw = ew % kGW, gl = gw * 32 + lane;
+    // gather: sum batch j's per-warp partials into the slots (fixed warp order)
+    auto reduce_batch = [&](int j) {
+      const int bj = j % NB;
+      mbar_wait(&empty[bj], (unsigned)((j / NB) & 1), 200000 + j);
+      const int4 h = hdr[bj];
+      if (h.z > 0) {
+        int X0, Y0, Z0, Ck, zc;
+        item_geom(h.x, X0, Y0, Z0, Ck, zc);
+        const int tx = X0 / kTXY, ty = Y0 / kTXY;
+        for (int p = gl; p < h.z; p += kGW * 32) {
+          const int4 m = meta[bj * BM + p];
+          if (m.x == 0) continue;
+          const double* ap = acc + (int64_t)(bj * BM + p) * ACS;
+          double sm[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sm[c] = 0.0;
+          for (int v = 0; v < kCW; ++v)
+            if ((m.x >> v) & 1)
+#pragma unroll
+              for (int c = 0; c < NC; ++c) sm[c] += ap[v * NC + c];
+          if (FM == 1) {   // column moments -> d/dx, d/dy: 2 alpha (h S + delta phi), delta = d0 + (X0 - j0) h
+            const double* rr = A.rec + (int64_t)m.w * RD;
+            const double ta = 2.0 * dv.alpha;
+            const double dx = rr[kRd] + (double)(X0 - m.y) * dv.h, dy = rr[kRd + 1] + (double)(Y0 - m.z) * dv.h;
+            sm[1] = ta * fma(dv.h, sm[1], dx * sm[0]);
+            sm[2] = ta * fma(dv.h, sm[2], dy * sm[0]);
+          }
+          const int sx = tx - fdiv(m.y, kTXY), sy = ty - fdiv(m.z, kTXY);
+          if (sx < 0 || sx >= dv.nsxy || sy < 0 || sy >= dv.nsxy || m.w < 0 || m.w >= dv.N) atomicOr(dv.err, 4);
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            A.gpart[(int64_t)((sx * dv.nsxy + sy) * NCT + COFF + c) * dv.N + m.w] = sm[c];
+        }
+      }
+    };
+    for (int k = gi;; k += kEG) {
+      const int b = k % NB, r = k % kNR;
+      mbar_wait(&rawb[r], (unsigned)((k / kNR) & 1), 300000 + k);
+      const int4 h = bhdr[r];
+      if (h.w & kKernelEnd) {   // drain this group's unreduced batches; end marker 0 goes to the consumers
+        if (GATHER)
+          for (int j = max(gi, k - NB); j < k; j += kEG) reduce_batch(j);
+        else if (k >= NB)
+          mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1), 600000 + k);
+        if (h.y == 0) {
+          if (gw == 0 && lane == 0) hdr[b] = h;
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[b]);
+        }
+        break;
+      }
+      if (k >= NB) {
+        if (GATHER) reduce_batch(k - NB);
+        else mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1), 600000 + k);
+      }
+      if (h.z > 0) {
+        int X0, Y0, Z0, Ck, zc;
+        item_geom(h.x, X0, Y0, Z0, Ck, zc);
+        // tasks: 2 per candidate (the tile's 16 x nodes, 16 y nodes)
+        for (int t = gl; t < h.z * 2; t += kGW * 32) {
+          const int cand = t >> 1, ax = t & 1, e = b * BM + cand;
+          const double* rr = raw + (int64_t)(r * BM + cand) * RD;
+          const int2 jj = *reinterpret_cast<const int2*>(rr);
+          // v[i] = A E^(t0+i) f1[t0+i] on the stencil nodes 0 <= t0+i < P, else 0, as base E^i with
+          // base = A E^t0 from a power tree (short dependency chains: the FP64 pipe is shared with
+          // the consumers' DMMAs); nodes 8..15 from base E^8
+          const double* ra = rr + (ax == 0 ? kRx : kRy);
+          const int t0 = ax == 0 ? X0 - jj.x : Y0 - jj.y;
+          const double E = ra[1], E8 = ra[3];
+          const bool neg = t0 < 0;
+          const int n = min(neg ? -t0 : t0, 63);
+          const double b1 = neg ? ra[2] : E;
+          const double b2 = b1 * b1, b4 = b2 * b2;
+          const double e8 = neg ? b4 * b4 : E8, e16 = e8 * e8, e32 = e16 * e16;
+          const double f01 = ((n & 1) ? b1 : 1.0) * ((n & 2) ? b2 : 1.0);
+          const double f23 = ((n & 4) ? b4 : 1.0) * ((n & 8) ? e8 : 1.0);
+          const double a0 = (!GATHER && ax == 0) ? ra[0] * rr[kRq] : ra[0];   // gridding: q folded into wx
+          const double base = (a0 * (((n & 16) ? e16 : 1.0) * ((n & 32) ? e32 : 1.0))) * (f01 * f23);
+          const double base8 = base * E8;
+          const double E2 = neg ? E * E : b2, E4 = neg ? E2 * E2 : b4;
+          const double E3 = E2 * E;
+          const double pw[8] = {1.0, E, E2, E3, E4, E4 * E, E4 * E2, E4 * E3};
+          double* o = rows + (int64_t)e * RS + 16 * ax;
+          const int key = xy_key(e, ax);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int tt = t0 + q;
+            o[8 * (q >> 3) + ((q & 7) ^ key)] = (tt >= 0 && tt < P) ? ((q < 8 ? base : base8) * f1[tt]) * pw[q & 7] : 0.0;
+          }
+          if (ax == 0) {
+            // consumer warps whose 4 x 4 block the stencil meets
+            const int bx0 = max(fdiv(jj.x - X0, 4), 0), bx1 = min(fdiv(jj.x - X0 + P - 1, 4), 3);
+            const int by0 = max(fdiv(jj.y - Y0, 4), 0), by1 = min(fdiv(jj.y - Y0 + P - 1, 4), 3);
+            int wm = 0;
+            if (bx0 <= bx1 && by0 <= by1) {
+              const int xb = ((1 << (bx1 + 1)) - 1) & ~((1 << bx0) - 1);
+              for (int by = by0; by <= by1; ++by) wm |= xb << (4 * by);
+            }
+            meta[e] = make_int4(wm, jj.x, jj.y, (int)__double_as_longlong(rr[kRi]));
+          }
+          // the z window: 16-byte chunks ax, ax + 2, ..., rotated by 3 steps for every other pair of
+          // candidates (conflict-free 16-byte stores)
+          const double2* zs = reinterpret_cast<const double2*>(rr + kRz);
+          double2* zd = reinterpret_cast<double2*>(rows + (int64_t)e * RS + kZ);
+          const int nz2 = 2 * NZB, rot = ((cand >> 1) & 1) * 3;
+#pragma unroll
+          for (int i = 0; i < nz2; ++i) {
+            int i2 = i + rot;
+            if (i2 >= nz2) i2 -= nz2;
+            zd[2 * i2 + ax] = zs[2 * i2 + ax];
+          }
+        }
+      }
+      if (gw == 0 && lane == 0) hdr[b] = h;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&rawfree[r]);
+        mbar_arrive(&full[b]);
+      }
+    }
+    return;
+  }
+
+  // ================================================================== consumers
+  const int g = lane >> 2, tg = lane & 3;
+  const int bxw = w & 3, byw = w >> 2;
+  const int xa = 4 * bxw + (g >> 2), yb = 4 * byw + (g & 3);   // this lane's columns g, g+8 -> x xa, xa+2; y yb
+  // x/y row offsets before the row's swizzle bits (xy_key: (e >> 1) & 3, XORed into the node index)
+  const int oxa = xa, oxa2 = xa + 2, oyb = 16 + (yb ^ 4);
+  auto sw4 = [](int e) { return (e >> 1) & 3; };
+  // gridding: B lane g holds frame node sg = (g >> 1) + 4 (g & 1), so C lane tg holds nodes tg, tg + 4;
+  // gather: K index tg (tg + 4) of block j is node 2 tg (2 tg + 1): one 16-byte pair of the record
+  const int sg = (g >> 1) + 4 * (g & 1);
+  int* wl = lists + w * (BM + 24);
+  double* rg = ring + w * 16 * S;   // gridding ring [16 cols][S]
+
+  int cur = -1, X0 = 0, Y0 = 0, Z0 = 0, Ck = 0, zc = 0;
+  int u = 0, flushed = 0;
+  bool fr = false;   // frame loaded for group u
+  double c[NZB][4];  // gridding frame accumulators / gather frame operand H~[16 cols x 8 z]
+#pragma unroll
+  for (int j = 0; j < NZB; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0;
+
+  // gridding: ring position p -> slot p mod R; lane's frame value (j, v): col g + 8 (v >> 1),
+  // node u + 8 j + tg + 4 (v & 1)
+  auto frame_io = [&](bool store) {
+#pragma unroll
+    for (int j = 0; j < NZB; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int col = g + 8 * (v >> 1);
+        const int sl = (u + 8 * j + tg + 4 * (v & 1)) % R;
+        double* p = rg + col * S + sl;
+        if (store) *p = c[j][v];
+        else c[j][v] = *p;
+      }
+  };
+  // gridding: write positions [f, f + 8) of the warp's 16 columns (grid, or overhang past Ck), zero them
+  auto flush_block = [&](int f) {
+    const int col = lane >> 1, hh = lane & 1;
+    const int x = X0 + 4 * bxw + (col >> 2), y = Y0 + 4 * byw + (col & 3);
+    double* p = rg + col * S + (f % R) + 4 * hh;
+    const double2 v0 = *reinterpret_cast<double2*>(p), v1 = *reinterpret_cast<double2*>(p + 2);
+    *reinterpret_cast<double2*>(p) = make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(p + 2) = make_double2(0.0, 0.0);
+    if (x < Mt && y < Mt) {
+      const double vv[4] = {v0.x, v0.y, v1.x, v1.y};
+      const int p0 = f + 4 * hh;
+      if (p0 + 4 <= Ck) {
+        double* gp = A.grid + ((int64_t)x * Mt + y) * M + Z0 + p0;
+        *reinterpret_cast<double2*>(gp) = v0;
+        *reinterpret_cast<double2*>(gp + 2) = v1;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int pp = p0 + i;
+          if (pp < Ck) A.grid[((int64_t)x * Mt + y) * M + Z0 + pp] = vv[i];
+          else if (pp < Ck + P - 1)
+            A.over[(((int64_t)zc * Mt + x) * Mt + y) * (P - 1) + (pp - Ck)] = vv[i];
+        }
+      }
+    }
+  };
+  // gather: the frame operand A[j] = H~[cols g, g+8][nodes a + 8j + 2 tg (+1)]
+  auto frame_load_gather = [&]() {
+#pragma unroll
+    for (int j = 0; j < NZB; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int col = g + 8 * (v & 1);
+        const int x = X0 + 4 * bxw + (col >> 2), y = Y0 + 4 * byw + (col & 3);
+        int z = Z0 + u + 8 * j + 2 * tg + (v >> 1);
+        while (z >= M) z -= M;
+        c[j][v] = (x < Mt && y < Mt) ? __ldg(A.grid + ((int64_t)x * Mt + y) * M + z) : 0.0;
+      }
+  };
+
+  auto ksteps = [&](int k0, int k1) {
+    if (!GATHER) {
+      for (int k = k0; k < k1; k += 8) {
+        const int e0 = wl[k + tg], e1 = wl[k + tg + 4];
+        const double* r0 = rows + e0 * RS;
+        const double* r1 = rows + e1 * RS;
+        const int s0 = sw4(e0), s1 = sw4(e1);
+        const double y0 = r0[oyb ^ s0], y1 = r1[oyb ^ s1];
+        const double a[4] = {r0[oxa ^ s0] * y0, r0[oxa2 ^ s0] * y0, r1[oxa ^ s1] * y1, r1[oxa2 ^ s1] * y1};
+#pragma unroll
+        for (int j = 0; j < NZB; ++j) dmma_16x8x8(c[j], a, r0[kZ + 8 * j + sg], r1[kZ + 8 * j + sg]);
+      }
+    } else {
+      for (int k = k0; k < k1; k += 8) {
+        const int e = wl[k + g];
+        const double* z = rows + e * RS + kZ + 2 * tg;
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NZB; ++j) {
+          const double2 bb = *reinterpret_cast<const double2*>(z + 8 * j);
+          dmma_16x8x8(t, c[j], bb.x, bb.y);
+        }
+        // T[col g (+8)][particle 2tg (+1)]: phi_p += wy (wx T + wx' T')
+        const int ea = wl[k + 2 * tg], eb = wl[k + 2 * tg + 1];
+        const double* ra = rows + ea * RS;
+        const double* rb2 = rows + eb * RS;
+        const int sa = sw4(ea), sb = sw4(eb);
+        double va[NC], vb[NC];
+        {
+          const double wxa = ra[oxa ^ sa], wxa2 = ra[oxa2 ^ sa], wya = ra[oyb ^ sa];
+          const double wxb = rb2[oxa ^ sb], wxb2 = rb2[oxa2 ^ sb], wyb = rb2[oyb ^ sb];
+          va[0] = wya * fma(wxa, t[0], wxa2 * t[2]);
+          vb[0] = wyb * fma(wxb, t[1], wxb2 * t[3]);
+          if (FM == 1) {   // column moments in tile coordinates (x: xa, xa + 2; y: yb)
+            const double cx = (double)xa;
+            va[1] = wya * fma(cx * wxa, t[0], (cx + 2.0) * wxa2 * t[2]);
+            vb[1] = wyb * fma(cx * wxb, t[1], (cx + 2.0) * wxb2 * t[3]);
+            va[2] = (double)yb * va[0];
+            vb[2] = (double)yb * vb[0];
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            va[cc] += __shfl_xor_sync(0xffffffffu, va[cc], o);
+            vb[cc] += __shfl_xor_sync(0xffffffffu, vb[cc], o);
+          }
+        if (g == 0) {
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            acc[(int64_t)ea * ACS + w * NC + cc] = va[cc];
+            acc[(int64_t)eb * ACS + w * NC + cc] = vb[cc];
+          }
+        }
+      }
+    }
+  };
+
+  int held = 0, bprev = -1;
+  for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
+    if (SE1P_SWEEP_WAIT_NS > 0 && !SE1P_SWEEP_WATCHDOG) {
+      while (!mbar_try_wait_hint(&full[b], (unsigned)ph)) {
+      }
+    } else {
+      mbar_wait(&full[b], (unsigned)ph, 400000 + b);
+    }
+    const int4 h = hdr[b];
+    if (h.w & kKernelEnd) {
+      __syncwarp();
+      if (lane == 0) {
+        if (bprev >= 0) mbar_arrive(&empty[bprev]);
+        mbar_arrive(&empty[b]);
+      }
+      break;
+    }
+    if (h.x != cur) {
+      cur = h.x;
+      item_geom(cur, X0, Y0, Z0, Ck, zc);
+      flushed = 0;
+      fr = false;
+    }
+    if (h.w & kItemEnd) {
+      if (!GATHER) {
+        __syncwarp();
+        for (; flushed < Ck + P - 1; flushed += 8) flush_block(flushed);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (bprev >= 0) mbar_arrive(&empty[bprev]);
+        mbar_arrive(&empty[b]);
+      }
+      bprev = -1;
+      continue;
+    }
+    if (h.w & kFirst) {
+      u = h.y;
+      if (!GATHER) {
+        __syncwarp();
+        for (; flushed + 8 <= u; flushed += 8) flush_block(flushed);
+        __syncwarp();
+      }
+      fr = false;
+    }
+    // this warp's candidates of the batch (order preserving), after the carried ones
+    int n = held;
+    const int cn = h.z;
+    for (int p0 = 0; p0 < cn; p0 += 32) {
+      const int p = p0 + lane;
+      const bool rel = p < cn && ((meta[b * BM + p].x >> w) & 1);
+      const unsigned bal = __ballot_sync(0xffffffffu, rel);
+      if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = b * BM + p;
+      n += __popc(bal);
+    }
+    if (lane == 0 && n > BM + 8) atomicOr(dv.err, 2);
+    __syncwarp();
+    // k-steps of 8 entries; the group's last batch pads and runs everything, and so does a batch
+    // that cannot fill one k-step on top of carried entries (at most one batch is ever held)
+    int kend = n & ~7;
+    if ((h.w & kLast) || (held > 0 && kend == 0)) {
+      kend = (n + 7) & ~7;
+      if (lane < kend - n) wl[n + lane] = dummy;
+      __syncwarp();
+    }
+    if (kend > 0) {
+      if (!fr) {
+        if (GATHER) frame_load_gather();
+        else frame_io(false);
+        fr = true;
+      }
+      ksteps(0, 8);
+      if (bprev >= 0) {   // the carried entries (all in the first k-step) named batch bprev
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[bprev]);
+        bprev = -1;
+      }
+      ksteps(8, kend);
+    }
+    const int rest = max(n - kend, 0);   // < 8, all from this batch (none after padding)
+    const int mv = lane < rest ? wl[kend + lane] : 0;
+    __syncwarp();
+    if (lane < rest) wl[lane] = mv;
+    held = rest;
+    if (h.w & kLast) {
+      if (!GATHER && fr) {
+        __syncwarp();
+        frame_io(true);
+      }
+      fr = false;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (held == 0) {
+      if (lane == 0) mbar_arrive(&empty[b]);
+    } else {
+      bprev = b;
+    }
+  }
+}
+
+// Overhang: the P-1 positions past each chunk belong to the next chunk (periodic in z); every
+// position receives at most one overhang (chunks hold >= P-1 nodes), so the adds do not race.
+__global__ void k_overhang(const double* __restrict__ over, double* __restrict__ grid, int Mt, int M, int P, int C,
+                           int nzc, int x_lo, int x_hi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ncol = (int64_t)(x_hi - x_lo) * Mt;
+  if (i >= ncol * nzc) return;
+  const int zc = (int)(i / ncol);
+  const int64_t col = (int64_t)x_lo * Mt + (i - (int64_t)zc * ncol);
+  const int Z0 = zc * C, Ck = min(C, M - Z0);
+  const double* o = over + ((int64_t)zc * Mt * Mt + col) * (P - 1);
+  double* gcol = grid + col * M;
+  for (int t = 0; t < P - 1; ++t) {
+    int z = Z0 + Ck + t;
+    while (z >= M) z -= M;
+    gcol[z] += o[t];
+  }
+}
+
+// Items (tx | ty << 10 | zc << 20) ordered by candidate count, heaviest first (ties: index order).
+__global__ void k_items(int ntx, int tx_lo, int nty, int nzc, int Mfree, int P, int* __restrict__ items,
+                        int* __restrict__ counter) {
+  const int n = ntx * nty * nzc;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) counter[0] = 0;
+  if (i >= n) return;
+  auto wt = [&](int j) {
+    const int zc = j % nzc, t2 = j / nzc, ty = t2 % nty, tx = t2 / nty + tx_lo;
+    (void)zc;
+    const int X0 = tx * kTXY, Y0 = ty * kTXY;
+    const int wx = max(0, min(X0 + kTXY - 1, Mfree) - max(X0 - P + 1, 1) + 1);
+    const int wy = max(0, min(Y0 + kTXY - 1, Mfree) - max(Y0 - P + 1, 1) + 1);
+    return wx * wy;
+  };
+  const int wi = wt(i);
+  int rank = 0;
+  for (int j = 0; j < n; ++j) {
+    const int wj = wt(j);
+    rank += (wj > wi) || (wj == wi && j < i);
+  }
+  const int zc = i % nzc, t2 = i / nzc, ty = t2 % nty, tx = t2 / nty + tx_lo;
+  items[rank] = tx | (ty << 10) | (zc << 20);
+}
+
+// Records of the sorted particles, stride rec_stride(NZB): {jx0, jy0} (reading R-3),
+// q, per free axis the Fast Gaussian Gridding factors of the first stencil node offset d0,
+// A = e^{-alpha d0^2}, E = e^{-2 alpha h d0} (node t: A E^t f1[t]) with E^-1 and E^8 for the
+// sweeps' power trees, d0 per axis, the record's own sorted index, and the periodic-axis window
+// wz[t] = e^{-alpha (d0z + t h)^2} for t < P (zero up to 8 NZB).
+__global__ void __launch_bounds__(128) k_records(KDev dv, const double4* __restrict__ P4, const int4* __restrict__ S4,
+                                                int64_t N, int RD, double* __restrict__ rec) {
+  extern __shared__ double srec[];   // 128 records, written out by the block with coalesced stores
+  const int64_t i0 = (int64_t)blockIdx.x * 128, i = i0 + threadIdx.x;
+  const int nrec = (int)(N - i0 < 128 ? N - i0 : 128);
+  if (i < N) {
+    const double4 pp = P4[i];
+    const int4 s = S4[i];
+    const double P2 = 0.5 * dv.P;
+    const double d0[3] = {((double)s.x - P2) * dv.h - pp.x, ((double)s.y - P2) * dv.h - pp.y,
+                          (double)s.z * dv.h - pp.z};
+    const double ah = 2.0 * dv.alpha * dv.h;
+    double* r = srec + threadIdx.x * RD;
+    r[0] = __hiloint2double(s.y, s.x);
+    r[kRq] = pp.w;
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      double* ra = r + (ax == 0 ? kRx : kRy);
+      ra[0] = exp(-dv.alpha * d0[ax] * d0[ax]);
+      ra[1] = exp(-ah * d0[ax]);
+      ra[2] = exp(ah * d0[ax]);
+      ra[3] = exp(-8.0 * ah * d0[ax]);
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) r[kRd + ax] = d0[ax];
+    r[kRi] = __longlong_as_double((long long)i);   // the sorted index (gather slots)
+    r[kRi + 1] = r[kRi + 2] = 0.0;
+    // z window by the FGG recurrence: e^{-alpha (d0 + t h)^2} = A E^t f1[t], with
+    // E^t f1[t] = prod_{s<t} E e^{-alpha h^2 (2s+1)}
+    const double g2 = exp(-2.0 * dv.alpha * dv.h * dv.h);
+    double wv = exp(-dv.alpha * d0[2] * d0[2]), step = exp(-ah * d0[2]) * exp(-dv.alpha * dv.h * dv.h);
+    for (int t = 0; t < RD - kRz; ++t) {
+      r[kRz + t] = (t < dv.P) ? wv : 0.0;
+      wv *= step;
+      step *= g2;
+    }
+  }
+  __syncthreads();
+  const double2* src = reinterpret_cast<const double2*>(srec);
+  double2* dst = reinterpret_cast<double2*>(rec + i0 * RD);
+  for (int k = threadIdx.x; k < nrec * RD / 2; k += 128) dst[k] = src[k];
+}
+
+// The field's second gather pass: the z windows become 2 alpha (node - z_p) wz (d/dz_p of the
+// window, Eq. (force_se1p)), in place.
+__global__ void k_records_zderiv(KDev dv, int64_t N, int RD, double* __restrict__ rec) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double* r = rec + i * RD;
+  const double dz = r[kRd + 2], ta = 2.0 * dv.alpha;
+  for (int t = 0; t < RD - kRz; ++t) r[kRz + t] *= ta * fma((double)t, dv.h, dz);
+}
+
+// Sum the per-tile partials of every particle in a fixed order and scatter to user order.
+// Only x tiles in [txlo, txhi) are summed (one slab of the distributed path; all tiles otherwise).
+// FIELD: the slots hold (phi, dphi/dx, dphi/dy, dphi/dz); field = -grad phi (3 per particle).
+template <bool FIELD>
+__global__ void k_gather_finish(KDev dv, const int4* __restrict__ S4, const int* __restrict__ perm,
+                                const double* __restrict__ gpart, int64_t N, double* __restrict__ phi,
+                                double* __restrict__ field, int txlo, int txhi) {
+  constexpr int NC = FIELD ? 4 : 1;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  const int4 st = S4[p];
+  const int P = dv.P;
+  const int tx0 = fdiv(st.x, kTXY), ty0 = fdiv(st.y, kTXY);
+  const int nx = fdiv(st.x + P - 1, kTXY) - tx0 + 1;
+  const int ny = fdiv(st.y + P - 1, kTXY) - ty0 + 1;
+  // slot-major partials [slot][value][particle]: consecutive particles at consecutive addresses
+  const double* gq = gpart + p;
+  double s[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s[c] = 0.0;
+  for (int a = 0; a < nx; ++a) {
+    if (tx0 + a < txlo || tx0 + a >= txhi) continue;
+    for (int b = 0; b < ny; ++b)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) s[c] += gq[(int64_t)((a * dv.nsxy + b) * NC + c) * N];
+  }
+  const int64_t u = perm[p];
+  if (phi) phi[u] = s[0];
+  if (FIELD)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) field[3 * u + c] = -s[1 + c];
+}
+
+// ------------------------------------------------------------------ host side
+int rec_doubles(int P) { return rec_stride(sw_nzb(P)); }
+
+void slot_geometry(KDev& dv) {
+  dv.nsxy = (dv.P - 1 + kTXY - 1) / kTXY + 1;
+  dv.nsz = 1;
+  dv.nslot = dv.nsxy * dv.nsxy;
+}
+
+int64_t gather_slots(const KDev& dv) {
+  KDev d = dv;
+  slot_geometry(d);
+  return d.nslot;
+}
+
+// chunking of the periodic axis: enough items for ~4 per SM, chunks of >= max(P, 16) nodes,
+// multiples of 8 (the flush blocks)
+static void sweep_chunks(const KDev& dv, int ncol, int& C, int& nzc) {
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int M = dv.M, P = dv.P;
+  nzc = 1;
+  C = M;
+  for (int z = 2; z <= 64; ++z) {
+    if ((int64_t)ncol * nzc >= 4 * (int64_t)n_sm) break;
+    const int c = (int)ceil_div(ceil_div(M, z), 8) * 8;
+    if (c < std::max(P, 16)) break;
+    const int nz = (int)ceil_div(M, c);
+    if (M - (nz - 1) * c < P - 1) continue;   // the last chunk must hold an overhang
+    if (nz > nzc) {
+      nzc = nz;
+      C = c;
+    }
+  }
+}
+
+// the largest chunk count sweep_chunks can pick: chunks of >= max(P, 16) nodes
+static int64_t sweep_nzc_max(const KDev& dv) { return dv.M / std::max(dv.P, 16) + 1; }
+int64_t sweep_overhang_doubles(const KDev& dv) {
+  return sweep_nzc_max(dv) * dv.Mt * dv.Mt * std::max(dv.P - 1, 1);
+}
+int64_t sweep_items_max(const KDev& dv) {
+  const int64_t nt = ceil_div(dv.Mt, kTXY);
+  return nt * nt * sweep_nzc_max(dv) + 2;
+}
+
+void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool field) {
+  (void)field;
+  const int nz = sw_nzb(pl.dv.P);
+  const int RD = rec_stride(nz);
+  const size_t sm = 128 * RD * sizeof(double);
+  if (sm > 48 * 1024)
+    SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_records, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_records<<<(unsigned)ceil_div(N, 128), 128, sm, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, RD,
+                                                         w.rec);
+  SE1P_LAUNCH_CHECK();
+}
+
+template <bool GATHER, int FM, int NZB>
+static void launch_sweep_t(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
+  SweepArgs a;
+  a.dv = pl.dv;
+  KDev& dv = a.dv;
+  slot_geometry(dv);
+  dv.err = w.flag + 1;
+  dv.N = N;
+  const int nty = (int)ceil_div(dv.Mt, kTXY), ntx = tx_hi - tx_lo;
+  if (ntx <= 0) return;
+  sweep_chunks(dv, ntx * nty, a.C, a.nzc);
+  a.n_items = ntx * nty * a.nzc;
+  // item table (heavy first); k_items also zeroes the work counter
+  if (w.items_cap < a.n_items + 2) throw Error{6, "sweep item table not allocated"};
+  k_items<<<(unsigned)ceil_div(a.n_items, 128), 128, 0, st>>>(ntx, tx_lo, nty, a.nzc, dv.Mfree, dv.P, w.items,
+                                                              w.items + a.n_items);
+  SE1P_LAUNCH_CHECK();
+  a.items = w.items;
+  a.counter = w.items + a.n_items;
+  a.rec = w.rec;
+  a.bin_start = w.bin_start;
+  a.f1 = pl.d_f1;
+  a.grid = w.grid;
+  a.over = w.over;
+  a.gpart = GATHER ? w.gpart : nullptr;
+  int BM = 0, NB = 0;
+  const int limit = 227 * 1024 - 512;
+  for (int nb : {kNB, 2})
+    for (int bm = 128; bm >= 8 && !BM; bm -= 8)
+      if (sweep_smem(bm, nb, NZB, GATHER, FM).total <= limit) {
+        BM = bm;
+        NB = nb;
+      }
+  if (!BM) throw Error{4, "sweep kernels do not fit in shared memory"};
+  a.BM = BM;
+  a.NB = NB;
+  const size_t smem = (size_t)sweep_smem(BM, NB, NZB, GATHER, FM).total;
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_sweep<GATHER, FM, NZB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const unsigned nblk = (unsigned)std::min(a.n_items, n_sm);
+  k_sweep<GATHER, FM, NZB><<<nblk, kSweepThreads, smem, st>>>(a);
+  SE1P_LAUNCH_CHECK();
+  if (!GATHER && dv.P > 1) {
+    const int x_lo = tx_lo * kTXY, x_hi = std::min(tx_hi * kTXY, dv.Mt);
+    const int64_t n = (int64_t)a.nzc * (x_hi - x_lo) * dv.Mt;
+    k_overhang<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(w.over, w.grid, dv.Mt, dv.M, dv.P, a.C, a.nzc, x_lo, x_hi);
+    SE1P_LAUNCH_CHECK();
+  }
+}
+
+template <bool GATHER, int FM>
+static void launch_sweep(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int tx_hi, cudaStream_t st) {
+  if (pl.dv.P > kMaxP) throw Error{4, "P > 64 is not supported by the sweep kernels"};
+  if (tx_hi < 0) tx_hi = (int)ceil_div(pl.dv.Mt, kTXY);
+  switch (sw_nzb(pl.dv.P)) {
+    case 2: launch_sweep_t<GATHER, FM, 2>(pl, w, N, tx_lo, tx_hi, st); break;
+    case 3: launch_sweep_t<GATHER, FM, 3>(pl, w, N, tx_lo, tx_hi, st); break;
+    case 4: launch_sweep_t<GATHER, FM, 4>(pl, w, N, tx_lo, tx_hi, st); break;
+    default: launch_sweep_t<GATHER, FM, 8>(pl, w, N, tx_lo, tx_hi, st); break;
+  }
+}
+
+void k_spread_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi) {
+  launch_sweep<false, 0>(pl, w, N, tx_lo, tx_hi, st);
+}
+
+void k_gather_tiles(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, int tx_lo, int tx_hi, bool field) {
+  if (field) {
+    launch_sweep<true, 1>(pl, w, N, tx_lo, tx_hi, st);   // phi, d/dx, d/dy
+    k_records_zderiv<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(pl.dv, N, rec_stride(sw_nzb(pl.dv.P)), w.rec);
+    SE1P_LAUNCH_CHECK();
+    launch_sweep<true, 2>(pl, w, N, tx_lo, tx_hi, st);   // d/dz
+  } else {
+    launch_sweep<true, 0>(pl, w, N, tx_lo, tx_hi, st);
+  }
+}
+
+void k_gather_finish_stage(const KPlan& pl, KWork& w, int64_t N, double* phi, cudaStream_t st, int tx_lo, int tx_hi,
+                           double* field) {
+  KDev dv = pl.dv;
+  slot_geometry(dv);
+  if (tx_hi < 0) tx_hi = (int)ceil_div(dv.Mt, kTXY);
+  const unsigned nb = (unsigned)ceil_div(N, 256);
+  const int4* s4 = (const int4*)w.s4;
+  if (field) k_gather_finish<true><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+  else k_gather_finish<false><<<nb, 256, 0, st>>>(dv, s4, w.perm, w.gpart, N, phi, field, tx_lo, tx_hi);
+  SE1P_LAUNCH_CHECK();
+}
+
+}  // namespace se1p

@@ -15,7 +15,7 @@ namespace se1p {
 constexpr int kTXY = 16;        // CTA tile extent in x and y (grid nodes)
 constexpr int kBXY = 4;         // particle bins: xy columns of kBXY x kBXY cells, z-sorted inside
 
-// Doubles per particle weight row (tiles.cu, k_records).
+// Doubles per particle record (sweep.cu, k_records).
 int rec_doubles(int P);
 
 __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], double b0, double b1) {

@@ -137,5 +137,3 @@ def test_field_errors():
     rc = lib.se1p_kspace_field_ex(se1p.ctypes.addressof(o), None, xd.data_ptr(), qd.data_ptr(), 50, se1p._Larr(L),
                                   4.0, 16, 8, 0.0, -1.0, -1.0, -1, None, None)
     assert rc == 1
-    with pytest.raises(se1p.SE1PError):
-        se1p.kspace(xd, qd, L, 4.0, 16, 8, field=True, reference_kernels=True)

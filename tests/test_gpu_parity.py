@@ -195,16 +195,6 @@ def test_plan_info_defaults():
     assert abs(info["eta"] - 16 * 16.0 / 256 / (0.95 ** 2 * math.pi)) < 1e-15
 
 
-@pytest.mark.parametrize("case", CASES[:4], ids=[c[0] for c in CASES[:4]])
-def test_reference_kernels_match_oracle(case):
-    """The simple v1 gridding/gather kernels (kept for A/B checks) against the same oracle."""
-    name, N, L, xi, M, P, n_l, S0, SI, SJ, seed = case
-    x, q = make_system(N, L, seed)
-    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
-    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ, reference_kernels=True)
-    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), name
-
-
 EDGE = [
     # name, N, L, xi, M, P, n_l, S0, SI, SJ, seed
     ("odd-P7", 90, (1, 1, 1), 4.0, 16, 7, 2, 64, 48, 24, 21),

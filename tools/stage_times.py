@@ -1,6 +1,5 @@
 """Per-stage device times of the k-space path for one config (CUDA events inside the library).
-    python tools/stage_times.py C5 [v1|field]   (v1: the simple reference gridding/gather kernels;
-                                                 field: the field (force) variant of the gather)"""
+    python tools/stage_times.py C5 [field]   (field: the field (force) variant of the gather)"""
 import sys
 
 import torch
@@ -10,16 +9,14 @@ import paper_1611_09538_b200 as se1p  # noqa: E402
 from se1p_synth import CONFIGS, kspace_kwargs, make_system  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C5"]
-v1 = len(sys.argv) > 2 and sys.argv[2] == "v1"
 field = len(sys.argv) > 2 and sys.argv[2] == "field"
 x, q = make_system(cfg.N, cfg.L, cfg.seed)
 xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
 kw = kspace_kwargs(cfg)
 acc = {}
 for r in range(6):
-    se1p.kspace(xd, qd, cfg.L, cfg.xi, cfg.M, cfg.P, skip_checks=True, profile=True, reference_kernels=v1, field=field,
-                **kw)
+    se1p.kspace(xd, qd, cfg.L, cfg.xi, cfg.M, cfg.P, skip_checks=True, profile=True, field=field, **kw)
     if r >= 2:
         for k, v in se1p.stage_times().items():
             acc[k] = acc.get(k, 0.0) + v / 4
-print(cfg.name, "v1" if v1 else ("field" if field else "tiles"), " ".join(f"{k}={v:.3f}" for k, v in acc.items()), f"total={sum(acc.values()):.3f} ms", flush=True)
+print(cfg.name, "field" if field else "sweep", " ".join(f"{k}={v:.3f}" for k, v in acc.items()), f"total={sum(acc.values()):.3f} ms", flush=True)
