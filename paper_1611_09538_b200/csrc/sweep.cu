@@ -68,10 +68,16 @@ constexpr int kNR = 2;   // record ring depth (batches): released once expanded
 __host__ __device__ constexpr int sw_R(int NZB) { return 8 * NZB + 8; }
 __host__ __device__ constexpr int sw_S(int NZB) { return sw_R(NZB) + ((4 - sw_R(NZB)) % 16 + 16) % 16; }
 __host__ __device__ constexpr int sw_nc(int FM) { return FM == 1 ? 3 : 1; }   // gather outputs per pass
-// node i (0..15) of free axis ax of the row of ring slot e sits at 16 ax + 8 (i >> 3) + ((i & 7) ^ key),
-// key = ((e >> 1) & 3) | (ax << 2): the 2 axes of 8 consecutive candidates, stored by one half-warp
-// (row stride 8 mod 16, BM a multiple of 8), then hit 16 distinct bank pairs
-__host__ __device__ __forceinline__ int xy_key(int e, int ax) { return ((e >> 1) & 3) | (ax << 2); }
+// Swizzles (row stride 8 mod 16 doubles, so row e starts at bank pair 8 (e & 1)): node i (0..15) of
+// free axis ax of the row of ring slot e sits at 16 ax + (i ^ xy_key(e, ax)), node n (0..7) of z block
+// j at kZ + 8 j + (n ^ z_key(e)).  A warp's list is mostly runs of consecutive slots, and for any 4
+// consecutive slots these keys make the consumers' loads conflict-free: the gridding z loads (4
+// particles x 8 nodes), x loads (4 x 2 nodes) and y loads (4 x 4 nodes), the gather's z pairs; the
+// 8 consecutive slots x 2 axes of one expander half-warp's stores hit 16 distinct bank pairs.
+__host__ __device__ __forceinline__ int xy_key(int e, int ax) {
+  return ax == 0 ? (2 * ((e >> 1) & 1) + 4 * ((e >> 2) & 1)) : (1 + 2 * ((e >> 2) & 1) + 4 * ((e >> 1) & 1));
+}
+__host__ __device__ __forceinline__ int z_key(int e) { return 2 * ((e >> 1) & 1); }
 
 struct SweepArgs {
   KDev dv;
@@ -87,7 +93,7 @@ struct SweepArgs {
 };
 
 struct SweepSmem {
-  int off_meta, off_lists, off_raw, off_rows, off_acc, off_ring, total;
+  int off_meta, off_mask, off_lists, off_raw, off_rows, off_acc, off_ring, total;
 };
 
 // barriers: full, empty, (unused) [kMaxNB], rawb, rawfree [kNR]; headers hdr [kMaxNB], bhdr [kNR]
@@ -99,6 +105,9 @@ __host__ __device__ inline SweepSmem sweep_smem(int BM, int NB, int NZB, bool ga
   o = (o + 15) & ~15;
   s.off_meta = o;
   o += (NB * BM + 1) * 16;
+  s.off_mask = o;
+  o += (NB * BM + 1) * 4;
+  o = (o + 15) & ~15;
   s.off_lists = o;
   o += kCW * (BM + 24) * 4;
   o = (o + 127) & ~127;
@@ -107,7 +116,7 @@ __host__ __device__ inline SweepSmem sweep_smem(int BM, int NB, int NZB, bool ga
   s.off_rows = o;
   o += (NB * BM + 1) * row_stride(NZB) * 8;
   s.off_acc = o;
-  if (gather) o += (NB * BM + 1) * kCW * sw_nc(FM) * 8;
+  if (gather) o += (NB * BM + 1) * (kCW * sw_nc(FM) + 1) * 8;
   o = (o + 127) & ~127;
   s.off_ring = o;
   if (!gather) o += kCW * 16 * sw_S(NZB) * 8;
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   constexpr int NC = sw_nc(FM);                   // values this pass writes per particle
   constexpr int NCT = FM ? 4 : 1;                 // values per gather slot
   constexpr int COFF = FM == 2 ? 3 : 0;           // first slot value of this pass
-  constexpr int ACS = kCW * NC;                   // acc doubles per candidate
+  constexpr int ACS = kCW * NC + 1;               // acc doubles per candidate (odd: conflict-free reduce)
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   int4* bhdr = hdr + kMaxNB;
   double* f1 = reinterpret_cast<double*>(smem + kSmemHead);
   int4* meta = reinterpret_cast<int4*>(smem + L.off_meta);
+  int* mask = reinterpret_cast<int*>(smem + L.off_mask);
   int* lists = reinterpret_cast<int*>(smem + L.off_lists);
   double* raw = reinterpret_cast<double*>(smem + L.off_raw);
   double* rows = reinterpret_cast<double*>(smem + L.off_rows);
@@ -216,6 +226,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   for (int k = tid; k < kMaxP; k += kSweepThreads) f1[k] = k < P ? A.f1[k] : 0.0;
   for (int k = tid; k < RS; k += kSweepThreads) rows[dummy * RS + k] = 0.0;
   if (tid < 4) reinterpret_cast<int*>(&meta[dummy])[tid] = 0;
+  if (tid == 0) mask[dummy] = 0;
   if (!GATHER)
     for (int k = tid; k < kCW * 16 * S; k += kSweepThreads) ring[k] = 0.0;
   __syncthreads();
@@ -323,13 +334,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         const int tx = X0 / kTXY, ty = Y0 / kTXY;
         for (int p = gl; p < h.z; p += kGW * 32) {
           const int4 m = meta[bj * BM + p];
-          if (m.x == 0) continue;
+          const int wm = mask[bj * BM + p];
+          if (wm == 0) continue;
           const double* ap = acc + (int64_t)(bj * BM + p) * ACS;
           double sm[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) sm[c] = 0.0;
           for (int v = 0; v < kCW; ++v)
-            if ((m.x >> v) & 1)
+            if ((wm >> v) & 1)
 #pragma unroll
               for (int c = 0; c < NC; ++c) sm[c] += ap[v * NC + c];
           if (FM == 1) {   // column moments -> d/dx, d/dy: 2 alpha (h S + delta phi), delta = d0 + (X0 - j0) h
@@ -340,7 +352,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
             sm[2] = ta * fma(dv.h, sm[2], dy * sm[0]);
           }
           const int sx = tx - fdiv(m.y, kTXY), sy = ty - fdiv(m.z, kTXY);
-          if (sx < 0 || sx >= dv.nsxy || sy < 0 || sy >= dv.nsxy || m.w < 0 || m.w >= dv.N) atomicOr(dv.err, 4);
+          if (sx < 0 || sx >= dv.nsxy || sy < 0 || sy >= dv.nsxy || m.w < 0 || m.w >= dv.N) {
+            atomicOr(dv.err, 4);
+#if SE1P_SWEEP_WATCHDOG
+            printf("slot check: blk %d j %d bj %d p %d h=(%d %d %d %d) wm %x meta=(%d %d %d %d) X0 %d Y0 %d\n", blockIdx.x, j,
+                   bj, p, h.x, h.y, h.z, h.w, wm, m.x, m.y, m.z, m.w, X0, Y0);
+#endif
+            continue;
+          }
 #pragma unroll
           for (int c = 0; c < NC; ++c)
             A.gpart[(int64_t)((sx * dv.nsxy + sy) * NCT + COFF + c) * dv.N + m.w] = sm[c];
@@ -365,8 +384,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         break;
       }
       if (k >= NB) {
-        if (GATHER) reduce_batch(k - NB);
-        else mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1), 600000 + k);
+        if (GATHER) {
+          reduce_batch(k - NB);
+          // the group's 4 warps reduced disjoint candidates of the slot: all done before it is refilled
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "n"(kGW * 32) : "memory");
+        } else {
+          mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1), 600000 + k);
+        }
       }
       if (h.z > 0) {
         int X0, Y0, Z0, Ck, zc;
@@ -400,7 +424,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int tt = t0 + q;
-            o[8 * (q >> 3) + ((q & 7) ^ key)] = (tt >= 0 && tt < P) ? ((q < 8 ? base : base8) * f1[tt]) * pw[q & 7] : 0.0;
+            o[q ^ key] = (tt >= 0 && tt < P) ? ((q < 8 ? base : base8) * f1[tt]) * pw[q & 7] : 0.0;
           }
           if (ax == 0) {
             // consumer warps whose 4 x 4 block the stencil meets
@@ -411,18 +435,20 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
               const int xb = ((1 << (bx1 + 1)) - 1) & ~((1 << bx0) - 1);
               for (int by = by0; by <= by1; ++by) wm |= xb << (4 * by);
             }
-            meta[e] = make_int4(wm, jj.x, jj.y, (int)__double_as_longlong(rr[kRi]));
+            meta[e] = make_int4(0, jj.x, jj.y, (int)__double_as_longlong(rr[kRi]));
+            mask[e] = wm;
           }
           // the z window: 16-byte chunks ax, ax + 2, ..., rotated by 3 steps for every other pair of
           // candidates (conflict-free 16-byte stores)
           const double2* zs = reinterpret_cast<const double2*>(rr + kRz);
           double2* zd = reinterpret_cast<double2*>(rows + (int64_t)e * RS + kZ);
-          const int nz2 = 2 * NZB, rot = ((cand >> 1) & 1) * 3;
+          const int nz2 = 2 * NZB, rot = ((cand >> 1) & 1) * 3, zk = z_key(e) >> 1;
 #pragma unroll
           for (int i = 0; i < nz2; ++i) {
             int i2 = i + rot;
             if (i2 >= nz2) i2 -= nz2;
-            zd[2 * i2 + ax] = zs[2 * i2 + ax];
+            const int sc = 2 * i2 + ax;   // source chunk (node pair) -> block sc >> 2, pair (sc & 3) ^ zk
+            zd[(sc & ~3) | ((sc & 3) ^ zk)] = zs[sc];
           }
         }
       }
@@ -441,9 +467,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   const int g = lane >> 2, tg = lane & 3;
   const int bxw = w & 3, byw = w >> 2;
   const int xa = 4 * bxw + (g >> 2), yb = 4 * byw + (g & 3);   // this lane's columns g, g+8 -> x xa, xa+2; y yb
-  // x/y row offsets before the row's swizzle bits (xy_key: (e >> 1) & 3, XORed into the node index)
-  const int oxa = xa, oxa2 = xa + 2, oyb = 16 + (yb ^ 4);
-  auto sw4 = [](int e) { return (e >> 1) & 3; };
+  // row offsets: x node xa (xa + 2) at xa ^ xy_key(e, 0), y node yb at 16 + (yb ^ xy_key(e, 1))
   // gridding: B lane g holds frame node sg = (g >> 1) + 4 (g & 1), so C lane tg holds nodes tg, tg + 4;
   // gather: K index tg (tg + 4) of block j is node 2 tg (2 tg + 1): one 16-byte pair of the record
   const int sg = (g >> 1) + 4 * (g & 1);
@@ -517,16 +541,18 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         const int e0 = wl[k + tg], e1 = wl[k + tg + 4];
         const double* r0 = rows + e0 * RS;
         const double* r1 = rows + e1 * RS;
-        const int s0 = sw4(e0), s1 = sw4(e1);
-        const double y0 = r0[oyb ^ s0], y1 = r1[oyb ^ s1];
-        const double a[4] = {r0[oxa ^ s0] * y0, r0[oxa2 ^ s0] * y0, r1[oxa ^ s1] * y1, r1[oxa2 ^ s1] * y1};
+        const int x0k = xy_key(e0, 0), x1k = xy_key(e1, 0);
+        const double y0 = r0[16 + (yb ^ xy_key(e0, 1))], y1 = r1[16 + (yb ^ xy_key(e1, 1))];
+        const double a[4] = {r0[xa ^ x0k] * y0, r0[(xa + 2) ^ x0k] * y0, r1[xa ^ x1k] * y1, r1[(xa + 2) ^ x1k] * y1};
+        const double* z0 = r0 + kZ + (sg ^ z_key(e0));
+        const double* z1 = r1 + kZ + (sg ^ z_key(e1));
 #pragma unroll
-        for (int j = 0; j < NZB; ++j) dmma_16x8x8(c[j], a, r0[kZ + 8 * j + sg], r1[kZ + 8 * j + sg]);
+        for (int j = 0; j < NZB; ++j) dmma_16x8x8(c[j], a, z0[8 * j], z1[8 * j]);
       }
     } else {
       for (int k = k0; k < k1; k += 8) {
         const int e = wl[k + g];
-        const double* z = rows + e * RS + kZ + 2 * tg;
+        const double* z = rows + e * RS + kZ + ((2 * tg) ^ z_key(e));
         double t[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int j = 0; j < NZB; ++j) {
@@ -537,11 +563,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         const int ea = wl[k + 2 * tg], eb = wl[k + 2 * tg + 1];
         const double* ra = rows + ea * RS;
         const double* rb2 = rows + eb * RS;
-        const int sa = sw4(ea), sb = sw4(eb);
+        const int sa = xy_key(ea, 0), sb = xy_key(eb, 0), ya = 16 + (yb ^ xy_key(ea, 1)), yb2 = 16 + (yb ^ xy_key(eb, 1));
         double va[NC], vb[NC];
         {
-          const double wxa = ra[oxa ^ sa], wxa2 = ra[oxa2 ^ sa], wya = ra[oyb ^ sa];
-          const double wxb = rb2[oxa ^ sb], wxb2 = rb2[oxa2 ^ sb], wyb = rb2[oyb ^ sb];
+          const double wxa = ra[xa ^ sa], wxa2 = ra[(xa + 2) ^ sa], wya = ra[ya];
+          const double wxb = rb2[xa ^ sb], wxb2 = rb2[(xa + 2) ^ sb], wyb = rb2[yb2];
           va[0] = wya * fma(wxa, t[0], wxa2 * t[2]);
           vb[0] = wyb * fma(wxb, t[1], wxb2 * t[3]);
           if (FM == 1) {   // column moments in tile coordinates (x: xa, xa + 2; y: yb)
@@ -620,7 +646,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
     const int cn = h.z;
     for (int p0 = 0; p0 < cn; p0 += 32) {
       const int p = p0 + lane;
-      const bool rel = p < cn && ((meta[b * BM + p].x >> w) & 1);
+      const bool rel = p < cn && ((mask[b * BM + p] >> w) & 1);
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
       if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = b * BM + p;
       n += __popc(bal);
