@@ -47,7 +47,10 @@ constexpr int kSweepThreads = (kCW + 1 + kSW) * 32;
 constexpr int kMaxNB = 4;
 // batch ring depth (shared-memory slots): even, so that a row slot is always reused by the
 // expander group that filled it
-constexpr int kNB = 4;
+#ifndef SE1P_SWEEP_NB
+#define SE1P_SWEEP_NB 4
+#endif
+constexpr int kNB = SE1P_SWEEP_NB;
 constexpr int kMaxP = 64;
 
 // header flags of a batch
@@ -63,21 +66,22 @@ __host__ __device__ constexpr int rec_stride(int NZB) { return kRz + 8 * NZB + (
 // stride 8 (mod 16) doubles
 constexpr int kZ = 32;
 __host__ __device__ constexpr int row_stride(int NZB) { return kZ + 8 * NZB + ((NZB & 1) ? 0 : 8); }
-constexpr int kNR = 2;   // record ring depth (batches): released once expanded
+#ifndef SE1P_SWEEP_NR
+#define SE1P_SWEEP_NR 2
+#endif
+constexpr int kNR = SE1P_SWEEP_NR;   // record ring depth (batches, a multiple of kEG): released once expanded
 // gridding ring: R positions (>= 8 NZB + 8), column stride S = 4 (mod 16) doubles
 __host__ __device__ constexpr int sw_R(int NZB) { return 8 * NZB + 8; }
 __host__ __device__ constexpr int sw_S(int NZB) { return sw_R(NZB) + ((4 - sw_R(NZB)) % 16 + 16) % 16; }
 __host__ __device__ constexpr int sw_nc(int FM) { return FM == 1 ? 3 : 1; }   // gather outputs per pass
-// Swizzles (row stride 8 mod 16 doubles, so row e starts at bank pair 8 (e & 1)): node i (0..15) of
-// free axis ax of the row of ring slot e sits at 16 ax + (i ^ xy_key(e, ax)), node n (0..7) of z block
-// j at kZ + 8 j + (n ^ z_key(e)).  A warp's list is mostly runs of consecutive slots, and for any 4
-// consecutive slots these keys make the consumers' loads conflict-free: the gridding z loads (4
-// particles x 8 nodes), x loads (4 x 2 nodes) and y loads (4 x 4 nodes), the gather's z pairs; the
-// 8 consecutive slots x 2 axes of one expander half-warp's stores hit 16 distinct bank pairs.
-__host__ __device__ __forceinline__ int xy_key(int e, int ax) {
-  return ax == 0 ? (2 * ((e >> 1) & 1) + 4 * ((e >> 2) & 1)) : (1 + 2 * ((e >> 2) & 1) + 4 * ((e >> 1) & 1));
-}
-__host__ __device__ __forceinline__ int z_key(int e) { return 2 * ((e >> 1) & 1); }
+// Swizzles (row stride 8 mod 16 doubles, so row e starts at bank pair 8 (e & 1)), with k = e & 6:
+// x node i (0..15) of the row of ring slot e sits at i ^ k, y node i at 16 + (ypos(i) ^ k ^ 1) with
+// ypos swapping bits 1 and 2 of i, z node n (0..7) of block j at kZ + 8 j + (n ^ (k & 2)).  A warp's
+// list is mostly runs of consecutive slots, and for any 4 consecutive slots these make the
+// consumers' loads conflict-free: the gridding z loads (4 particles x 8 nodes), x loads (4 x 2 nodes)
+// and y loads (4 x 4 nodes), the gather's z pairs; the 8 consecutive slots x 2 axes of one expander
+// half-warp's stores hit 16 distinct bank pairs.
+__host__ __device__ __forceinline__ int ypos(int i) { return (i & ~6) | ((i & 2) << 1) | ((i & 4) >> 1); }
 
 struct SweepArgs {
   KDev dv;
@@ -420,11 +424,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
           const double E3 = E2 * E;
           const double pw[8] = {1.0, E, E2, E3, E4, E4 * E, E4 * E2, E4 * E3};
           double* o = rows + (int64_t)e * RS + 16 * ax;
-          const int key = xy_key(e, ax);
+          const int key = (e & 6) | ax;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int tt = t0 + q;
-            o[q ^ key] = (tt >= 0 && tt < P) ? ((q < 8 ? base : base8) * f1[tt]) * pw[q & 7] : 0.0;
+            o[(ax ? ypos(q) : q) ^ key] = (tt >= 0 && tt < P) ? ((q < 8 ? base : base8) * f1[tt]) * pw[q & 7] : 0.0;
           }
           if (ax == 0) {
             // consumer warps whose 4 x 4 block the stencil meets
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
           // candidates (conflict-free 16-byte stores)
           const double2* zs = reinterpret_cast<const double2*>(rr + kRz);
           double2* zd = reinterpret_cast<double2*>(rows + (int64_t)e * RS + kZ);
-          const int nz2 = 2 * NZB, rot = ((cand >> 1) & 1) * 3, zk = z_key(e) >> 1;
+          const int nz2 = 2 * NZB, rot = ((cand >> 1) & 1) * 3, zk = (e >> 1) & 1;
 #pragma unroll
           for (int i = 0; i < nz2; ++i) {
             int i2 = i + rot;
@@ -467,7 +471,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   const int g = lane >> 2, tg = lane & 3;
   const int bxw = w & 3, byw = w >> 2;
   const int xa = 4 * bxw + (g >> 2), yb = 4 * byw + (g & 3);   // this lane's columns g, g+8 -> x xa, xa+2; y yb
-  // row offsets: x node xa (xa + 2) at xa ^ xy_key(e, 0), y node yb at 16 + (yb ^ xy_key(e, 1))
+  // row offsets (see ypos): x node xa (xa + 2) at xa ^ k, y node yb at 16 + (yq ^ k), k = e & 6
+  const int yq = ypos(yb) ^ 1;
   // gridding: B lane g holds frame node sg = (g >> 1) + 4 (g & 1), so C lane tg holds nodes tg, tg + 4;
   // gather: K index tg (tg + 4) of block j is node 2 tg (2 tg + 1): one 16-byte pair of the record
   const int sg = (g >> 1) + 4 * (g & 1);
@@ -536,23 +541,26 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   };
 
   auto ksteps = [&](int k0, int k1) {
+#ifdef SE1P_SWEEP_EXP_NO_KSTEPS   // experiment build: the staging and bookkeeping floor
+    return;
+#endif
     if (!GATHER) {
       for (int k = k0; k < k1; k += 8) {
         const int e0 = wl[k + tg], e1 = wl[k + tg + 4];
         const double* r0 = rows + e0 * RS;
         const double* r1 = rows + e1 * RS;
-        const int x0k = xy_key(e0, 0), x1k = xy_key(e1, 0);
-        const double y0 = r0[16 + (yb ^ xy_key(e0, 1))], y1 = r1[16 + (yb ^ xy_key(e1, 1))];
-        const double a[4] = {r0[xa ^ x0k] * y0, r0[(xa + 2) ^ x0k] * y0, r1[xa ^ x1k] * y1, r1[(xa + 2) ^ x1k] * y1};
-        const double* z0 = r0 + kZ + (sg ^ z_key(e0));
-        const double* z1 = r1 + kZ + (sg ^ z_key(e1));
+        const int k0 = e0 & 6, k1 = e1 & 6;
+        const double y0 = r0[16 + (yq ^ k0)], y1 = r1[16 + (yq ^ k1)];
+        const double a[4] = {r0[xa ^ k0] * y0, r0[(xa + 2) ^ k0] * y0, r1[xa ^ k1] * y1, r1[(xa + 2) ^ k1] * y1};
+        const double* z0 = r0 + kZ + (sg ^ (k0 & 2));
+        const double* z1 = r1 + kZ + (sg ^ (k1 & 2));
 #pragma unroll
         for (int j = 0; j < NZB; ++j) dmma_16x8x8(c[j], a, z0[8 * j], z1[8 * j]);
       }
     } else {
       for (int k = k0; k < k1; k += 8) {
         const int e = wl[k + g];
-        const double* z = rows + e * RS + kZ + ((2 * tg) ^ z_key(e));
+        const double* z = rows + e * RS + kZ + ((2 * tg) ^ (e & 2));
         double t[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int j = 0; j < NZB; ++j) {
@@ -563,7 +571,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         const int ea = wl[k + 2 * tg], eb = wl[k + 2 * tg + 1];
         const double* ra = rows + ea * RS;
         const double* rb2 = rows + eb * RS;
-        const int sa = xy_key(ea, 0), sb = xy_key(eb, 0), ya = 16 + (yb ^ xy_key(ea, 1)), yb2 = 16 + (yb ^ xy_key(eb, 1));
+        const int sa = ea & 6, sb = eb & 6, ya = 16 + (yq ^ sa), yb2 = 16 + (yq ^ sb);
         double va[NC], vb[NC];
         {
           const double wxa = ra[xa ^ sa], wxa2 = ra[(xa + 2) ^ sa], wya = ra[ya];
