@@ -8,7 +8,8 @@ in HBM.  value = particles of the system / time.  Multi-GPU (torchrun): ONE syst
 the ranks (paper_1611_09538_b200/dist.py: x slabs, k3 modes owned by ranks, two all-to-all
 transposes and an all-reduce over NCCL) -> "scaling": "strong"; time = max over ranks.
 The CPU oracle (oracle/) is timed beside it on a bounded sample (cpu_baseline), and
---impl reference times the oracle as the reference arm.
+--impl reference times the oracle as the reference arm.  Run with --gpus N > 1 outside torchrun,
+bench.py launches itself under torch.distributed.run with N ranks (127.0.0.1).
 """
 from __future__ import annotations
 
@@ -59,10 +60,10 @@ def kspace_flops_spread(cfg):
 
 
 def cpu_oracle_rate(cfg, seconds):
-    """Oracle (plain CPU Ewald1P, oracle/ewald1p.c) on seeded targets vs all N sources."""
+    """Oracle (plain CPU Ewald1P, oracle/ewald1p.c) on seeded targets vs all N sources; its
+    source sums are split over fixed source blocks, so all cores work for any number of targets."""
     import oracle
     x, q = make_system(cfg.N, cfg.L, cfg.seed)
-    cores = len(os.sched_getaffinity(0))
     # calibrate on a few targets, then run a sample sized for ~`seconds`
     t0 = time.perf_counter()
     oracle.phi_exact(x, q, cfg.L, sample_targets(cfg.N, 4, cfg.seed))
@@ -72,6 +73,7 @@ def cpu_oracle_rate(cfg, seconds):
     t0 = time.perf_counter()
     oracle.phi_exact(x, q, cfg.L, tg)
     dt = time.perf_counter() - t0
+    cores = oracle.threads_used(cfg.N, m)
     return {"value": m / dt, "unit": "particles/s", "cores": cores, "kind": "oracle",
             "sample": f"{m} seeded targets of {cfg.name} (exact Ewald1P potential, all {cfg.N} sources each), {dt:.1f} s"}
 
@@ -174,13 +176,32 @@ def bench_ours(args, cfg, rank, world, local):
     clocks = clk.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # end-to-end through the public API: every step copies its x, q from pinned host memory to the
-    # device, runs the step and reads phi back to pinned host memory.  Single GPU: two buffer
-    # slots and copy streams, so step i+1's H2D and step i-1's D2H run on the copy engines while
-    # step i computes (a streaming user's pipeline); multi-GPU: one slot, serial.
+    # end-to-end through the C ABI with HOST buffers (se1p_kspace_ex, opts->host_io): every call
+    # copies x, q from pinned host memory into the library's device buffers, runs the step and
+    # copies phi back to pinned host memory before it returns (synchronous), K calls timed on the
+    # device between events on the call's stream.  Multi-GPU: the torch-staged copies below.
     xh = torch.from_numpy(x_np).pin_memory()
     qh = torch.from_numpy(q_np).pin_memory()
+    ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
     ke = max(3, args.steps // 2)
+    e2e_pipelined = None
+    if world == 1:
+        xhn, qhn, phn = xh.numpy(), qh.numpy(), ph.numpy()
+        legacy = torch.cuda.default_stream(dev)
+        se1p.kspace(xhn, qhn, cfg.L, cfg.xi, cfg.M, cfg.P, out=phn, skip_checks=True, **kw)   # host staging buffers
+        torch.cuda.synchronize(dev)
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(legacy)
+        for _ in range(ke):
+            se1p.kspace(xhn, qhn, cfg.L, cfg.xi, cfg.M, cfg.P, out=phn, skip_checks=True, **kw)
+        f1.record(legacy)
+        torch.cuda.synchronize(dev)
+        e2e_s = f0.elapsed_time(f1) / ke * 1e-3
+        assert np.array_equal(phn, phi.cpu().numpy()), "host-buffer result differs from the device step"
+
+    # end-to-end as a streaming user pipelines it (torch-staged copies): two buffer slots and copy
+    # streams, so step i+1's H2D and step i-1's D2H overlap step i; multi-GPU: one slot, serial.
     nslot = 2 if world == 1 else 1
     slots = [dict(x=torch.empty_like(x), q=torch.empty_like(q), phi=torch.empty_like(phi),
                   ph=torch.empty(cfg.N, dtype=torch.float64).pin_memory(),
@@ -216,9 +237,12 @@ def bench_ours(args, cfg, rank, world, local):
     e2e_run(ke)
     f1.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_s = max_over_ranks(f0.elapsed_time(f1) / ke) * 1e-3
+    pipe_s = max_over_ranks(f0.elapsed_time(f1) / ke) * 1e-3
     if world == 1:
         assert np.array_equal(slots[0]["ph"].numpy(), phi.cpu().numpy()), "e2e result differs from the device step"
+        e2e_pipelined = cfg.N / pipe_s
+    else:
+        e2e_s = pipe_s
 
     if world > 1:
         import torch.distributed as dist
@@ -267,7 +291,7 @@ def bench_ours(args, cfg, rank, world, local):
                    "l2": "per-step working set %.0f MB (particle records, grid, planes) > 126 MB L2; no flush"
                          % (info["workspace_bytes"] / 1e6 + 700 * cfg.N / 1e6)},
         "stages_ms": stage_sum,
-        "roofline": {"bound": "alu", "kernel": f"k_tiles ({dom_name})", "achieved": achieved,
+        "roofline": {"bound": "alu", "kernel": f"k_sweep ({dom_name})", "achieved": achieved,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                      "traffic": traffic,
                      "note": "FP64 pipe (DMMA): 2 N P^3 algorithmic flops per launch / CUDA-event launch time on "
@@ -282,7 +306,13 @@ def bench_ours(args, cfg, rank, world, local):
                 "frac": (b_alg / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]) if peaks.get("hbm_gbs") else None,
                 "note": "the path is FP64-bound (see roofline); DESIGN.md section 5"},
         "e2e": {"value": cfg.N / e2e_s, "unit": "particles/s",
-                "h2d_bytes_per_step": 32 * cfg.N * world, "d2h_bytes_per_step": 8 * cfg.N * world},
+                "h2d_bytes_per_step": 32 * cfg.N * world, "d2h_bytes_per_step": 8 * cfg.N * world,
+                "how": "C ABI se1p_kspace_ex with host buffers (pinned), synchronous per call" if world == 1
+                       else "torch-staged pinned copies around the distributed step"},
+        "e2e_pipelined": ({"value": e2e_pipelined, "unit": "particles/s",
+                           "how": "torch-staged pinned copies on two copy streams overlapping the graph step"}
+                          if e2e_pipelined else None),
+        "plan_ms": info.get("plan_ms"),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
@@ -301,13 +331,14 @@ def kernel_traffic(which):
 def bench_reference(args, cfg, rank, world=1):
     if rank != 0:
         return None
-    cores = len(os.sched_getaffinity(0))
     import oracle
     x, q = make_system(cfg.N, cfg.L, cfg.seed)
     t0 = time.perf_counter()
     oracle.phi_exact(x, q, cfg.L, sample_targets(cfg.N, 2, cfg.seed))
     per_target = max((time.perf_counter() - t0) / 2, 1e-6)
     budget = 150.0 / max(1, args.steps + args.warmup)    # whole run within a few minutes
+    # at least one target per core, so the reference arm and cpu_baseline time the same thing
+    budget = max(budget, per_target * min(16, len(os.sched_getaffinity(0))) * 1.01)
     m = int(max(2, min(cfg.N, budget / per_target)))
     for i in range(args.warmup):
         oracle.phi_exact(x, q, cfg.L, sample_targets(cfg.N, m, cfg.seed + 10 + i))
@@ -316,6 +347,7 @@ def bench_reference(args, cfg, rank, world=1):
         oracle.phi_exact(x, q, cfg.L, sample_targets(cfg.N, m, cfg.seed + 100 + i))
     dt = (time.perf_counter() - t0) / args.steps
     value = m / dt
+    cores = oracle.threads_used(cfg.N, m)
     sample = f"{m} seeded targets per step of {cfg.name} (exact Ewald1P, all {cfg.N} sources)"
     return {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "particles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -328,9 +360,27 @@ def bench_reference(args, cfg, rank, world=1):
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run with N ranks on
+    127.0.0.1 (NCCL init lines on, for the rank check) and return its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     rank, world, local = dist_env()
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         line = bench_reference(args, cfg, rank, world)

@@ -26,7 +26,10 @@
  *     argument errors are still returned synchronously.
  *   - On any non-OK return, se1p_last_error() gives a thread-local message.
  *   - Thread safety: calls on different threads are serialised by an internal mutex
- *     (plans and workspaces are per device and shared).
+ *     (plans and workspaces are per device and shared).  Calls may use different streams:
+ *     each call's stream first waits (cudaStreamWaitEvent) for the work the previous call on
+ *     the same device enqueued, so stream-ordered (sync == 0) calls on two streams never
+ *     overlap on the shared workspace.
  */
 #ifndef SE1P_H
 #define SE1P_H
@@ -83,6 +86,8 @@ typedef struct se1p_plan_info {
   int n_planes;         /* M/2 + 1 (Hermitian half along z)                              */
   int64_t grid_points;  /* M~^2 * M real grid points                                     */
   int64_t workspace_bytes;
+  double plan_ms;       /* host wall time of the plan build (tables, kernel spectra); paid once
+                           per parameter set, not per call                                   */
 } se1p_plan_info;
 
 /* k-space potential phi^F (Alg. 1 OUTPUT): no real-space and no self term.
@@ -258,7 +263,7 @@ void se1p_release(void);
    on comes from alloc(bytes, ctx) (must return device memory of the current device, >= 256-byte
    aligned, or NULL -> SE1P_ENOMEM) and goes back through release(ptr, ctx).  Before a pointer is
    released the library synchronises the device, so the hook may reuse it at once.  The call
-   first frees everything allocated so far (se1p_release, through the allocator that made it),
+   first frees everything allocated so far on every device (through the allocator that made it),
    then installs the hook; alloc = release = NULL restores cudaMalloc / cudaFree.  Not to be
    called while another thread is inside the library.  Returns SE1P_OK, or SE1P_EINVAL if
    exactly one of alloc, release is NULL (nothing changes then). */

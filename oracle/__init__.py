@@ -83,8 +83,17 @@ def _load():
         lib.orc_modes_needed.argtypes = [d, d]
         lib.orc_rc_converged.restype = d
         lib.orc_rc_converged.argtypes = [d]
+        lib.orc_threads.restype = i32
+        lib.orc_threads.argtypes = []
         _lib = lib
     return _lib
+
+
+def threads_used(N, m):
+    """OpenMP threads the source sums of phi_exact keep busy for m targets of an N-particle
+    system: the work items are (target, source block) pairs (ewald1p.c, orc_src_blocks)."""
+    blocks = 1 if N < 65536 else 64
+    return int(min(_load().orc_threads(), m * blocks))
 
 
 def _prep(x, q, L, targets):

@@ -44,6 +44,27 @@ static inline void nsum_add(nsum* a, double v) {
 }
 static inline double nsum_get(const nsum* a) { return a->s + a->c; }
 
+/* Work split for the source sums: target it, sources [n0, n1) of block bk.  Large systems use a
+   fixed number of source blocks (independent of the thread count) with one compensated partial
+   each, combined in block order -- deterministic, and every core busy for any number of targets;
+   small systems (N < 65536, every test size) use one block, i.e. the plain per-target sum. */
+static int64_t orc_src_blocks(int64_t N) { return N < 65536 ? 1 : 64; }
+static double orc_combine(const nsum* part, int64_t nb) {
+  if (nb == 1) return nsum_get(&part[0]);
+  nsum t = {0.0, 0.0};
+  for (int64_t b = 0; b < nb; ++b) {
+    nsum_add(&t, part[b].s);
+    nsum_add(&t, part[b].c);
+  }
+  return nsum_get(&t);
+}
+#ifdef _OPENMP
+#include <omp.h>
+int orc_threads(void) { return omp_get_max_threads(); }
+#else
+int orc_threads(void) { return 1; }
+#endif
+
 /* ---------------------------------------------------------------- E1, g */
 /* App. A uses the series for 0<x<1 and the continued fraction for "x >~ 1".  The
    series loses ~e^x/E1(x) * eps to cancellation above ~1.5, so the switch is at x = 1.5
@@ -242,13 +263,15 @@ double orc_dK0db(double a, double b) {
 void orc_phi_real(const double* x, const double* q, int64_t N, const double* L, double xi,
                   double rc, const int64_t* targets, int64_t m, double* out) {
   const double L3 = L[2];
-  const int64_t A = (int64_t)ceil(rc / L3) + 1;
+  const int64_t A = (int64_t)ceil(rc / L3) + 1, NB = orc_src_blocks(N);
+  nsum* part = (nsum*)malloc(sizeof(nsum) * (size_t)(m * NB));
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t it = 0; it < m; ++it) {
+  for (int64_t k = 0; k < m * NB; ++k) {
+    const int64_t it = k / NB, bk = k % NB, n0 = N * bk / NB, n1 = N * (bk + 1) / NB;
     const int64_t t = targets[it];
     nsum s = {0.0, 0.0};
     for (int64_t alpha = -A; alpha <= A; ++alpha) {
-      for (int64_t n = 0; n < N; ++n) {
+      for (int64_t n = n0; n < n1; ++n) {
         if (alpha == 0 && n == t) continue;          /* the prime in Eq. (3) */
         double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
         double dz = x[3 * t + 2] - x[3 * n + 2] + alpha * L3;
@@ -256,8 +279,10 @@ void orc_phi_real(const double* x, const double* q, int64_t N, const double* L, 
         if (d <= rc) nsum_add(&s, q[n] * erfc(xi * d) / d);
       }
     }
-    out[it] = nsum_get(&s);
+    part[k] = s;
   }
+  for (int64_t it = 0; it < m; ++it) out[it] = orc_combine(part + it * NB, NB);
+  free(part);
 }
 
 /* phi^{F,k3!=0}: Eq. (4b) P:88 with the +k3 and -k3 terms folded into 2cos(k3 dz).
@@ -266,39 +291,49 @@ void orc_phi_k3nz(const double* x, const double* q, int64_t N, const double* L, 
                   int J, const int64_t* targets, int64_t m, double* out) {
   if (!gl_ready) gl_init();
   const double L3 = L[2];
+  const int64_t NB = orc_src_blocks(N);
+  nsum* part = (nsum*)malloc(sizeof(nsum) * (size_t)(m * NB));
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t it = 0; it < m; ++it) {
+  for (int64_t k = 0; k < m * NB; ++k) {
+    const int64_t it = k / NB, bk = k % NB, n0 = N * bk / NB, n1 = N * (bk + 1) / NB;
     const int64_t t = targets[it];
     nsum s = {0.0, 0.0};
     for (int j = 1; j <= J; ++j) {
       const double k3 = 2.0 * ORC_PI * j / L3;
       const double a = k3 * k3 / (4.0 * xi * xi);
-      for (int64_t n = 0; n < N; ++n) {
+      for (int64_t n = n0; n < n1; ++n) {
         double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
         double dz = x[3 * t + 2] - x[3 * n + 2];
         double rho2 = dx * dx + dy * dy;
         nsum_add(&s, q[n] * 2.0 * cos(k3 * dz) * orc_K0inc(a, rho2 * xi * xi));
       }
     }
-    out[it] = nsum_get(&s) / L3;
+    part[k] = s;
   }
+  for (int64_t it = 0; it < m; ++it) out[it] = orc_combine(part + it * NB, NB) / L3;
+  free(part);
 }
 
 /* phi^{F,k3=0}: Eq. (5); the n = m term is excluded. */
 void orc_phi_k30(const double* x, const double* q, int64_t N, const double* L, double xi,
                  const int64_t* targets, int64_t m, double* out) {
   const double L3 = L[2];
+  const int64_t NB = orc_src_blocks(N);
+  nsum* part = (nsum*)malloc(sizeof(nsum) * (size_t)(m * NB));
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t it = 0; it < m; ++it) {
+  for (int64_t k = 0; k < m * NB; ++k) {
+    const int64_t it = k / NB, bk = k % NB, n0 = N * bk / NB, n1 = N * (bk + 1) / NB;
     const int64_t t = targets[it];
     nsum s = {0.0, 0.0};
-    for (int64_t n = 0; n < N; ++n) {
+    for (int64_t n = n0; n < n1; ++n) {
       if (n == t) continue;
       double dx = x[3 * t] - x[3 * n], dy = x[3 * t + 1] - x[3 * n + 1];
       nsum_add(&s, q[n] * orc_g(xi * xi * (dx * dx + dy * dy)));
     }
-    out[it] = -nsum_get(&s) / L3;
+    part[k] = s;
   }
+  for (int64_t it = 0; it < m; ++it) out[it] = -orc_combine(part + it * NB, NB) / L3;
+  free(part);
 }
 
 /* phi^self: Eq. (6) P:90. */

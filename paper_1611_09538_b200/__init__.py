@@ -44,7 +44,8 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("h", ctypes.c_double), ("eta", ctypes.c_double), ("M", ctypes.c_int), ("Mfree", ctypes.c_int),
                 ("Mt", ctypes.c_int), ("P", ctypes.c_int), ("n_local", ctypes.c_int), ("Ntilde", ctypes.c_int),
                 ("S0", ctypes.c_int), ("SI", ctypes.c_int), ("LK", ctypes.c_int), ("n_kernel_planes", ctypes.c_int),
-                ("n_planes", ctypes.c_int), ("grid_points", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
+                ("n_planes", ctypes.c_int), ("grid_points", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("plan_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

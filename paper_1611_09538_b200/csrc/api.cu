@@ -9,6 +9,8 @@
 #include <vector>
 
 #include "../../include/se1p.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "kspace.cuh"
 #include "real.cuh"
 #include "sort.cuh"
@@ -41,14 +43,33 @@ struct DevState {
   double* dq = nullptr;
   double* dphi = nullptr;
   int64_t io_cap = 0;
+  cudaEvent_t ws_done = nullptr;   // recorded after every call's work on its stream (WsOrder)
+  cudaStream_t ws_stream = nullptr;
 };
 static DevState g_dev[64];
+static uint64_t g_dev_used = 0;   // devices with state (se1p_set_allocator releases them all)
 
 static DevState& dev_state() {
   int d = 0;
   SE1P_CUDA_TRY(cudaGetDevice(&d));
+  g_dev_used |= 1ull << (d & 63);
   return g_dev[d & 63];
 }
+
+// Calls may come on different streams (graph mode's side stream, the caller's streams) and all
+// share the device's workspace: each call's stream first waits for the work of the last call.
+struct WsOrder {
+  DevState& ds;
+  cudaStream_t st;
+  WsOrder(DevState& d, cudaStream_t s) : ds(d), st(s) {
+    if (!ds.ws_done) SE1P_CUDA_TRY(cudaEventCreateWithFlags(&ds.ws_done, cudaEventDisableTiming));
+    else if (ds.ws_stream != st) SE1P_CUDA_TRY(cudaStreamWaitEvent(st, ds.ws_done, 0));
+  }
+  ~WsOrder() {
+    if (cudaEventRecord(ds.ws_done, st) == cudaSuccess) ds.ws_stream = st;
+    else cudaGetLastError();
+  }
+};
 
 static uint64_t g_ws_generation = 1;   // bumped on every workspace reallocation (graphs bake pointers)
 
@@ -241,18 +262,26 @@ static void fill_info(const KPlan& pl, se1p_plan_info* info) {
   info->n_planes = pl.n_planes;
   info->grid_points = (int64_t)pl.dv.Mt * pl.dv.Mt * pl.prm.M;
   info->workspace_bytes = info->grid_points * 8 + (int64_t)pl.n_planes * pl.dv.Mt * pl.dv.Mt * 16 + pl.t_off_total * 16;
+  info->plan_ms = pl.plan_ms;
 }
 
+// Stage boundaries of a k-space call: CUDA events on the call's stream (profiling mode) and NVTX
+// ranges named after the stages (SURVEY 5 "Tracing"; no-ops without a tool attached).
 struct StageTimer {
+  static constexpr const char* kNames[8] = {"se1p bin", "se1p records", "se1p spread", "se1p zfft",
+                                            "se1p modes", "se1p izfft",  "se1p gather", "se1p finish"};
   bool on;
   cudaStream_t st;
   cudaEvent_t ev[10];
-  int n = 0;
+  int n = 0, nm = 0;
   StageTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
     if (on)
       for (auto& e : ev) cudaEventCreate(&e);
   }
   void mark() {
+    if (nm > 0 && nm <= 8) nvtxRangePop();
+    if (nm < 8) nvtxRangePushA(kNames[nm]);
+    ++nm;
     if (on && n < 10) cudaEventRecord(ev[n++], st);
   }
   void finish() {
@@ -266,6 +295,7 @@ struct StageTimer {
     }
   }
   ~StageTimer() {
+    if (nm > 0 && nm <= 8) nvtxRangePop();
     if (on)
       for (auto& e : ev) cudaEventDestroy(e);
   }
@@ -339,6 +369,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
   }
   KPlan* pl = kplan_get(prm, st);
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   KWork& w = ds.w;
   const KDev& dv = pl->dv;
   ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
@@ -442,6 +473,7 @@ static void kspace3p_impl(const se1p_opts* o, cudaStream_t st, const double* x, 
   KPlan* pl = kplan_get(pa, st);
   KPlan* p3 = kplan_get(pb, st);
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   KWork& w = ds.w;
   const KDev& dv = pl->dv;
   ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
@@ -505,6 +537,7 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   if (!(xi > 0) || !(rc > 0) || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "xi, rc, L must be > 0"};
   const RDev d = real_geometry(L, xi, rc, N);
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   KWork& w = ds.w;
   ensure_particles(w, N, d.nc[0] * d.nc[1] * d.nc[2]);
   const bool host_io = o && o->host_io;
@@ -576,6 +609,7 @@ static void slab_forward_impl(const se1p_opts* o, cudaStream_t st, const double*
   check_slab(*pl, x_lo, x_hi);
   const std::vector<int> slot = check_order(*pl, plane_order);
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   KWork& w = ds.w;
   const KDev& dv = pl->dv;
   ensure_particles(w, N, dv.nbx * dv.M * dv.Mfree);
@@ -653,6 +687,7 @@ static void modes_impl(const se1p_opts* o, cudaStream_t st, const double L[3], d
   maps.insert(maps.end(), glJ.begin(), glJ.end());
   maps.insert(maps.end(), liJ.begin(), liJ.end());
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   KWork& w = ds.w;
   grow(w.T, w.T_cap, pl->t_off_total);
   if (!w.flag) ensure_particles(w, 1, 1);
@@ -668,6 +703,7 @@ static void slab_backward_impl(const se1p_opts* o, cudaStream_t st, int64_t N, c
   if (!phi_partial || (!planes_in && x_hi > x_lo)) throw Error{1, "null pointer"};
   const KParams prm = resolve(o, L, xi, M, P, eta, s0, sf, n_local);
   DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
   if (!(ds.fwd_N == N && ds.fwd_prm == prm))
     throw Error{1, "se1p_kspace_slab_backward needs the particle state of a matching se1p_kspace_slab_forward "
                    "on this device (same N and parameters)"};
@@ -864,11 +900,13 @@ int se1p_debug_copy(int which, double* host_dst, int64_t count) {
   });
 }
 
-void se1p_release(void) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  kplan_release_all();
-  int d = 0;
-  cudaGetDevice(&d);
+}  // extern "C"
+
+namespace se1p {
+// Frees everything the library holds on the CURRENT device d: its plans, workspace, tables,
+// streams and the CUDA graphs (which bake the freed pointers).  Caller holds g_mu.
+static void release_device(int d) {
+  kplan_release_all(d);
   DevState& ds = g_dev[d & 63];
   KWork& w = ds.w;
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
@@ -882,10 +920,22 @@ void se1p_release(void) {
   if (w.ev_join) cudaEventDestroy(w.ev_join);
   if (w.side2) cudaStreamDestroy(w.side2);
   if (w.ev_join2) cudaEventDestroy(w.ev_join2);
+  if (ds.ws_done) cudaEventDestroy(ds.ws_done);
   ds = DevState{};
-  for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);   // they bake the freed pointers
+  g_dev_used &= ~(1ull << (d & 63));
+  for (auto& g : g_graphs) cudaGraphExecDestroy(g.exec);
   g_graphs.clear();
   ++g_ws_generation;
+}
+}  // namespace se1p
+
+extern "C" {
+
+void se1p_release(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int d = 0;
+  cudaGetDevice(&d);
+  release_device(d);
 }
 
 int se1p_set_allocator(void* (*alloc)(size_t, void*), void (*release)(void*, void*), void* ctx) {
@@ -893,8 +943,16 @@ int se1p_set_allocator(void* (*alloc)(size_t, void*), void (*release)(void*, voi
     g_err = "se1p_set_allocator: alloc and release must both be set or both be null";
     return 1;
   }
-  se1p_release();   // everything allocated so far goes back through the allocator that made it
   std::lock_guard<std::mutex> lk(g_mu);
+  // everything allocated so far, on every device, goes back through the allocator that made it
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < 64; ++d)
+    if ((g_dev_used >> d) & 1) {
+      cudaSetDevice(d);
+      release_device(d);
+    }
+  cudaSetDevice(cur);
   g_alloc_fn = alloc;
   g_release_fn = release;
   g_alloc_ctx = ctx;

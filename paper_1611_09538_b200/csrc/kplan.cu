@@ -140,7 +140,9 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   return raw;
 }
 
-KPlan* kplan_get(const KParams& p, cudaStream_t st) {
+KPlan* kplan_get(const KParams& p0, cudaStream_t st) {
+  KParams p = p0;
+  SE1P_CUDA_TRY(cudaGetDevice(&p.device));   // tables live on one device: plans are per device
   for (auto& q : g_plans)
     if (q->prm == p) return q.get();
   ++g_plan_generation;
@@ -157,17 +159,22 @@ KPlan* kplan_get(const KParams& p, cudaStream_t st) {
   return build(p, st);
 }
 
-void kplan_release_all() {
+void kplan_release_all(int device) {
   ++g_plan_generation;
-  for (auto& q : g_plans) {
+  for (auto it = g_plans.begin(); it != g_plans.end();) {
+    KPlan* q = it->get();
+    if (q->prm.device != device) {
+      ++it;
+      continue;
+    }
     dev_free(q->d_tw);
     dev_free(q->d_khat);
     dev_free(q->d_exJ);
     dev_free(q->d_k2J);
     dev_free(q->d_pl);
     dev_free(q->d_f1);
+    it = g_plans.erase(it);
   }
-  g_plans.clear();
 }
 
 }  // namespace se1p

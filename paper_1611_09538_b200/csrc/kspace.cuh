@@ -45,8 +45,9 @@ struct KParams {       // everything a k-space plan is keyed on
   int S0, SI, SJ;      // resolved padded extents
   int periodic = 0;    // 1: SE3P transform plan (grid Mfree x Mfree x M, every plane a J plane, SJ = Mfree)
   std::vector<int> SIn;   // multi-tier upsampling: extent of mode n = 1..n_l (empty: SI for all)
+  int device = -1;        // the plan cache keys plans per device (kplan_get)
   bool operator==(const KParams& o) const {
-    return L[0] == o.L[0] && L[1] == o.L[1] && L[2] == o.L[2] && xi == o.xi && M == o.M && P == o.P &&
+    return device == o.device && L[0] == o.L[0] && L[1] == o.L[1] && L[2] == o.L[2] && xi == o.xi && M == o.M && P == o.P &&
            eta == o.eta && n_l == o.n_l && S0 == o.S0 && SI == o.SI && SJ == o.SJ && periodic == o.periodic &&
            SIn == o.SIn;
   }
@@ -117,7 +118,7 @@ struct KWork {                  // per-N workspace (grown on demand)
 };
 
 KPlan* kplan_get(const KParams& p, cudaStream_t st);   // cached
-void kplan_release_all();
+void kplan_release_all(int device);   // the plans of one device
 uint64_t kplan_generation();   // changes whenever a plan is built or freed
 void plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out);   // planner.cu
 double lambert_w0(double x);

@@ -202,13 +202,30 @@ def kspace_emulated(x, q, plan: DistPlan, backend):
     return phi
 
 
+_PLANS = {}
+
+
+def cached_plan(L, xi, M, P, R, **kw):
+    """DistPlan of the parameters for R ranks, built once (plan_info and the slab-bound DP are
+    host work that does not change between calls)."""
+    import paper_1611_09538_b200 as se1p
+    pk = {k: kw.get(k) for k in ("eta", "s0", "sf", "n_local", "Ntilde", "S0", "SI")}
+    key = (tuple(float(v) for v in L), float(xi), int(M), int(P), int(R), tuple(sorted(pk.items())))
+    if key not in _PLANS:
+        _PLANS[key] = make_plan(se1p.plan_info(L, xi, M, P, **pk), R)
+    return _PLANS[key]
+
+
 def kspace(x, q, L, xi, M, P, group=None, stream=None, **kw):
     """phi^F of one system sharded over the ranks of `group` (default: the world), every rank
-    passing the same x [N,3], q [N] (CUDA, float64) and parameters."""
+    passing the same x [N,3], q [N] (CUDA, float64) and parameters.  The library stages and the
+    collectives run on one stream (`stream`, default torch's current one), so each collective is
+    ordered after the stage that produced its input."""
+    import torch
     import torch.distributed as dist
-    import paper_1611_09538_b200 as se1p
     R = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    info = se1p.plan_info(L, xi, M, P, **{k: kw.get(k) for k in ("eta", "s0", "sf", "n_local", "Ntilde", "S0", "SI")})
-    plan = make_plan(info, R)
-    return kspace_rank(x, q, plan, CudaBackend(L, xi, M, P, stream=stream, **kw), rank, group)
+    plan = cached_plan(L, xi, M, P, R, **kw)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.stream(st):
+        return kspace_rank(x, q, plan, CudaBackend(L, xi, M, P, stream=st, **kw), rank, group)

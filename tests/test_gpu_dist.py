@@ -79,3 +79,35 @@ def test_nccl_world_one():
         assert torch.equal(phi, ref)
     finally:
         dist.destroy_process_group()
+
+
+def _nccl_worker(rank, world, port, cfgname, out):
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    c = CONFIGS[cfgname]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    phi = sdist.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kspace_kwargs(c))
+    torch.cuda.synchronize()
+    if rank == 0:
+        np.save(out, phi.cpu().numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="the NCCL path needs two GPUs")
+def test_nccl_two_ranks_match_single_gpu(tmp_path):
+    """dist.kspace over NCCL with world = 2 (one process per GPU) equals the single-GPU result."""
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "phi.npy")
+    mp.spawn(_nccl_worker, args=(2, port, "C3", out), nprocs=2, join=True)
+    c = CONFIGS["C3"]
+    x, q = make_system(c.N, c.L, c.seed)
+    ref = se1p.kspace(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda(), c.L, c.xi, c.M, c.P,
+                      **kspace_kwargs(c)).cpu().numpy()
+    got = np.load(out)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
