@@ -174,7 +174,7 @@ int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const dou
    field_out: [N][3] doubles (x, y, z components) in the caller's particle order, required;
    phi_out: N doubles or NULL -- when given, the potential of the matching non-field call is
    written too (same values).  Arguments, ownership, opts and errors as the _ex entries above.
-   The k-space field runs on the tile kernels only (opts->reserved[2] == 1 -> SE1P_EINVAL). */
+   opts->reserved[2] must be 0. */
 int se1p_kspace_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
                          int64_t N, const double L[3], double xi, int M, int P, double eta,
                          double s0, double sf, int n_local, double* phi_out, double* field_out);
@@ -182,6 +182,17 @@ int se1p_kspace_field_ex(const se1p_opts* opts, void* stream, const double* x, c
 int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
                        int64_t N, const double L[3], double xi, double rc, double* phi_out,
                        double* field_out);
+
+/* Energy, potentials and forces of the full singly periodic sum (Eq. (2), and its
+   gradient): phi = phi^F + phi^R + phi^self, E = E^F + E^R (the two field entries above, with rc
+   for the real-space term), F_n = q_n E_n (reading R-17) and the energy
+   U = 1/2 sum_n q_n phi_n, reduced on the device in a fixed order (bitwise
+   reproducible).  U_out: 1 double; phi_out: N doubles or NULL; F_out: [N][3] doubles, required.
+   All are device pointers, or host pointers with opts->host_io (then the call is synchronous).
+   Arguments and errors as se1p_kspace_ex and se1p_real_ex (rc > 0). */
+int se1p_energy_forces(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                       const double L[3], double xi, double rc, int M, int P, double eta, double s0,
+                       double sf, int n_local, double* U_out, double* phi_out, double* F_out);
 
 /* Resolve the plan the k-space call with these arguments would use (no device work
    beyond plan creation).  Returns SE1P_OK or the same errors as se1p_kspace_ex. */

@@ -26,7 +26,7 @@ EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_p
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
            "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol",
-           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex", "se1p_set_allocator"]
+           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex", "se1p_set_allocator", "se1p_energy_forces"]
 
 
 class SE1PError(RuntimeError):
@@ -83,6 +83,8 @@ def load(build_if_needed: bool = True):
     lib.se1p_kspace3p_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, vp]
     lib.se1p_plan_from_tol.argtypes = [vp, d, d, d, vp]
     lib.se1p_kspace_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32, vp, vp]
+    lib.se1p_energy_forces.argtypes = [vp, vp, vp, vp, i64, vp, d, d, i32, i32, d, d, d, i32, vp, vp, vp]
+    lib.se1p_energy_forces.restype = i32
     lib.se1p_real_field_ex.argtypes = [vp, vp, vp, vp, i64, vp, d, d, vp, vp]
     lib.se1p_plan_query.argtypes = [vp, vp, d, i32, i32, d, d, d, i32, vp]
     lib.se1p_last_stage_times.argtypes = [vp, i32]
@@ -268,20 +270,32 @@ def potential(x, q, L, xi, rc=None, M=None, P=None, tol=None, **kw):
     return kspace(x, q, L, xi, M, P, **kw) + real(x, q, L, xi, rc)
 
 
-def energy_forces(x, q, L, xi, rc=None, M=None, P=None, tol=None, **kw):
-    """(U, phi, F): the electrostatic energy U = 1/2 sum_n q_n phi_n, the potentials and the forces
-    F_n = q_n E_n, E = E^F + E^R (Eq. (2) and its gradient).  rc, M, P or tol as in potential()."""
+def energy_forces(x, q, L, xi, rc=None, M=None, P=None, tol=None, stream=None, sync=True, skip_checks=False,
+                  eta=None, s0=None, sf=None, n_local=None, Ntilde=None, S0=None, SI=None):
+    """(U, phi, F) from se1p_energy_forces: the electrostatic energy U = 1/2 sum_n q_n phi_n, the
+    potentials phi = phi^F + phi^R + phi^self and the forces F_n = q_n E_n, E = E^F + E^R (Eq. (2)
+    and its gradient), all computed in the library.  rc, M, P or tol as in potential().
+    CUDA tensors in -> CUDA tensors out (U a 0-d tensor); numpy in -> numpy out (U a float)."""
     if tol is not None:
         rc, M, P, kw2 = _tol_params(q, L, xi, tol)
-        kw = {**kw2, **kw}
+        eta, n_local, S0, SI, Ntilde = kw2["eta"], kw2["n_local"], kw2["S0"], kw2["SI"], kw2["Ntilde"]
     if rc is None or M is None or P is None:
         raise ValueError("give rc, M, P or tol")
-    pk, ek = kspace(x, q, L, xi, M, P, field=True, **kw)
-    pr, er = real(x, q, L, xi, rc, field=True)
-    phi, E = pk + pr, ek + er
-    U = 0.5 * float((q * phi).sum())
-    F = E * (q[:, None] if not isinstance(q, np.ndarray) else np.asarray(q)[:, None])
-    return U, phi, F
+    lib = load()
+    xp, qp, N, host, keep = _args(x, q)
+    phi, F, pptr, fptr = _outputs(x, N, True, None, None)
+    if host:
+        U = np.zeros(1)
+        uptr = U.ctypes.data
+    else:
+        import torch
+        U = torch.zeros((), dtype=torch.float64, device=x.device)
+        uptr = U.data_ptr()
+    o = _opts(Ntilde, S0, SI, host, skip_checks, sync)
+    _check(lib.se1p_energy_forces(ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi),
+                                  float(rc), int(M), int(P), _neg(eta, 0.0), _neg(s0), _neg(sf),
+                                  -1 if n_local is None else int(n_local), uptr, pptr, fptr))
+    return (float(U[0]) if host else U), phi, F
 
 
 def _ints(v):

@@ -39,6 +39,8 @@ struct DevState {
   int64_t idmap_cap = 0;
   double* xsel = nullptr;       // compacted x (3n), q (n), phi partial (n)
   int64_t xsel_cap = 0;
+  double* ef = nullptr;         // se1p_energy_forces: x, q staging, field parts, outputs
+  int64_t ef_cap = 0;
   double* dx = nullptr;   // host_io staging (device side)
   double* dq = nullptr;
   double* dphi = nullptr;
@@ -731,6 +733,79 @@ static void slab_backward_impl(const se1p_opts* o, cudaStream_t st, int64_t N, c
   finish_call(o, w, st);
 }
 
+// phi = phi^F + phi^R, F = q (E^F + E^R) per particle
+__global__ void k_combine_forces(const double* __restrict__ q, const double* __restrict__ pk,
+                                 const double* __restrict__ ek, const double* __restrict__ pr,
+                                 const double* __restrict__ er, int64_t N, double* __restrict__ phi,
+                                 double* __restrict__ F) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  if (phi) phi[i] = pk[i] + pr[i];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) F[3 * i + c] = q[i] * (ek[3 * i + c] + er[3 * i + c]);
+}
+
+// U = 1/2 sum q (phi^F + phi^R): one block, fixed per-thread strides and a fixed tree
+__global__ void k_energy(const double* __restrict__ q, const double* __restrict__ pk, const double* __restrict__ pr,
+                         int64_t N, double* __restrict__ U) {
+  __shared__ double s[1024];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) a += q[i] * (pk[i] + pr[i]);
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = 512; off > 0; off >>= 1) {
+    if (threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *U = 0.5 * s[0];
+}
+
+static void energy_forces_impl(const se1p_opts* o, cudaStream_t st, const double* x, const double* q, int64_t N,
+                               const double L[3], double xi, double rc, int M, int P, double eta, double s0,
+                               double sf, int n_local, double* U_out, double* phi_out, double* F_out) {
+  if (!x || !q || !U_out || !F_out || !L) throw Error{1, "null pointer"};
+  if (N < 1 || N > (int64_t)2000000000) throw Error{1, "N out of range"};
+  DevState& ds = dev_state();
+  WsOrder ws_order(ds, st);
+  const bool host_io = o && o->host_io;
+  grow(ds.ef, ds.ef_cap, 17 * N + 1);
+  double *dx = ds.ef, *dq = dx + 3 * N, *pk = dq + N, *ek = pk + N, *pr = ek + 3 * N, *er = pr + N;
+  double *dphi = er + 3 * N, *dF = dphi + N, *dU = dF + 3 * N;
+  if (host_io) {
+    SE1P_CUDA_TRY(cudaMemcpyAsync(dx, x, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    SE1P_CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  } else {
+    dx = const_cast<double*>(x);
+    dq = const_cast<double*>(q);
+    dphi = phi_out;
+    dF = F_out;
+    dU = U_out;
+  }
+  se1p_opts od{};
+  if (o) od = *o;
+  od.host_io = 0;
+  od.sync = 0;
+  kspace_impl(&od, st, dx, dq, N, L, xi, M, P, eta, s0, sf, n_local, pk, ek);
+  od.skip_checks = 1;
+  real_impl(&od, st, dx, dq, N, L, xi, rc, pr, er);
+  k_combine_forces<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(dq, pk, ek, pr, er, N, dphi, dF);
+  SE1P_LAUNCH_CHECK();
+  k_energy<<<1, 1024, 0, st>>>(dq, pk, pr, N, dU);
+  SE1P_LAUNCH_CHECK();
+  if (host_io) {
+    SE1P_CUDA_TRY(cudaMemcpyAsync(U_out, dU, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (phi_out) SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    SE1P_CUDA_TRY(cudaMemcpyAsync(F_out, dF, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));
+  }
+  if (!o || o->sync || host_io) {
+    SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+    int kerr = 0;
+    SE1P_CUDA_TRY(cudaMemcpy(&kerr, ds.w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+  }
+  SE1P_CUDA_TRY(cudaGetLastError());
+}
+
 template <typename F>
 static int guarded(F&& f) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -831,6 +906,17 @@ int se1p_real_field_ex(const se1p_opts* opts, void* stream, const double* x, con
   });
 }
 
+int se1p_energy_forces(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
+                       const double L[3], double xi, double rc, int M, int P, double eta, double s0, double sf,
+                       int n_local, double* U_out, double* phi_out, double* F_out) {
+  return guarded([&] {
+    se1p_opts o{};
+    if (opts) o = *opts;
+    energy_forces_impl(&o, (cudaStream_t)stream, x, q, N, L, xi, rc, M, P, eta, s0, sf, n_local, U_out, phi_out,
+                       F_out);
+  });
+}
+
 int se1p_kspace_slab_forward(const se1p_opts* opts, void* stream, const double* x, const double* q, int64_t N,
                              const double L[3], double xi, int M, int P, double eta, double s0, double sf,
                              int n_local, int x_lo, int x_hi, const int* plane_order, void* planes_out) {
@@ -912,7 +998,7 @@ static void release_device(int d) {
   for (void* p : {(void*)w.xs, (void*)w.perm, (void*)w.keys, (void*)w.bin_start, (void*)w.scratch,
                   (void*)w.grid, (void*)w.planes, (void*)w.T, (void*)w.red, (void*)w.flag, (void*)ds.dx,
                   (void*)w.gpart, (void*)w.rec, (void*)w.s4, (void*)ds.dmap, (void*)w.grid3, (void*)ds.sel,
-                  (void*)ds.idmap, (void*)ds.xsel, (void*)w.over, (void*)w.items})
+                  (void*)ds.idmap, (void*)ds.xsel, (void*)w.over, (void*)w.items, (void*)ds.ef})
     dev_free(p);
   real_release_tables(d);
   if (w.side) cudaStreamDestroy(w.side);

@@ -23,7 +23,16 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_1611_09538_b200 as se1p  # noqa: E402
 
-from test_gpu_fullsize import _targets  # noqa: E402
+from se1p_synth import edge_targets, sample_targets  # noqa: E402
+
+# field targets per config: (random, edge); the exact field costs O(N) per target
+FIELD_SUBSETS = {"C3": (1024, 128), "C4": (256, 64), "C5": (48, 16)}
+
+
+def _targets(cfg, x):
+    m, me = FIELD_SUBSETS[cfg.name]
+    h = cfg.L[2] / cfg.M
+    return np.unique(np.concatenate([sample_targets(cfg.N, m, cfg.seed), edge_targets(x, cfg.L, cfg.P * h, me, cfg.seed)]))
 from test_gpu_parity import CASES  # noqa: E402
 
 
@@ -73,7 +82,11 @@ def test_full_field_vs_exact_oracle(cfg):
     print(f"{cfg} field rel rms {err:.3e}")
     assert err <= 1e-9
     ref_phi = oracle.phi_exact(x, q, c.L)
+    U = float(U)
     assert abs(U - 0.5 * float(np.dot(q, ref_phi))) <= 1e-9 * 0.5 * float(np.dot(np.abs(q), np.abs(ref_phi)))
+    # host buffers through the same C entry (opts->host_io): identical results
+    Uh, phih, Fh = se1p.energy_forces(x, q, c.L, c.xi, c.rc, c.M, c.P, **kspace_kwargs(c))
+    assert Uh == U and np.array_equal(phih, phi.cpu().numpy()) and np.array_equal(Fh, F.cpu().numpy())
 
 
 @pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])

@@ -304,38 +304,78 @@ def test_multi_tier_matches_oracle():
         se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=4 * Mt, Ntilde=2 * Mt, S_modes=[Mt - 1] * n_l)
 
 
+def _random_config(rng):
+    """A seeded random valid configuration (tools/fuzz_parity.py's generator), or None."""
+    M = int(rng.choice([8, 10, 12, 14, 16, 20, 24, 30, 32, 36, 40, 48]))
+    P = int(rng.integers(2, min(M, 28) + 1))
+    L3 = float(rng.choice([0.5, 1.0, 1.5, 2.0]))
+    m1 = int(rng.choice([M // 2, M, (3 * M) // 2])) if M % 2 == 0 else M
+    h = L3 / M
+    m2 = int(rng.integers(max(1, m1 // 2), m1 + 1)) if rng.random() < 0.3 else m1   # rectangular (R-19)
+    Lsq = (m1 * h, m1 * h, L3)
+    L = (m1 * h, m2 * h, L3) if rng.random() < 0.5 else (m2 * h, m1 * h, L3)
+    xi = float(rng.uniform(2.0, 9.0)) / max(L)
+    eta = P * xi ** 2 * h ** 2 / (0.95 ** 2 * math.pi)
+    if not (0.05 < eta < 0.95):
+        return None
+    Mt = m1 + P
+    n_l = int(rng.integers(0, M // 2 + 1))
+    S0 = int(Mt * rng.uniform(2.5, 4.0))
+    SI = int(Mt * rng.uniform(1.0, 3.0)) if n_l else Mt
+    SJ = int(rng.integers(Mt, 2 * Mt))
+    while not all(f in (2, 3, 5, 7) for f in _factors(SJ)):
+        SJ += 1
+    if not all(f in (2, 3, 5, 7) for f in _factors(M)):
+        return None
+    N = int(rng.integers(2, 400))
+    return M, P, L, Lsq, xi, n_l, S0, SI, SJ, N, int(rng.integers(1, 10 ** 6))
+
+
 def test_random_configurations_match_oracle():
-    """Seeded random valid configurations (M, P, box aspect, xi, n_l, extents, N): element-wise
-    parity with the Alg. 1 oracle -- catches index/tiling assumptions the named cases miss."""
+    """40 seeded random valid configurations (M, P, box aspect incl. rectangular cross-sections
+    against the square-embedding oracle, reading R-19, xi, n_l, extents, N): element-wise parity
+    with the Alg. 1 oracle; every 4th also the field, and the SE3P path where it applies."""
     rng = np.random.default_rng(2024)
     checked = 0
-    while checked < 12:
-        M = int(rng.choice([8, 10, 12, 14, 16, 20, 24, 30, 32, 36, 40, 48]))
-        P = int(rng.integers(2, min(M, 28) + 1))
-        L3 = float(rng.choice([0.5, 1.0, 1.5, 2.0]))
-        m1 = int(rng.choice([M // 2, M, (3 * M) // 2])) if M % 2 == 0 else M
-        h = L3 / M
-        L = (m1 * h, m1 * h, L3)
-        xi = float(rng.uniform(2.0, 9.0)) / max(L)
-        eta = P * xi ** 2 * h ** 2 / (0.95 ** 2 * math.pi)
-        if not (0.05 < eta < 0.95):
+    while checked < 40:
+        c = _random_config(rng)
+        if c is None:
             continue
-        Mt = m1 + P
-        n_l = int(rng.integers(0, M // 2 + 1))
-        S0 = int(Mt * rng.uniform(2.5, 4.0))
-        SI = int(Mt * rng.uniform(1.0, 3.0)) if n_l else Mt
-        SJ = int(rng.integers(Mt, 2 * Mt))
-        while not all(f in (2, 3, 5, 7) for f in _factors(SJ)):
-            SJ += 1
-        if not all(f in (2, 3, 5, 7) for f in _factors(M)):
-            continue
-        N = int(rng.integers(2, 400))
-        x, q = make_system(N, L, int(rng.integers(1, 10 ** 6)))
-        ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+        M, P, L, Lsq, xi, n_l, S0, SI, SJ, N, seed = c
+        x, q = make_system(N, L, seed)
+        ref = sd.se1p_kspace(x, q, Lsq, xi, M, P, n_l, S0, SI, SJ)
         got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
         err = np.max(np.abs(got - ref))
         assert err <= 1e-11 * np.max(np.abs(ref)), (M, P, L, xi, n_l, S0, SI, SJ, N, err)
+        if checked % 4 == 0:
+            _, Eref = sd.se1p_kspace(x, q, Lsq, xi, M, P, n_l, S0, SI, SJ, return_field=True)
+            xd, qd = _dev(x, q)
+            _, E = se1p.kspace(xd, qd, L, xi, M, P, n_local=n_l, S0=S0, SI=SI, Ntilde=SJ, field=True)
+            assert np.max(np.abs(E.cpu().numpy() - Eref)) <= 1e-11 * np.max(np.abs(Eref)), ("field", c)
+            if P % 2 == 0 and L[0] == L[1] == L[2]:
+                from oracle import se3p_discrete as s3
+                r3 = s3.se3p_kspace(x, q, L, xi, M, P)
+                g3 = se1p.kspace3p(xd, qd, L, xi, M, P).cpu().numpy()
+                assert np.max(np.abs(g3 - r3)) <= 1e-11 * np.max(np.abs(r3)), ("3p", c)
         checked += 1
+
+
+@pytest.mark.parametrize("M,P,N,L3", [(64, 24, 20000, 1.0), (96, 23, 30000, 2.0)])
+def test_large_sweeps_match_oracle(M, P, N, L3):
+    """Sizes where the sweep kernels run many batches per group (BM-sized pieces, carried k-step
+    entries), several periodic-axis chunks per column tile (overhang added to the next chunk) and
+    many work items per CTA: element-wise parity with the Alg. 1 oracle."""
+    L = (L3 * 64 / M, L3 * 64 / M, L3) if M != 64 else (1.0, 1.0, 1.0)
+    h = L[2] / M
+    Mt = int(round(L[0] / h)) + P
+    xi = 12.0 / L[0]
+    x, q = make_system(N, L, 77 + M)
+    n_l, S0, SI, SJ = 4, 4 * Mt, 3 * Mt, Mt + (Mt % 2)
+    while not all(f in (2, 3, 5, 7) for f in _factors(SJ)):
+        SJ += 1
+    ref = sd.se1p_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    got = _gpu_kspace(x, q, L, xi, M, P, n_l, S0, SI, SJ)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
 
 
 def _factors(n):
