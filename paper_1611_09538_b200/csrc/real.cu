@@ -78,44 +78,61 @@ __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restr
         const double shift = w * d.L[2];
         const int c = (ax * d.nc[1] + ay) * d.nc[2] + az;
         const int s = cell_start[c], e = cell_start[c + 1];
-        for (int j = s; j < e; ++j) {
-          if (w == 0 && j == t) continue;   // the prime in Eq. (3): n = m only at p = 0
-          const double4 ps = P4[j];
-          const double dx = pt.x - ps.x, dy = pt.y - ps.y, dz = pt.z - (ps.z + shift);
-          const double r2 = dx * dx + dy * dy + dz * dz;
-          if (r2 <= rc2) {
-#if SE1P_REAL_TABLE
-            // erfc(xi r) from the local polynomial of r's interval (no erfc, exp or division)
-            const double rinv = rsqrt(r2), r = r2 * rinv;
-            const int it = min((int)(r * d.inv_dr), kTabN - 1);
-            const double u = r - ((double)it + 0.5) * d.dr;
-            const double* cf = d.tab + it * (kTabDeg + 1);
-            double pv = __ldg(cf + kTabDeg), dv = 0.0;
+        // candidates two at a time: both positions are loaded before either is used
+        for (int j = s; j < e; j += 2) {
+          const bool two = j + 1 < e;
+          const double4 pa = P4[j];
+          const double4 pb = two ? P4[j + 1] : pa;
 #pragma unroll
-            for (int k = kTabDeg - 1; k >= 0; --k) {
-              if (FIELD) dv = fma(dv, u, pv);
-              pv = fma(pv, u, __ldg(cf + k));
-            }
-            const double ec = pv * rinv;
-            acc = fma(ps.w, ec, acc);
-            if (FIELD) {   // dv = d/dr erfc(xi r) = -(2 xi/sqrt(pi)) e^{-xi^2 r^2}
-              const double g = ps.w * (ec - dv) * (rinv * rinv);
-              ex = fma(g, dx, ex);
-              ey = fma(g, dy, ey);
-              ez = fma(g, dz, ez);
-            }
+          for (int h2 = 0; h2 < 2; ++h2) {
+            if (h2 == 1 && !two) break;
+            const int jj = j + h2;
+            const double4 ps = h2 ? pb : pa;
+            if (w == 0 && jj == t) continue;   // the prime in Eq. (3): n = m only at p = 0
+            const double dx = pt.x - ps.x, dy = pt.y - ps.y, dz = pt.z - (ps.z + shift);
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 <= rc2) {
+#if SE1P_REAL_TABLE
+              // erfc(xi r) from the local polynomial of r's interval (no erfc, exp or division)
+              const double rinv = rsqrt(r2), r = r2 * rinv;
+              const int it = min((int)(r * d.inv_dr), d.ntab - 1);
+              const double u = r - ((double)it + 0.5) * d.dr;
+              const double2* cf = reinterpret_cast<const double2*>(d.tab + it * (kTabDeg + 1));
+              const double2 c67 = __ldg(cf + 3), c45 = __ldg(cf + 2), c23 = __ldg(cf + 1), c01 = __ldg(cf);
+              double pv = fma(c67.y, u, c67.x);
+              pv = fma(pv, u, c45.y);
+              pv = fma(pv, u, c45.x);
+              pv = fma(pv, u, c23.y);
+              pv = fma(pv, u, c23.x);
+              pv = fma(pv, u, c01.y);
+              const double ec = fma(pv, u, c01.x) * rinv;
+              acc = fma(ps.w, ec, acc);
+              if (FIELD) {   // dv = d/dr erfc(xi r) = -(2 xi/sqrt(pi)) e^{-xi^2 r^2}
+                double dv = 7.0 * c67.y;
+                dv = fma(dv, u, 6.0 * c67.x);
+                dv = fma(dv, u, 5.0 * c45.y);
+                dv = fma(dv, u, 4.0 * c45.x);
+                dv = fma(dv, u, 3.0 * c23.y);
+                dv = fma(dv, u, 2.0 * c23.x);
+                dv = fma(dv, u, c01.y);
+                const double g = ps.w * (ec - dv) * (rinv * rinv);
+                ex = fma(g, dx, ex);
+                ey = fma(g, dy, ey);
+                ez = fma(g, dz, ez);
+              }
 #else
-            const double r = sqrt(r2);
-            const double ec = erfc(d.xi * r) / r;
-            acc = fma(ps.w, ec, acc);
-            if (FIELD) {
-              const double g = ps.w * (ec + 1.128379167095512573896158903121545172 * d.xi *   // 2/sqrt(pi)
-                                                exp(-d.xi * d.xi * r2)) / r2;
-              ex = fma(g, dx, ex);
-              ey = fma(g, dy, ey);
-              ez = fma(g, dz, ez);
-            }
+              const double r = sqrt(r2);
+              const double ec = erfc(d.xi * r) / r;
+              acc = fma(ps.w, ec, acc);
+              if (FIELD) {
+                const double g = ps.w * (ec + 1.128379167095512573896158903121545172 * d.xi *   // 2/sqrt(pi)
+                                                  exp(-d.xi * d.xi * r2)) / r2;
+                ex = fma(g, dx, ex);
+                ey = fma(g, dy, ey);
+                ez = fma(g, dz, ez);
+              }
 #endif
+            }
           }
         }
       }
@@ -150,12 +167,12 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
 
 // Taylor coefficients of erfc(xi r) about the interval midpoints r_i = (i + 1/2) dr:
 // d^n/dx^n erfc(x) = (-1)^n (2/sqrt(pi)) H_{n-1}(x) e^{-x^2} (physicists' Hermite polynomials),
-// evaluated in long double; term n carries xi^n/n!.  Interval half-width xi dr/2 <= 0.013 for
-// xi rc <= 6.6, so the degree-10 remainder is below 1e-25 relative to the leading term.
-static std::vector<double> erfc_table(double xi, double rc) {
-  std::vector<double> t((size_t)kTabN * (kTabDeg + 1));
-  const long double dr = (long double)rc / kTabN, two_over_sqrtpi = 1.128379167095512573896158903121545172L;
-  for (int i = 0; i < kTabN; ++i) {
+// evaluated in long double; term n carries xi^n/n!.  The interval count (real.cuh) keeps the
+// degree-7 remainder below 1e-16 relative to erfc itself.
+static std::vector<double> erfc_table(double xi, double rc, int ntab) {
+  std::vector<double> t((size_t)ntab * (kTabDeg + 1));
+  const long double dr = (long double)rc / ntab, two_over_sqrtpi = 1.128379167095512573896158903121545172L;
+  for (int i = 0; i < ntab; ++i) {
     const long double x0 = (long double)xi * ((long double)i + 0.5L) * dr;
     const long double g = two_over_sqrtpi * expl(-x0 * x0);
     long double hm1 = 0.0L, h = 1.0L;   // H_{-1} (unused), H_0
@@ -178,6 +195,7 @@ static std::vector<double> erfc_table(double xi, double rc) {
 struct TabCache {
   double xi = 0, rc = 0;
   double* dev = nullptr;
+  int64_t cap = 0;
 };
 static TabCache g_tab[64];
 
@@ -195,17 +213,26 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     int dev = 0;
     SE1P_CUDA_TRY(cudaGetDevice(&dev));
     TabCache& tc = g_tab[dev & 63];
+    const int ntab = real_table_intervals(d.xi, d.rc);
     if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
-      const std::vector<double> t = erfc_table(d.xi, d.rc);
-      if (!tc.dev) dev_alloc(tc.dev, t.size());
+      const std::vector<double> t = erfc_table(d.xi, d.rc, ntab);
+      if (tc.dev && tc.cap < (int64_t)t.size()) {
+        dev_free(tc.dev);
+        tc.dev = nullptr;
+      }
+      if (!tc.dev) {
+        dev_alloc(tc.dev, t.size());
+        tc.cap = (int64_t)t.size();
+      }
       SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
       SE1P_CUDA_TRY(cudaStreamSynchronize(st));
       tc.xi = d.xi;
       tc.rc = d.rc;
     }
     d.tab = tc.dev;
-    d.dr = d.rc / kTabN;
-    d.inv_dr = kTabN / d.rc;
+    d.ntab = ntab;
+    d.dr = d.rc / ntab;
+    d.inv_dr = ntab / d.rc;
   }
 #endif
   const int ncell = d.nc[0] * d.nc[1] * d.nc[2];

@@ -14,11 +14,19 @@ struct RDev {
   int K;          // periodic-axis cell reach
   int Kx, Ky;     // free-axis cell reach (cells are >= rc/D wide)
   double xi, rc;
-  // erfc(xi r) on [0, rc] as kTabN local Taylor polynomials of degree kTabDeg in r - r_mid
+  // erfc(xi r) on [0, rc] as ntab local Taylor polynomials of degree kTabDeg in r - r_mid
   const double* tab = nullptr;
+  int ntab = 0;
   double inv_dr = 0.0, dr = 0.0;
 };
-constexpr int kTabN = 256, kTabDeg = 10;
+// degree 7 (8 coefficients, four 16-byte loads per pair); the interval count grows with
+// X = xi rc so that the remainder (2 X dx)^8/8! (dx the interval half-width in xi r) stays
+// below 1e-16 relative: ntab = X^2 / 0.03 (C5: 300 intervals, 19 KB)
+constexpr int kTabDeg = 7;
+inline int real_table_intervals(double xi, double rc) {
+  const double X = xi * rc;
+  return std::min(8192, std::max(64, (int)std::ceil(X * X / 0.03)));
+}
 
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
