@@ -96,8 +96,11 @@ struct SweepArgs {
   int n_items, C, nzc, BM, NB;
 };
 
+// list capacity per (slot, consumer warp): a batch's entries plus the k-step padding
+__host__ __device__ constexpr int sw_ls(int BM) { return BM + 8; }
+
 struct SweepSmem {
-  int off_meta, off_mask, off_lists, off_raw, off_rows, off_acc, off_ring, total;
+  int off_meta, off_mask, off_lists, off_lcnt, off_cb, off_raw, off_rows, off_acc, off_ring, total;
 };
 
 // barriers: full, empty, (unused) [kMaxNB], rawb, rawfree [kNR]; headers hdr [kMaxNB], bhdr [kNR]
@@ -112,8 +115,13 @@ __host__ __device__ inline SweepSmem sweep_smem(int BM, int NB, int NZB, bool ga
   s.off_mask = o;
   o += (NB * BM + 1) * 4;
   o = (o + 15) & ~15;
-  s.off_lists = o;
-  o += kCW * (BM + 24) * 4;
+  s.off_lists = o;   // per-slot consumer lists, written by the expanders
+  o += NB * kCW * sw_ls(BM) * 2;
+  o = (o + 15) & ~15;
+  s.off_lcnt = o;
+  o += NB * kCW * 4;
+  s.off_cb = o;      // per-warp carry lists
+  o += kCW * 16 * 2;
   o = (o + 127) & ~127;
   s.off_raw = o;
   o += kNR * BM * rec_stride(NZB) * 8;
@@ -154,20 +162,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
       : "memory");
   return ok != 0;
 }
-// consumers' waits for a batch: try_wait with a suspend-time hint (ns; 0: the hardware default), so
-// waiting warps leave the issue slots to the expanders
-#ifndef SE1P_SWEEP_WAIT_NS
-#define SE1P_SWEEP_WAIT_NS 0
-#endif
-__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* b, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity), "n"(SE1P_SWEEP_WAIT_NS > 0 ? SE1P_SWEEP_WAIT_NS : 1)
-      : "memory");
-  return ok != 0;
-}
 // SE1P_SWEEP_WATCHDOG (debug builds): report and trap a wait that never completes
 #ifndef SE1P_SWEEP_WATCHDOG
 #define SE1P_SWEEP_WATCHDOG 0
@@ -188,6 +182,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, int tag 
 #endif
 }
 
+// SE1P_SWEEP_TRACE (experiment builds): CTA 0's per-batch timeline (clock64): producer post,
+// expander sees the records / a free slot / arrives full, consumer warp 0 sees full / arrives empty,
+// its k-steps and the batch size, then consumer checkpoints; read with se1p_sweep_trace
+#ifndef SE1P_SWEEP_TRACE
+#define SE1P_SWEEP_TRACE 0
+#endif
+#if SE1P_SWEEP_TRACE
+constexpr int kTraceN = 8192, kTraceF = 12;
+__device__ long long g_trace[2][kTraceN][kTraceF];   // [gridding, gather]
+#define SW_TRACE(k, i, v) \
+  if (blockIdx.x == 0 && (k) < kTraceN) g_trace[GATHER][k][i] = (v)
+#define SW_CTRACE(i) \
+  if (w == 0 && lane == 0) SW_TRACE(kc, i, clock64())
+#else
+#define SW_TRACE(k, i, v)
+#define SW_CTRACE(i)
+#endif
+
 template <bool GATHER, int FM, int NZB>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   constexpr int RD = rec_stride(NZB), RS = row_stride(NZB), R = sw_R(NZB), S = sw_S(NZB);
@@ -195,6 +207,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   constexpr int NCT = FM ? 4 : 1;                 // values per gather slot
   constexpr int COFF = FM == 2 ? 3 : 0;           // first slot value of this pass
   constexpr int ACS = kCW * NC + 1;               // acc doubles per candidate (odd: conflict-free reduce)
+  constexpr bool XL = GATHER;                     // consumer lists built by the expanders
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
@@ -208,7 +221,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   double* f1 = reinterpret_cast<double*>(smem + kSmemHead);
   int4* meta = reinterpret_cast<int4*>(smem + L.off_meta);
   int* mask = reinterpret_cast<int*>(smem + L.off_mask);
-  int* lists = reinterpret_cast<int*>(smem + L.off_lists);
+  unsigned short* lists = reinterpret_cast<unsigned short*>(smem + L.off_lists);
+  int* lcnt = reinterpret_cast<int*>(smem + L.off_lcnt);
+  const int LS = sw_ls(BM);
   double* raw = reinterpret_cast<double*>(smem + L.off_raw);
   double* rows = reinterpret_cast<double*>(smem + L.off_rows);
   double* acc = reinterpret_cast<double*>(smem + L.off_acc);
@@ -256,6 +271,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       if (lane == 0) {
         bhdr[b] = h;
         mbar_arrive(&rawb[b]);
+        SW_TRACE(k, 0, clock64());
       }
       __syncwarp();
       ++k;
@@ -373,6 +389,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
     for (int k = gi;; k += kEG) {
       const int b = k % NB, r = k % kNR;
       mbar_wait(&rawb[r], (unsigned)((k / kNR) & 1), 300000 + k);
+      if (gw == 0 && lane == 0) SW_TRACE(k, 1, clock64());
       const int4 h = bhdr[r];
       if (h.w & kKernelEnd) {   // drain this group's unreduced batches; end marker 0 goes to the consumers
         if (GATHER)
@@ -396,6 +413,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
           mbar_wait(&empty[b], (unsigned)(((k - NB) / NB) & 1), 600000 + k);
         }
       }
+      if (gw == 0 && lane == 0) SW_TRACE(k, 2, clock64());
       if (h.z > 0) {
         int X0, Y0, Z0, Ck, zc;
         item_geom(h.x, X0, Y0, Z0, Ck, zc);
@@ -455,13 +473,34 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
             zd[(sc & ~3) | ((sc & 3) ^ zk)] = zs[sc];
           }
         }
+        // gather: the consumer lists of this batch (candidate order), warp gw builds those of
+        // consumers gw, gw + 4, gw + 8, gw + 12 once the group's masks are all written (gridding:
+        // the consumers build their own, the expanders being the slower side there)
+        if (XL) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "n"(kGW * 32) : "memory");
+        unsigned short* Lb = lists + b * kCW * LS;
+        int nl[4] = {0, 0, 0, 0};
+        const unsigned lt = (1u << lane) - 1u;
+        for (int p0 = 0; p0 < h.z; p0 += 32) {
+          const int p = p0 + lane;
+          const int m = p < h.z ? mask[b * BM + p] : 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool rel = (m >> (gw + 4 * i)) & 1;
+            const unsigned bal = __ballot_sync(0xffffffffu, rel);
+            if (rel) Lb[(gw + 4 * i) * LS + nl[i] + __popc(bal & lt)] = (unsigned short)(b * BM + p);
+            nl[i] += __popc(bal);
+          }
+        }
+        if (lane < 4) lcnt[b * kCW + gw + 4 * lane] = lane == 0 ? nl[0] : lane == 1 ? nl[1] : lane == 2 ? nl[2] : nl[3];
+        }
       }
       if (gw == 0 && lane == 0) hdr[b] = h;
-      __threadfence_block();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&rawfree[r]);
         mbar_arrive(&full[b]);
+        if (gw == 0) SW_TRACE(k, 3, clock64());
       }
     }
     return;
@@ -476,7 +515,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   // gridding: B lane g holds frame node sg = (g >> 1) + 4 (g & 1), so C lane tg holds nodes tg, tg + 4;
   // gather: K index tg (tg + 4) of block j is node 2 tg (2 tg + 1): one 16-byte pair of the record
   const int sg = (g >> 1) + 4 * (g & 1);
-  int* wl = lists + w * (BM + 24);
+  unsigned short* cb = reinterpret_cast<unsigned short*>(smem + L.off_cb) + w * 16;   // carried entries
   double* rg = ring + w * 16 * S;   // gridding ring [16 cols][S]
 
   int cur = -1, X0 = 0, Y0 = 0, Z0 = 0, Ck = 0, zc = 0;
@@ -527,20 +566,23 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
     }
   };
   // gather: the frame operand A[j] = H~[cols g, g+8][nodes a + 8j + 2 tg (+1)]
+  // (column pointers gp0, gp1 of cols g, g + 8 set per item; null outside the grid)
+  const double* gp0 = nullptr;
+  const double* gp1 = nullptr;
   auto frame_load_gather = [&]() {
+    const int zb = Z0 + u + 2 * tg;
 #pragma unroll
     for (int j = 0; j < NZB; ++j)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int col = g + 8 * (v & 1);
-        const int x = X0 + 4 * bxw + (col >> 2), y = Y0 + 4 * byw + (col & 3);
-        int z = Z0 + u + 8 * j + 2 * tg + (v >> 1);
-        while (z >= M) z -= M;
-        c[j][v] = (x < Mt && y < Mt) ? __ldg(A.grid + ((int64_t)x * Mt + y) * M + z) : 0.0;
+      for (int s = 0; s < 2; ++s) {
+        int z = zb + 8 * j + s;
+        z = z >= M ? z - M : z;   // z < 2 M
+        c[j][2 * s] = gp0 ? __ldg(gp0 + z) : 0.0;
+        c[j][2 * s + 1] = gp1 ? __ldg(gp1 + z) : 0.0;
       }
   };
 
-  auto ksteps = [&](int k0, int k1) {
+  auto ksteps = [&](const unsigned short* wl, int k0, int k1) {
 #ifdef SE1P_SWEEP_EXP_NO_KSTEPS   // experiment build: the staging and bookkeeping floor
     return;
 #endif
@@ -605,13 +647,15 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   };
 
   int held = 0, bprev = -1;
+#if SE1P_SWEEP_TRACE
+  int kc = -1;
+#endif
   for (int b = 0, ph = 0;; b = (b + 1 == NB) ? 0 : b + 1, ph ^= (b == 0)) {
-    if (SE1P_SWEEP_WAIT_NS > 0 && !SE1P_SWEEP_WATCHDOG) {
-      while (!mbar_try_wait_hint(&full[b], (unsigned)ph)) {
-      }
-    } else {
-      mbar_wait(&full[b], (unsigned)ph, 400000 + b);
-    }
+    mbar_wait(&full[b], (unsigned)ph, 400000 + b);
+#if SE1P_SWEEP_TRACE
+    ++kc;
+#endif
+    SW_CTRACE(4);
     const int4 h = hdr[b];
     if (h.w & kKernelEnd) {
       __syncwarp();
@@ -626,6 +670,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       item_geom(cur, X0, Y0, Z0, Ck, zc);
       flushed = 0;
       fr = false;
+      if (GATHER) {
+        const int x0 = X0 + 4 * bxw + (g >> 2), x1 = x0 + 2, y = Y0 + 4 * byw + (g & 3);
+        gp0 = (x0 < Mt && y < Mt) ? A.grid + ((int64_t)x0 * Mt + y) * M : nullptr;
+        gp1 = (x1 < Mt && y < Mt) ? A.grid + ((int64_t)x1 * Mt + y) * M : nullptr;
+      }
     }
     if (h.w & kItemEnd) {
       if (!GATHER) {
@@ -649,24 +698,31 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       }
       fr = false;
     }
-    // this warp's candidates of the batch (order preserving), after the carried ones
-    int n = held;
-    const int cn = h.z;
-    for (int p0 = 0; p0 < cn; p0 += 32) {
-      const int p = p0 + lane;
-      const bool rel = p < cn && ((mask[b * BM + p] >> w) & 1);
-      const unsigned bal = __ballot_sync(0xffffffffu, rel);
-      if (rel) wl[n + __popc(bal & ((1u << lane) - 1u))] = b * BM + p;
-      n += __popc(bal);
+    // this warp's list of the batch (built by the expanders), after the held entries: positions
+    // [0, held) are cb, [held, tot) are L
+    SW_CTRACE(8);
+    unsigned short* Lw = lists + (b * kCW + w) * LS;
+    int n = 0;
+    if (XL) {
+      n = lcnt[b * kCW + w];
+    } else {
+      for (int p0 = 0; p0 < h.z; p0 += 32) {
+        const int p = p0 + lane;
+        const bool rel = p < h.z && ((mask[b * BM + p] >> w) & 1);
+        const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        if (rel) Lw[n + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(b * BM + p);
+        n += __popc(bal);
+      }
+      __syncwarp();
     }
-    if (lane == 0 && n > BM + 8) atomicOr(dv.err, 2);
-    __syncwarp();
+    const int tot = held + n;
+    SW_CTRACE(9);
     // k-steps of 8 entries; the group's last batch pads and runs everything, and so does a batch
-    // that cannot fill one k-step on top of carried entries (at most one batch is ever held)
-    int kend = n & ~7;
+    // that cannot fill one k-step on top of held entries (at most one batch is ever held)
+    int kend = tot & ~7;
     if ((h.w & kLast) || (held > 0 && kend == 0)) {
-      kend = (n + 7) & ~7;
-      if (lane < kend - n) wl[n + lane] = dummy;
+      kend = (tot + 7) & ~7;
+      if (lane < kend - tot) Lw[n + lane] = (unsigned short)dummy;
       __syncwarp();
     }
     if (kend > 0) {
@@ -675,19 +731,23 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         else frame_io(false);
         fr = true;
       }
-      ksteps(0, 8);
-      if (bprev >= 0) {   // the carried entries (all in the first k-step) named batch bprev
-        __threadfence_block();
+      if (held > 0) {   // one mixed k-step: the held entries (batch bprev), then this batch's first
+        if (lane >= held && lane < 8) cb[lane] = Lw[lane - held];
+        __syncwarp();
+        ksteps(cb, 0, 8);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[bprev]);
         bprev = -1;
+        ksteps(Lw + 8 - held, 0, kend - 8);
+      } else {
+        ksteps(Lw, 0, kend);
       }
-      ksteps(8, kend);
     }
-    const int rest = max(n - kend, 0);   // < 8, all from this batch (none after padding)
-    const int mv = lane < rest ? wl[kend + lane] : 0;
+    SW_CTRACE(10);
+    const int rest = max(tot - kend, 0);   // < 8, all from this batch (none after padding)
+    const int mv = lane < rest ? Lw[kend - held + lane] : 0;
     __syncwarp();
-    if (lane < rest) wl[lane] = mv;
+    if (lane < rest) cb[lane] = (unsigned short)mv;
     held = rest;
     if (h.w & kLast) {
       if (!GATHER && fr) {
@@ -696,15 +756,28 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       }
       fr = false;
     }
-    __threadfence_block();
+    SW_CTRACE(11);
     __syncwarp();
     if (held == 0) {
       if (lane == 0) mbar_arrive(&empty[b]);
     } else {
       bprev = b;
     }
+#if SE1P_SWEEP_TRACE
+    if (w == 0 && lane == 0) {
+      SW_TRACE(kc, 5, clock64());
+      SW_TRACE(kc, 6, kend / 8);
+      SW_TRACE(kc, 7, h.z);
+    }
+#endif
   }
 }
+
+#if SE1P_SWEEP_TRACE
+extern "C" int se1p_sweep_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
+}
+#endif
 
 // Overhang: the P-1 positions past each chunk belong to the next chunk (periodic in z); every
 // position receives at most one overhang (chunks hold >= P-1 nodes), so the adds do not race.
