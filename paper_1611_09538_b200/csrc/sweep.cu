@@ -33,6 +33,7 @@
 // No floating-point atomics: each grid point is written by one warp; the gather's partials go
 // to fixed slots summed in a fixed order (k_gather_finish) -> bitwise reproducible.
 #include <cstdint>
+#include <type_traits>
 #include <vector>
 
 #include "tiles.cuh"
@@ -51,6 +52,11 @@ constexpr int kMaxNB = 4;
 #define SE1P_SWEEP_NB 4
 #endif
 constexpr int kNB = SE1P_SWEEP_NB;
+// gather k-steps issued together (1 or 2)
+#ifndef SE1P_SWEEP_GU
+#define SE1P_SWEEP_GU 1
+#endif
+constexpr int kGU = SE1P_SWEEP_GU;
 constexpr int kMaxP = 64;
 
 // header flags of a batch
@@ -600,49 +606,80 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         for (int j = 0; j < NZB; ++j) dmma_16x8x8(c[j], a, z0[8 * j], z1[8 * j]);
       }
     } else {
-      for (int k = k0; k < k1; k += 8) {
-        const int e = wl[k + g];
-        const double* z = rows + e * RS + kZ + ((2 * tg) ^ (e & 2));
-        double t[4] = {0.0, 0.0, 0.0, 0.0};
+      // U k-steps at once (independent chains); T[col g (+8)][particle 2tg (+1)] of k-step u gives
+      // the particle's column partial wy (wx T + wx' T'), summed over the 8 g lanes by a
+      // transposing butterfly: each round halves the values a lane holds, so lane g < 2U ends
+      // with the full sum of particle 2tg + (g & 1) of k-step g >> 1
+      auto gstep = [&](auto uc, int k) {
+        constexpr int U = decltype(uc)::value;
+        double t[U][4];
+        int ee[U][2];
 #pragma unroll
-        for (int j = 0; j < NZB; ++j) {
-          const double2 bb = *reinterpret_cast<const double2*>(z + 8 * j);
-          dmma_16x8x8(t, c[j], bb.x, bb.y);
-        }
-        // T[col g (+8)][particle 2tg (+1)]: phi_p += wy (wx T + wx' T')
-        const int ea = wl[k + 2 * tg], eb = wl[k + 2 * tg + 1];
-        const double* ra = rows + ea * RS;
-        const double* rb2 = rows + eb * RS;
-        const int sa = ea & 6, sb = eb & 6, ya = 16 + (yq ^ sa), yb2 = 16 + (yq ^ sb);
-        double va[NC], vb[NC];
-        {
-          const double wxa = ra[xa ^ sa], wxa2 = ra[(xa + 2) ^ sa], wya = ra[ya];
-          const double wxb = rb2[xa ^ sb], wxb2 = rb2[(xa + 2) ^ sb], wyb = rb2[yb2];
-          va[0] = wya * fma(wxa, t[0], wxa2 * t[2]);
-          vb[0] = wyb * fma(wxb, t[1], wxb2 * t[3]);
-          if (FM == 1) {   // column moments in tile coordinates (x: xa, xa + 2; y: yb)
-            const double cx = (double)xa;
-            va[1] = wya * fma(cx * wxa, t[0], (cx + 2.0) * wxa2 * t[2]);
-            vb[1] = wyb * fma(cx * wxb, t[1], (cx + 2.0) * wxb2 * t[3]);
-            va[2] = (double)yb * va[0];
-            vb[2] = (double)yb * vb[0];
+        for (int uu = 0; uu < U; ++uu) {
+          const int e = wl[k + 8 * uu + g];
+          const double* z = rows + e * RS + kZ + ((2 * tg) ^ (e & 2));
+          t[uu][0] = t[uu][1] = t[uu][2] = t[uu][3] = 0.0;
+#pragma unroll
+          for (int j = 0; j < NZB; ++j) {
+            const double2 bb = *reinterpret_cast<const double2*>(z + 8 * j);
+            dmma_16x8x8(t[uu], c[j], bb.x, bb.y);
           }
+          ee[uu][0] = wl[k + 8 * uu + 2 * tg];
+          ee[uu][1] = wl[k + 8 * uu + 2 * tg + 1];
         }
+        double v[U][2][NC];
 #pragma unroll
-        for (int cc = 0; cc < NC; ++cc)
+        for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            va[cc] += __shfl_xor_sync(0xffffffffu, va[cc], o);
-            vb[cc] += __shfl_xor_sync(0xffffffffu, vb[cc], o);
+          for (int pb = 0; pb < 2; ++pb) {
+            const int ep = ee[uu][pb];
+            const double* rp = rows + ep * RS;
+            const int sp = ep & 6;
+            const double wx = rp[xa ^ sp], wx2 = rp[(xa + 2) ^ sp], wy = rp[16 + (yq ^ sp)];
+            const double tp = t[uu][pb], tp2 = t[uu][pb + 2];
+            v[uu][pb][0] = wy * fma(wx, tp, wx2 * tp2);
+            if (FM == 1) {   // column moments in tile coordinates (x: xa, xa + 2; y: yb)
+              const double cx = (double)xa;
+              v[uu][pb][1] = wy * fma(cx * wx, tp, (cx + 2.0) * wx2 * tp2);
+              v[uu][pb][2] = (double)yb * v[uu][pb][0];
+            }
           }
-        if (g == 0) {
+        // round 1 (lanes g ^ 1): keep particle (g & 1) of each k-step
+        const bool b1 = g & 1;
+        double r1[U][NC];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu)
 #pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
-            acc[(int64_t)ea * ACS + w * NC + cc] = va[cc];
-            acc[(int64_t)eb * ACS + w * NC + cc] = vb[cc];
+            const double send = b1 ? v[uu][0][cc] : v[uu][1][cc];
+            const double keep = b1 ? v[uu][1][cc] : v[uu][0][cc];
+            r1[uu][cc] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
           }
+        double x[NC];
+        if (U == 2) {   // round 2 (lanes g ^ 2): keep k-step (g >> 1) & 1
+          const bool b2 = (g >> 1) & 1;
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            const double send = b2 ? r1[0][cc] : r1[U - 1][cc];
+            const double keep = b2 ? r1[U - 1][cc] : r1[0][cc];
+            x[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) x[cc] = r1[0][cc] + __shfl_xor_sync(0xffffffffu, r1[0][cc], 8);
         }
-      }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) x[cc] += __shfl_xor_sync(0xffffffffu, x[cc], 16);
+        if (g < 2 * U) {
+          const int uu = g >> 1;
+          const int ep = (uu == 0) ? (b1 ? ee[0][1] : ee[0][0]) : (b1 ? ee[U - 1][1] : ee[U - 1][0]);
+#pragma unroll
+          for (int cc = 0; cc < NC; ++cc) acc[(int64_t)ep * ACS + w * NC + cc] = x[cc];
+        }
+      };
+      int k = k0;
+      for (; k + 16 <= k1 && kGU == 2; k += 16) gstep(std::integral_constant<int, kGU>(), k);
+      for (; k < k1; k += 8) gstep(std::integral_constant<int, 1>(), k);
     }
   };
 

@@ -1,11 +1,11 @@
 """Stall-reason sums per source-line range of the first kernel in an ncu report (needs -lineinfo).
-    python tools/ncu_stalls.py report.ncu-rep name:lo-hi [name:lo-hi ...] [--kernel N]"""
+    python tools/ncu_stalls.py report.ncu-rep name:lo-hi [name:lo-hi ...] [--kernel substring] [--lines lo-hi]"""
 import csv
 import subprocess
 import sys
 
 rep, specs = sys.argv[1], [a for a in sys.argv[2:] if ":" in a]
-kidx = int(sys.argv[sys.argv.index("--kernel") + 1]) if "--kernel" in sys.argv else 0
+ksel = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else ""
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout.splitlines()
 blocks, cur = [], None
@@ -16,7 +16,7 @@ for line in out:
     elif cur is not None:
         cur["rows"].append(line)
 big = sorted(blocks, key=lambda b: -len(b["rows"]))
-f = [b for b in blocks if len(b["rows"]) > 100][kidx]
+f = max([b for b in blocks if ksel in b["name"]], key=lambda b: len(b["rows"]))   # the kernel's own file
 rows = list(csv.reader(f["rows"]))
 hdr = rows[0]
 cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
