@@ -38,6 +38,30 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 static int rows_for(int W) { int r = SE1P_ROW_SMEM / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? SE1P_COLS_LARGE : SE1P_COLS_SMALL; }
 constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT passes
+#ifndef SE1P_FFT_MINB
+#define SE1P_FFT_MINB 4
+#endif
+#define SE1P_FFT_LB __launch_bounds__(SE1P_FFT_THREADS, SE1P_FFT_MINB)
+
+// Global -> shared copies with U independent loads in flight per thread (a plain strided loop
+// waits out one load latency per element): st(i, ld(i)) for i in [0, n).
+template <int U, class T, class LD, class ST>
+__device__ __forceinline__ void copy_batched(int n, int tid, int nthr, LD ld, ST st) {
+  for (int b = tid; b < n; b += U * nthr) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + u * nthr;
+      if (i < n) v[u] = ld(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + u * nthr;
+      if (i < n) st(i, v[u]);
+    }
+  }
+}
+constexpr int kLdU = 8;
 
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
 // Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if
@@ -47,7 +71,7 @@ constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT 
 // CB (columns per block) is a template constant and M's log2 (or -1) is passed, so the index
 // splits below are shifts, not integer divisions by runtime values.
 template <int CB>
-__global__ void k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LB k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
@@ -58,10 +82,17 @@ __global__ void k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
   const double* src = grid + ((int64_t)x * Mt + y0) * M;
   double* bd = reinterpret_cast<double*>(buf);
-  for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
-    const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
-    bd[2 * ((c >> 1) * S + k) + (c & 1)] = (y0 + c < Mt) ? src[idx] : 0.0;
-  }
+  const int ncol = min(CB, Mt - y0);
+  copy_batched<kLdU, double>(
+      CB * M, threadIdx.x, blockDim.x,
+      [&](int idx) {
+        const int c = mshift >= 0 ? idx >> mshift : idx / M;
+        return c < ncol ? __ldg(src + idx) : 0.0;
+      },
+      [&](int idx, double v) {
+        const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
+        bd[2 * ((c >> 1) * S + k) + (c & 1)] = v;
+      });
   __syncthreads();
   double2* out = fft_rows<-1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
@@ -78,7 +109,7 @@ __global__ void k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const
 // Inverse: the Hermitian spectra a, b of columns 2r, 2r+1 combine into W[n] = a[n] + i b[n],
 // W[M-n] = conj a[n] + i conj b[n]; the complex inverse FFT gives col_2r + i col_2r+1.
 template <int CB>
-__global__ void k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LB k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
@@ -87,14 +118,20 @@ __global__ void k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const
   double2* buf = sm;
   double2* tmp = sm + CH * S;
   const int x = L.xlo[0] + blockIdx.y, y0 = blockIdx.x * CB;
-  for (int idx = threadIdx.x; idx < nplanes * CH; idx += blockDim.x) {
-    const int n = idx / CH, r = idx - n * CH;
-    const int64_t row = slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + 2 * r;
-    const double2 a = (y0 + 2 * r < Mt) ? planes[row] : make_double2(0.0, 0.0);
-    const double2 b = (y0 + 2 * r + 1 < Mt) ? planes[row + 1] : make_double2(0.0, 0.0);
-    buf[r * S + n] = make_double2(a.x - b.y, a.y + b.x);
-    if (n > 0 && 2 * n < M) buf[r * S + (M - n)] = make_double2(a.x + b.y, b.x - a.y);   // Hermitian half
-  }
+  copy_batched<4, double4>(
+      nplanes * CH, threadIdx.x, blockDim.x,
+      [&](int idx) {
+        const int n = idx / CH, r = idx - n * CH;
+        const int64_t row = slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + 2 * r;
+        const double2 a = (y0 + 2 * r < Mt) ? planes[row] : make_double2(0.0, 0.0);
+        const double2 b = (y0 + 2 * r + 1 < Mt) ? planes[row + 1] : make_double2(0.0, 0.0);
+        return make_double4(a.x, a.y, b.x, b.y);
+      },
+      [&](int idx, double4 ab) {
+        const int n = idx / CH, r = idx - n * CH;
+        buf[r * S + n] = make_double2(ab.x - ab.w, ab.y + ab.z);
+        if (n > 0 && 2 * n < M) buf[r * S + (M - n)] = make_double2(ab.x + ab.w, ab.z - ab.y);   // Hermitian half
+      });
   __syncthreads();
   double2* out = fft_rows<1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   double* dst = grid + ((int64_t)x * Mt + y0) * M;
@@ -118,25 +155,27 @@ struct PlaneSel {
   __device__ __forceinline__ int slot(int by) const { return li ? li[by] : global(by); }
 };
 
-__global__ void k_rowfwd(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LB k_rowfwd(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
                          const double2* __restrict__ planes, double2* __restrict__ T, SlabLayout L, PlaneSel S) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
   double2* tmp = sm + RB * W;
   const int i = S.slot(blockIdx.y), x0 = blockIdx.x * RB;
   const int nr = min(RB, Mt - x0);
-  for (int r = 0; r < RB; ++r) {
-    const double2* src = (r < nr) ? planes + slab_row(L, i, x0 + r, Mt) : nullptr;
-    for (int y = threadIdx.x; y < W; y += blockDim.x)
-      buf[r * W + y] = (src && y < Mt) ? src[y] : make_double2(0.0, 0.0);
-  }
+  copy_batched<kLdU, double2>(
+      RB * W, threadIdx.x, blockDim.x,
+      [&](int idx) {
+        const int r = idx / W, y = idx - r * W;
+        return (r < nr && y < Mt) ? planes[slab_row(L, i, x0 + r, Mt) + y] : make_double2(0.0, 0.0);
+      },
+      [&](int idx, double2 v) { buf[idx] = v; });
   __syncthreads();
   double2* out = fft_rows<-1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
   double2* dst = T + base + (int64_t)blockIdx.y * Mt * W + (int64_t)x0 * W;
   for (int idx = threadIdx.x; idx < nr * W; idx += blockDim.x) dst[idx] = out[idx];
 }
 
-__global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LB k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const double2* __restrict__ tw,
                          const double2* __restrict__ T, double2* __restrict__ planes, SlabLayout L, PlaneSel S) {
   extern __shared__ double2 sm[];
   double2* buf = sm;
@@ -144,19 +183,9 @@ __global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const d
   const int i = S.slot(blockIdx.y), x0 = blockIdx.x * RB;
   const int nr = min(RB, Mt - x0);
   const double2* src = T + base + (int64_t)blockIdx.y * Mt * W + (int64_t)x0 * W;
-  {
-    int r = threadIdx.x / W;   // flat loop, row split carried incrementally (no division per entry)
-    const int dr = blockDim.x / W;
-    for (int idx = threadIdx.x, y = threadIdx.x - r * W; idx < RB * W; idx += blockDim.x) {
-      buf[idx] = (r < nr) ? src[idx] : make_double2(0.0, 0.0);
-      r += dr;
-      y += blockDim.x - dr * W;
-      if (y >= W) {
-        y -= W;
-        ++r;
-      }
-    }
-  }
+  copy_batched<kLdU, double2>(
+      RB * W, threadIdx.x, blockDim.x, [&](int idx) { return idx < nr * W ? src[idx] : make_double2(0.0, 0.0); },
+      [&](int idx, double2 v) { buf[idx] = v; });
   __syncthreads();
   double2* out = fft_rows<1>(buf, tmp, f, tw, RB, W, threadIdx.x, blockDim.x);
   for (int r = 0; r < nr; ++r) {
@@ -168,7 +197,7 @@ __global__ void k_rowinv(int Mt, int W, int64_t base, int RB, FftDesc f, const d
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
 // kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
 template <int CB>
-__global__ void k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LB k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
                           double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
                           const double2* __restrict__ pl, PlaneSel S) {
@@ -176,13 +205,31 @@ __global__ void k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2*
   const int SW = W + 1;   // padded row stride: the transposed accesses stay conflict-free
   double2* buf = sm;
   double2* tmp = sm + CB * SW;
+  double* mul = reinterpret_cast<double*>(sm + 2 * CB * SW);   // kernel class: khat columns [CB][W]
   const int n = S.global(blockIdx.y), y0 = blockIdx.x * CB;
   const int nc = min(CB, W - y0);
   double2* Tp = T + base + (int64_t)blockIdx.y * Mt * W;
-  for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
-    const int a = idx / CB, c = idx - a * CB;
-    buf[c * SW + a] = (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
-  }
+  copy_batched<kLdU, double2>(
+      CB * W, threadIdx.x, blockDim.x,
+      [&](int idx) {
+        const int a = idx / CB, c = idx - a * CB;
+        return (a < Mt && c < nc) ? Tp[(int64_t)a * W + y0 + c] : make_double2(0.0, 0.0);
+      },
+      [&](int idx, double2 v) {
+        const int a = idx / CB, c = idx - a * CB;
+        buf[c * SW + a] = v;
+      });
+  if (kernel_class)   // khat[n][a][y0 + c], issued before the FFT so its latency overlaps it
+    copy_batched<kLdU, double>(
+        CB * W, threadIdx.x, blockDim.x,
+        [&](int idx) {
+          const int a = idx / CB, c = idx - a * CB;
+          return __ldg(khat + ((int64_t)n * W + a) * W + min(y0 + c, W - 1));
+        },
+        [&](int idx, double v) {
+          const int a = idx / CB, c = idx - a * CB;
+          mul[c * W + a] = v;
+        });
   __syncthreads();
   double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
   double2* oth = (out == buf) ? tmp : buf;
@@ -194,7 +241,7 @@ __global__ void k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2*
     const int y = min(y0 + c, W - 1);
     double m;
     if (kernel_class) {
-      m = khat[((int64_t)n * W + a) * W + y];
+      m = mul[c * W + a];
     } else {
       const double den = k2J[a] + k2J[y] + pn.y;   // 0 only at k = 0 of an SE3P plan: mode dropped
       m = den > 0.0 ? pn.x * exJ[a] * exJ[y] / den : 0.0;
@@ -279,7 +326,7 @@ void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const Slab
 template <int CB>
 static void colpass_launch(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
                            int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
-  const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2);
+  const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2) + (kernel_class ? (size_t)CB * W * sizeof(double) : 0);
   set_smem((const void*)k_colpass<CB>, smc);
   k_colpass<CB><<<dim3((unsigned)ceil_div(W, CB), nplanes), kFftThreads, smc, st>>>(
       pl.dv.Mt, W, base, f, tw, w.T, kernel_class, pl.d_khat, pl.d_exJ, pl.d_k2J, (const double2*)pl.d_pl, S);
