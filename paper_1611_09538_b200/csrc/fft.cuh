@@ -4,7 +4,7 @@
 // One FFT length n = r_0 r_1 ... r_{S-1}; stage s (radix r, Ns = r_0...r_{s-1}) reads
 // v_t = in[j + t n/r], multiplies by w^{t (j mod Ns)} with w = e^{-+2 pi i/(Ns r)}, does an
 // r-point DFT and writes out[(j/Ns) Ns r + (j mod Ns) + q Ns] (Stockham autosort, natural
-// order in and out).  Radices 4, 2, 3, 5 have dedicated butterflies; any other prime
+// order in and out).  Radices 8, 9, 4, 2, 3, 5 have dedicated butterflies; any other prime
 // factor up to 61 uses an O(r^2) butterfly with a root table.  Twiddles are tabulated on
 // the host in long double and rounded once.
 #pragma once
@@ -85,6 +85,60 @@ __device__ __forceinline__ void bfly5(double2* v) {
   v[3] = csub(r2, i2);
 }
 
+// 8-point DFT as two 4-point DFTs (even / odd inputs) and a radix-2 combine with w8^q
+template <int DIR>
+__device__ __forceinline__ void bfly8(double2* v) {
+  const double r = 0.707106781186547524400844362104849039;   // 1/sqrt(2)
+  double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+  bfly4<DIR>(e);
+  bfly4<DIR>(o);
+  // w8^1 = (r, DIR r), w8^2 = DIR i, w8^3 = (-r, DIR r)
+  const double2 o1 = make_double2(r * (o[1].x - DIR * o[1].y), r * (o[1].y + DIR * o[1].x));
+  const double2 o2 = mul_i_dir<DIR>(o[2]);
+  const double2 o3 = make_double2(-r * (o[3].x + DIR * o[3].y), r * (DIR * o[3].x - o[3].y));
+  v[0] = cadd(e[0], o[0]);
+  v[4] = csub(e[0], o[0]);
+  v[1] = cadd(e[1], o1);
+  v[5] = csub(e[1], o1);
+  v[2] = cadd(e[2], o2);
+  v[6] = csub(e[2], o2);
+  v[3] = cadd(e[3], o3);
+  v[7] = csub(e[3], o3);
+}
+
+// 9-point DFT as 3 x 3: DFT3 over t1 of v[3 t1 + t2], twiddle w9^(t2 q1), DFT3 over t2 -> q1 + 3 q2
+template <int DIR>
+__device__ __forceinline__ void bfly9(double2* v) {
+  const double c1 = 0.766044443118978035202392650555416673;   // cos(2pi/9)
+  const double s1 = 0.642787609686539326322643409907263432;   // sin(2pi/9)
+  const double c2 = 0.173648177666930348851716626769314796;   // cos(4pi/9)
+  const double s2 = 0.984807753012208059366743024589523014;   // sin(4pi/9)
+  const double c4 = -0.939692620785908384054109277324731470;  // cos(8pi/9)
+  const double s4 = 0.342020143325668733044099614682259581;   // sin(8pi/9)
+  double2 y[3][3];
+#pragma unroll
+  for (int t2 = 0; t2 < 3; ++t2) {
+    double2 a[3] = {v[t2], v[3 + t2], v[6 + t2]};
+    bfly3<DIR>(a);
+    y[t2][0] = a[0];
+    y[t2][1] = a[1];
+    y[t2][2] = a[2];
+  }
+  // w9^k = (cos, DIR sin)
+  y[1][1] = cmul(y[1][1], make_double2(c1, DIR * s1));
+  y[1][2] = cmul(y[1][2], make_double2(c2, DIR * s2));
+  y[2][1] = cmul(y[2][1], make_double2(c2, DIR * s2));
+  y[2][2] = cmul(y[2][2], make_double2(c4, DIR * s4));
+#pragma unroll
+  for (int q1 = 0; q1 < 3; ++q1) {
+    double2 a[3] = {y[0][q1], y[1][q1], y[2][q1]};
+    bfly3<DIR>(a);
+    v[q1] = a[0];
+    v[q1 + 3] = a[1];
+    v[q1 + 6] = a[2];
+  }
+}
+
 // ------------------------------------------------------------------ one stage
 // Butterfly j (0 <= j < n/R) of row `row`: inputs j + t n/R, twiddle index k = j mod Ns, outputs
 // (j / Ns) Ns R + k + q Ns.  Threads own a fixed j across rows (when n/R <= nthr) so the index
@@ -95,6 +149,8 @@ __device__ __forceinline__ void bfly_fixed(double2* v) {
   if (R == 3) bfly3<DIR>(v);
   if (R == 4) bfly4<DIR>(v);
   if (R == 5) bfly5<DIR>(v);
+  if (R == 8) bfly8<DIR>(v);
+  if (R == 9) bfly9<DIR>(v);
 }
 
 template <int R, int DIR>
@@ -203,6 +259,8 @@ __device__ double2* fft_rows(double2* buf, double2* tmp, const FftDesc& d, const
       case 3: stage_fixed<3, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
       case 4: stage_fixed<4, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
       case 5: stage_fixed<5, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      case 8: stage_fixed<8, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
+      case 9: stage_fixed<9, DIR>(in, out, d.n, Ns, tws, nrows, rowstride, tid, nthr); break;
       default:
         stage_generic<DIR>(in, out, d.n, R, Ns, tws, tw + d.rootoff[s], nrows, rowstride, tid, nthr);
     }
@@ -216,11 +274,13 @@ __device__ double2* fft_rows(double2* buf, double2* tmp, const FftDesc& d, const
 }
 
 // ------------------------------------------------------------------ host side
-// Factorise n into stage radices (4s first, then 2, 3, 5, other primes).  Returns false if a
-// prime factor exceeds kMaxGenericRadix or there are too many stages.
-bool fft_factor(int n, std::vector<int>& rad);
+// Factorise n into stage radices: odd ones first (9 if r8, 3, 5), then 8 (if r8), 4, 2, then any
+// other prime.  Returns false if a prime factor exceeds kMaxGenericRadix or there are too many
+// stages.
+bool fft_factor(int n, std::vector<int>& rad, bool r8 = false);
 // Build the descriptor and append its twiddle/root table to `table` (host), setting offsets.
-bool fft_make(int n, FftDesc& d, std::vector<double2>& table);
+// r8: radix-8/9 stages (fewer shared-memory passes, more registers per butterfly).
+bool fft_make(int n, FftDesc& d, std::vector<double2>& table, bool r8);
 // "FFT-friendly": only factors 2, 3, 5.
 bool fft_friendly(int n);
 int next_friendly(int n);

@@ -62,7 +62,8 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   pl->LK = p.periodic ? p.SJ : next_friendly(2 * Mt - 1);
 
   std::vector<double2> tw;
-  if (!fft_make(p.M, pl->fz, tw) || !fft_make(p.SJ, pl->fJ, tw) || !fft_make(pl->LK, pl->fK, tw))
+  // (z-FFT: radix <= 5, its kernels run at 4 blocks per SM; the 2D passes: radix 8/9 at 3)
+  if (!fft_make(p.M, pl->fz, tw, false) || !fft_make(p.SJ, pl->fJ, tw, true) || !fft_make(pl->LK, pl->fK, tw, true))
     throw Error{4, "FFT extent has a prime factor > 61"};
   // descriptor offsets (twoff/rootoff) index the combined table directly
   pl->twz = pl->twJ = pl->twK = 0;

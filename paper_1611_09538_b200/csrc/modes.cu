@@ -38,10 +38,15 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 static int rows_for(int W) { int r = SE1P_ROW_SMEM / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? SE1P_COLS_LARGE : SE1P_COLS_SMALL; }
 constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT passes
-#ifndef SE1P_FFT_MINB
-#define SE1P_FFT_MINB 4
+// blocks per SM the register allocation targets: z passes (radix <= 5) and 2D passes (radix 8/9)
+#ifndef SE1P_FFT_MINB_Z
+#define SE1P_FFT_MINB_Z 4
 #endif
-#define SE1P_FFT_LB __launch_bounds__(SE1P_FFT_THREADS, SE1P_FFT_MINB)
+#ifndef SE1P_FFT_MINB_2D
+#define SE1P_FFT_MINB_2D 3
+#endif
+#define SE1P_FFT_LBZ __launch_bounds__(SE1P_FFT_THREADS, SE1P_FFT_MINB_Z)
+#define SE1P_FFT_LB __launch_bounds__(SE1P_FFT_THREADS, SE1P_FFT_MINB_2D)
 
 // Global -> shared copies with U independent loads in flight per thread (a plain strided loop
 // waits out one load latency per element): st(i, ld(i)) for i in [0, n).
@@ -71,7 +76,7 @@ constexpr int kLdU = 8;
 // CB (columns per block) is a template constant and M's log2 (or -1) is passed, so the index
 // splits below are shifts, not integer divisions by runtime values.
 template <int CB>
-__global__ void SE1P_FFT_LB k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LBZ k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
@@ -109,7 +114,7 @@ __global__ void SE1P_FFT_LB k_zfwd(int Mt, int M, int mshift, int nplanes, FftDe
 // Inverse: the Hermitian spectra a, b of columns 2r, 2r+1 combine into W[n] = a[n] + i b[n],
 // W[M-n] = conj a[n] + i conj b[n]; the complex inverse FFT gives col_2r + i col_2r+1.
 template <int CB>
-__global__ void SE1P_FFT_LB k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
+__global__ void SE1P_FFT_LBZ k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
   extern __shared__ double2 sm[];
