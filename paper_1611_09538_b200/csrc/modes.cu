@@ -66,7 +66,10 @@ __device__ __forceinline__ void copy_batched(int n, int tid, int nthr, LD ld, ST
     }
   }
 }
-constexpr int kLdU = 8;
+#ifndef SE1P_LDU
+#define SE1P_LDU 8
+#endif
+constexpr int kLdU = SE1P_LDU;
 
 // ------------------------------------------------------------------ z-FFT (AFT step 1)
 // Rows x = L.xlo[0] .. L.xlo[L.nslab]-1 of the grid; plane n goes to slot slot_of[n] (identity if
@@ -199,6 +202,17 @@ __global__ void SE1P_FFT_LB k_rowinv(int Mt, int W, int64_t base, int RB, FftDes
   }
 }
 
+// 1/d for d > 0 (normal): the hardware approximation refined by two Newton steps (relative error
+// ~2^-23 -> 2^-46 -> below 1 ulp), a fraction of the cost of an IEEE division
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
 // kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
 template <int CB>
@@ -236,20 +250,23 @@ __global__ void SE1P_FFT_LB k_colpass(int Mt, int W, int64_t base, FftDesc f, co
           mul[c * W + a] = v;
         });
   __syncthreads();
-  double2* out = fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
+#ifndef SE1P_COLPASS_EXP   // experiment builds: 1 no FFTs, 2 no multiply, 3 neither
+#define SE1P_COLPASS_EXP 0
+#endif
+  double2* out = (SE1P_COLPASS_EXP & 1) ? buf : fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
   double2* oth = (out == buf) ? tmp : buf;
   const double2 pn = pl[n];
   // flat loop over the CB x W entries with the (c, a) split carried incrementally (no division)
   int c = threadIdx.x / W, a = threadIdx.x - c * W;
   const int dc = blockDim.x / W, da = blockDim.x - dc * W;
-  for (; c < CB;) {
+  for (; c < CB && !(SE1P_COLPASS_EXP & 2);) {
     const int y = min(y0 + c, W - 1);
     double m;
     if (kernel_class) {
       m = mul[c * W + a];
     } else {
       const double den = k2J[a] + k2J[y] + pn.y;   // 0 only at k = 0 of an SE3P plan: mode dropped
-      m = den > 0.0 ? pn.x * exJ[a] * exJ[y] / den : 0.0;
+      m = den > 0.0 ? pn.x * exJ[a] * exJ[y] * rcp_nr(den) : 0.0;
     }
     double2 v = out[c * SW + a];
     out[c * SW + a] = make_double2(v.x * m, v.y * m);
@@ -261,7 +278,7 @@ __global__ void SE1P_FFT_LB k_colpass(int Mt, int W, int64_t base, FftDesc f, co
     }
   }
   __syncthreads();
-  double2* res = fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
+  double2* res = (SE1P_COLPASS_EXP & 1) ? out : fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < Mt * CB; idx += blockDim.x) {
     const int a = idx / CB, c = idx - a * CB;
     if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * SW + a];
