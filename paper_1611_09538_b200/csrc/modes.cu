@@ -13,6 +13,9 @@
 // plan-time spectrum of the exact aperiodic kernel equivalent to the paper's padded
 // transform of extent S.  All normalisations (1/M, 1/W^2) and the
 // gather constant are folded into the multipliers.
+#include <algorithm>
+#include <type_traits>
+
 #include "kspace.cuh"
 
 namespace se1p {
@@ -34,6 +37,13 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 #endif
 #ifndef SE1P_FFT_THREADS
 #define SE1P_FFT_THREADS 256
+#endif
+// persistent column passes: columns per item (3 slots per CTA)
+#ifndef SE1P_PCOLS_SMALL
+#define SE1P_PCOLS_SMALL 4
+#endif
+#ifndef SE1P_PCOLS_LARGE
+#define SE1P_PCOLS_LARGE 2
 #endif
 static int rows_for(int W) { int r = SE1P_ROW_SMEM / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? SE1P_COLS_LARGE : SE1P_COLS_SMALL; }
@@ -295,10 +305,302 @@ static int log2_or_neg(int n) {
   return (1 << s) == n ? s : -1;
 }
 
+// ------------------------------------------------------------------ persistent passes
+// The FFT passes above load a block's data, transform it and store it in sequence, so every
+// block waits out a full global-memory latency with nothing else to do (a variant with the
+// transforms removed keeps 2/3 of the mode stage's time).  The persistent form runs
+// ~blocks-per-SM x 148 CTAs that walk the pass's items, and prefetches item i + grid into a third
+// shared buffer with cp.async (SASS LDGSTS; zero-fill for padding) while item i is transformed in
+// the other two.  Each pass supplies load (async copies into a slot), compute (returns the
+// buffer holding the result; may use both buffers) and store.
+// SE1P_PERSIST bits: 1 z-FFT, 2 inverse z-FFT, 4 row passes, 8 column passes.  Measured at C5
+// (ncu, per launch): rows 87 -> 78 us and inverse z 167 -> 158 us persistent; the column passes
+// lose (their slot budget halves the columns per item: 133 -> 170 us) and the z-FFT is even.
+#ifndef SE1P_PERSIST
+#define SE1P_PERSIST 6
+#endif
+__device__ __forceinline__ unsigned sm_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sm_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sm_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <class PassT, int MINB>
+__global__ void __launch_bounds__(SE1P_FFT_THREADS, MINB) k_persist(const PassT P) {
+  extern __shared__ double2 sm[];
+  double2* B[3] = {sm, sm + P.slot, sm + 2 * P.slot};
+  int d = 0, p = 1;
+  const int x = 2;
+  int it = blockIdx.x;
+  if (it < P.n_items) P.load(it, B[d]);
+  cp_async_commit();
+  for (; it < P.n_items; it += gridDim.x) {
+    const int nx = it + gridDim.x;
+    if (nx < P.n_items) P.load(nx, B[p]);
+    cp_async_commit();
+    cp_async_wait1();   // every group but the newest: item it has landed (this thread's copies)
+    __syncthreads();    // (and every thread's)
+    const double2* res = P.compute(it, B[d], B[x]);
+    P.store(it, res);
+    __syncthreads();    // result read out before its buffers take the next prefetch
+    const int t = d;
+    d = p;
+    p = t;
+  }
+}
+
+// rows of a plane: item = (plane by, row group); planes -> FFT along y -> T
+struct RowFwdPass {
+  int n_items, slot, nxb, Mt, W, RB;
+  int64_t base;
+  FftDesc f;
+  const double2* tw;
+  const double2* planes;
+  double2* T;
+  SlabLayout L;
+  PlaneSel S;
+  __device__ void load(int it, double2* dst) const {
+    const int by = it / nxb, x0 = (it - by * nxb) * RB, i = S.slot(by), nr = min(RB, Mt - x0);
+    for (int r = 0; r < RB; ++r) {
+      const double2* src = planes + (r < nr ? slab_row(L, i, x0 + r, Mt) : 0);
+      for (int y = threadIdx.x; y < W; y += blockDim.x) {
+        const bool v = r < nr && y < Mt;
+        cp_async16(dst + r * W + y, v ? src + y : planes, v);
+      }
+    }
+  }
+  __device__ const double2* compute(int, double2* b, double2* t) const {
+    return fft_rows<-1>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
+  }
+  __device__ void store(int it, const double2* res) const {
+    const int by = it / nxb, x0 = (it - by * nxb) * RB, nr = min(RB, Mt - x0);
+    double2* dst = T + base + (int64_t)by * Mt * W + (int64_t)x0 * W;
+    for (int idx = threadIdx.x; idx < nr * W; idx += blockDim.x) dst[idx] = res[idx];
+  }
+};
+
+// inverse rows: T -> inverse FFT along y -> planes (y < Mt)
+struct RowInvPass {
+  int n_items, slot, nxb, Mt, W, RB;
+  int64_t base;
+  FftDesc f;
+  const double2* tw;
+  const double2* T;
+  double2* planes;
+  SlabLayout L;
+  PlaneSel S;
+  __device__ void load(int it, double2* dst) const {
+    const int by = it / nxb, x0 = (it - by * nxb) * RB, nr = min(RB, Mt - x0);
+    const double2* src = T + base + (int64_t)by * Mt * W + (int64_t)x0 * W;
+    for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
+      const bool v = idx < nr * W;
+      cp_async16(dst + idx, v ? src + idx : T, v);
+    }
+  }
+  __device__ const double2* compute(int, double2* b, double2* t) const {
+    return fft_rows<1>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
+  }
+  __device__ void store(int it, const double2* res) const {
+    const int by = it / nxb, x0 = (it - by * nxb) * RB, i = S.slot(by), nr = min(RB, Mt - x0);
+    for (int r = 0; r < nr; ++r) {
+      double2* dst = planes + slab_row(L, i, x0 + r, Mt);
+      for (int y = threadIdx.x; y < Mt; y += blockDim.x) dst[y] = res[r * W + y];
+    }
+  }
+};
+
+// columns: item = (plane by, column block of CB); FFT along x, multiply, inverse FFT; the kernel
+// class's multiplier columns khat[n][a][y] ride in the slot behind the data
+template <int CB>
+struct ColPass {
+  int n_items, slot, ncb, Mt, W, kernel_class;
+  int64_t base;
+  FftDesc f;
+  const double2* tw;
+  double2* T;
+  const double* khat;
+  const double* exJ;
+  const double* k2J;
+  const double2* pl;
+  PlaneSel S;
+  __device__ void load(int it, double2* dst) const {
+    const int by = it / ncb, y0 = (it - by * ncb) * CB, nc = min(CB, W - y0), SW = W + 1, n = S.global(by);
+    const double2* Tp = T + base + (int64_t)by * Mt * W;
+    for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
+      const int a = idx / CB, c = idx - a * CB;
+      const bool v = a < Mt && c < nc;
+      cp_async16(dst + c * SW + a, v ? Tp + (int64_t)a * W + y0 + c : Tp, v);
+    }
+    if (kernel_class) {
+      double* mul = reinterpret_cast<double*>(dst + CB * SW);
+      for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
+        const int a = idx / CB, c = idx - a * CB;
+        cp_async8(mul + c * W + a, khat + ((int64_t)n * W + a) * W + min(y0 + c, W - 1), true);
+      }
+    }
+  }
+  __device__ const double2* compute(int it, double2* b, double2* t) const {
+    const int by = it / ncb, y0 = (it - by * ncb) * CB, SW = W + 1, n = S.global(by);
+    const double* mul = reinterpret_cast<const double*>(b + CB * SW);
+    double2* out = fft_rows<-1>(b, t, f, tw, CB, SW, threadIdx.x, blockDim.x);
+    double2* oth = (out == b) ? t : b;
+    const double2 pn = pl[n];
+    for (int idx = threadIdx.x; idx < CB * W; idx += blockDim.x) {
+      const int c = idx / W, a = idx - c * W;
+      double m;
+      if (kernel_class) {
+        m = mul[c * W + a];
+      } else {
+        const int y = min(y0 + c, W - 1);
+        const double den = k2J[a] + k2J[y] + pn.y;   // 0 only at k = 0 of an SE3P plan: mode dropped
+        m = den > 0.0 ? pn.x * exJ[a] * exJ[y] * rcp_nr(den) : 0.0;
+      }
+      const double2 v = out[c * SW + a];
+      out[c * SW + a] = make_double2(v.x * m, v.y * m);
+    }
+    __syncthreads();
+    return fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
+  }
+  __device__ void store(int it, const double2* res) const {
+    const int by = it / ncb, y0 = (it - by * ncb) * CB, nc = min(CB, W - y0), SW = W + 1;
+    double2* Tp = T + base + (int64_t)by * Mt * W;
+    for (int idx = threadIdx.x; idx < Mt * CB; idx += blockDim.x) {
+      const int a = idx / CB, c = idx - a * CB;
+      if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * SW + a];
+    }
+  }
+};
+
+// z-FFT: item = (grid row x, column block of CB); two real columns per complex FFT (see k_zfwd)
+template <int CB>
+struct ZfwdPass {
+  int n_items, slot, ncb, Mt, M, mshift, nplanes;
+  FftDesc f;
+  const double2* tw;
+  const double* grid;
+  double2* planes;
+  SlabLayout L;
+  const int* slot_of;
+  __device__ void load(int it, double2* dst) const {
+    const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB, ncol = min(CB, Mt - y0), S = M + 1;
+    const double* src = grid + ((int64_t)x * Mt + y0) * M;
+    double* bd = reinterpret_cast<double*>(dst);
+    for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
+      const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
+      const bool v = c < ncol;
+      cp_async8(bd + 2 * ((c >> 1) * S + k) + (c & 1), v ? src + idx : grid, v);
+    }
+  }
+  __device__ const double2* compute(int, double2* b, double2* t) const {
+    return fft_rows<-1>(b, t, f, tw, CB / 2, M + 1, threadIdx.x, blockDim.x);
+  }
+  __device__ void store(int it, const double2* out) const {
+    const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB, S = M + 1;
+    for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
+      const int n = idx / CB, c = idx - n * CB;
+      if (y0 + c < Mt) {
+        const double2 Z = out[(c >> 1) * S + n], Zm = out[(c >> 1) * S + (n ? M - n : 0)];
+        const double2 v = (c & 1) ? make_double2(0.5 * (Z.y + Zm.y), 0.5 * (Zm.x - Z.x))    // (Z - conj Zm)/(2i)
+                                  : make_double2(0.5 * (Z.x + Zm.x), 0.5 * (Z.y - Zm.y));   // (Z + conj Zm)/2
+        planes[slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + c] = v;
+      }
+    }
+  }
+};
+
+// inverse z-FFT: the slot first holds the raw (a, b) spectrum pairs, combined into the FFT input
+// in the other buffer (see k_zinv)
+template <int CB>
+struct ZinvPass {
+  int n_items, slot, ncb, Mt, M, mshift, nplanes;
+  FftDesc f;
+  const double2* tw;
+  const double2* planes;
+  double* grid;
+  SlabLayout L;
+  const int* slot_of;
+  __device__ void load(int it, double2* dst) const {
+    constexpr int CH = CB / 2;
+    const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB;
+    for (int idx = threadIdx.x; idx < nplanes * CH; idx += blockDim.x) {
+      const int n = idx / CH, r = idx - n * CH;
+      const int64_t row = slab_row(L, slot_of ? slot_of[n] : n, x, Mt) + y0 + 2 * r;
+      const bool va = y0 + 2 * r < Mt, vb = y0 + 2 * r + 1 < Mt;
+      cp_async16(dst + 2 * idx, va ? planes + row : planes, va);
+      cp_async16(dst + 2 * idx + 1, vb ? planes + row + 1 : planes, vb);
+    }
+  }
+  __device__ const double2* compute(int, double2* b, double2* t) const {
+    constexpr int CH = CB / 2;
+    const int S = M + 1;
+    for (int idx = threadIdx.x; idx < nplanes * CH; idx += blockDim.x) {
+      const int n = idx / CH, r = idx - n * CH;
+      const double2 a = b[2 * idx], bb = b[2 * idx + 1];
+      t[r * S + n] = make_double2(a.x - bb.y, a.y + bb.x);
+      if (n > 0 && 2 * n < M) t[r * S + (M - n)] = make_double2(a.x + bb.y, bb.x - a.y);   // Hermitian half
+    }
+    __syncthreads();
+    return fft_rows<1>(t, b, f, tw, CH, S, threadIdx.x, blockDim.x);
+  }
+  __device__ void store(int it, const double2* out) const {
+    const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB, S = M + 1;
+    double* dstg = grid + ((int64_t)x * Mt + y0) * M;
+    for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
+      const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
+      if (y0 + c < Mt) {
+        const double2 v = out[(c >> 1) * S + k];
+        dstg[idx] = (c & 1) ? v.y : v.x;
+      }
+    }
+  }
+};
+
+// grid for a persistent pass: resident CTAs (occupancy query) x SMs, at most one per item
+template <class PassT, int MINB>
+static void persist_launch(const PassT& P, cudaStream_t st) {
+  if (P.n_items <= 0) return;
+  const size_t smem = 3 * (size_t)P.slot * sizeof(double2);
+  const void* fn = (const void*)k_persist<PassT, MINB>;
+  set_smem(fn, smem);
+  int dev = 0, nsm = 0, per = 0;
+  SE1P_CUDA_TRY(cudaGetDevice(&dev));
+  SE1P_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  SE1P_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, SE1P_FFT_THREADS, smem));
+  const int grid = std::max(1, std::min(P.n_items, std::max(per, 1) * nsm));
+  k_persist<PassT, MINB><<<grid, SE1P_FFT_THREADS, smem, st>>>(P);
+  SE1P_LAUNCH_CHECK();
+}
+
 template <int CB>
 static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
                         int rows, cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt;
+#if SE1P_PERSIST & 1
+  {
+    ZfwdPass<CB> P{};
+    P.ncb = (int)ceil_div(Mt, CB);
+    P.n_items = P.ncb * rows;
+    P.slot = (CB / 2) * (M + 1);
+    P.Mt = Mt;
+    P.M = M;
+    P.mshift = log2_or_neg(M);
+    P.nplanes = pl.n_planes;
+    P.f = pl.fz;
+    P.tw = pl.d_tw + pl.twz;
+    P.grid = w.grid;
+    P.planes = planes;
+    P.L = L;
+    P.slot_of = slot_of;
+    persist_launch<ZfwdPass<CB>, SE1P_FFT_MINB_Z>(P, st);
+    return;
+  }
+#endif
   const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zfwd<CB>, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
@@ -311,6 +613,26 @@ template <int CB>
 static void zinv_launch(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
                         int rows, cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt;
+#if SE1P_PERSIST & 2
+  {
+    ZinvPass<CB> P{};
+    P.ncb = (int)ceil_div(Mt, CB);
+    P.n_items = P.ncb * rows;
+    P.slot = std::max((CB / 2) * (M + 1), 2 * pl.n_planes * (CB / 2));
+    P.Mt = Mt;
+    P.M = M;
+    P.mshift = log2_or_neg(M);
+    P.nplanes = pl.n_planes;
+    P.f = pl.fz;
+    P.tw = pl.d_tw + pl.twz;
+    P.planes = planes;
+    P.grid = w.grid;
+    P.L = L;
+    P.slot_of = slot_of;
+    persist_launch<ZinvPass<CB>, SE1P_FFT_MINB_Z>(P, st);
+    return;
+  }
+#endif
   const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
   set_smem((const void*)k_zinv<CB>, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
@@ -360,6 +682,50 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
   if (nplanes <= 0) return;
   const int Mt = pl.dv.Mt;
   const int RB = rows_for(W), CB = cols_for(W);
+#if SE1P_PERSIST & 4
+  {
+    const double2* tw = pl.d_tw + twoff;
+    const int nxb = (int)ceil_div(Mt, RB);
+    RowFwdPass R{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, planes, w.T, L, S};
+    persist_launch<RowFwdPass, SE1P_FFT_MINB_2D>(R, st);
+#if SE1P_PERSIST & 8
+    const int cb = W > 400 ? SE1P_PCOLS_LARGE : SE1P_PCOLS_SMALL;
+    auto col = [&](auto cbc) {
+      constexpr int C = decltype(cbc)::value;
+      ColPass<C> P{};
+      P.ncb = (int)ceil_div(W, C);
+      P.n_items = P.ncb * nplanes;
+      P.slot = C * (W + 1) + (kernel_class ? (C * W + 1) / 2 : 0);
+      P.Mt = Mt;
+      P.W = W;
+      P.kernel_class = kernel_class;
+      P.base = base;
+      P.f = f;
+      P.tw = tw;
+      P.T = w.T;
+      P.khat = pl.d_khat;
+      P.exJ = pl.d_exJ;
+      P.k2J = pl.d_k2J;
+      P.pl = (const double2*)pl.d_pl;
+      P.S = S;
+      persist_launch<ColPass<C>, SE1P_FFT_MINB_2D>(P, st);
+    };
+    if (cb == 2) col(std::integral_constant<int, 2>());
+    else if (cb == 8) col(std::integral_constant<int, 8>());
+    else col(std::integral_constant<int, 4>());
+#else
+    switch (CB) {
+      case 2: colpass_launch<2>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+      case 4: colpass_launch<4>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+      case 16: colpass_launch<16>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st); break;
+      default: colpass_launch<8>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
+    }
+#endif
+    RowInvPass Q{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, w.T, planes, L, S};
+    persist_launch<RowInvPass, SE1P_FFT_MINB_2D>(Q, st);
+    return;
+  }
+#endif
   const size_t smr = 2 * (size_t)RB * W * sizeof(double2);
   set_smem((const void*)k_rowfwd, smr);
   set_smem((const void*)k_rowinv, smr);
