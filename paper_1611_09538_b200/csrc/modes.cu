@@ -48,6 +48,7 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 static int rows_for(int W) { int r = SE1P_ROW_SMEM / (2 * W * 16); return r < 1 ? 1 : (r > 16 ? 16 : r); }
 static int cols_for(int W) { return W > 400 ? SE1P_COLS_LARGE : SE1P_COLS_SMALL; }
 constexpr int kFftThreads = SE1P_FFT_THREADS;   // threads per block of the FFT passes
+constexpr int kColMaxThreads = 384;             // column pass: block size chosen per plan (col_threads)
 // blocks per SM the register allocation targets: z passes (radix <= 5) and 2D passes (radix 8/9)
 #ifndef SE1P_FFT_MINB_Z
 #define SE1P_FFT_MINB_Z 4
@@ -226,7 +227,7 @@ __device__ __forceinline__ double rcp_nr(double d) {
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
 // kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
 template <int CB>
-__global__ void SE1P_FFT_LB k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
+__global__ void __launch_bounds__(kColMaxThreads, 2) k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
                           double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
                           const double2* __restrict__ pl, PlaneSel S) {
@@ -667,12 +668,28 @@ void k_zfft_inverse(const KPlan& pl, KWork& w, const double2* planes, const Slab
   }
 }
 
+// Column-pass block size: the warp multiple <= kColMaxThreads with the fewest butterfly rounds
+// over the FFT's stages (stage s has CB W / R_s butterflies), then the fewest threads -- e.g. the
+// 320-point J columns (radices 5, 8, 8) x 8 take 320 threads: 2 + 1 + 1 rounds instead of 2 + 2 + 2
+static int col_threads(const FftDesc& f, int CB) {
+  int best = kFftThreads, best_rounds = 1 << 30;
+  for (int t = 128; t <= kColMaxThreads; t += 32) {
+    int rounds = 0;
+    for (int s = 0; s < f.nst; ++s) rounds += (int)ceil_div((int64_t)CB * (f.n / f.rad[s]), t);
+    if (rounds < best_rounds) {
+      best_rounds = rounds;
+      best = t;
+    }
+  }
+  return best;
+}
+
 template <int CB>
 static void colpass_launch(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
                            int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
   const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2) + (kernel_class ? (size_t)CB * W * sizeof(double) : 0);
   set_smem((const void*)k_colpass<CB>, smc);
-  k_colpass<CB><<<dim3((unsigned)ceil_div(W, CB), nplanes), kFftThreads, smc, st>>>(
+  k_colpass<CB><<<dim3((unsigned)ceil_div(W, CB), nplanes), col_threads(f, CB), smc, st>>>(
       pl.dv.Mt, W, base, f, tw, w.T, kernel_class, pl.d_khat, pl.d_exJ, pl.d_k2J, (const double2*)pl.d_pl, S);
   SE1P_LAUNCH_CHECK();
 }
