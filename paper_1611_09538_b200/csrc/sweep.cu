@@ -820,28 +820,30 @@ extern "C" int se1p_sweep_trace(long long* host) {
 // position receives at most one overhang (chunks hold >= P-1 nodes), so the adds do not race.
 __global__ void k_overhang(const double* __restrict__ over, double* __restrict__ grid, int Mt, int M, int P, int C,
                            int nzc, int x_lo, int x_hi) {
+  // one thread per (chunk, column, overhang node): contiguous reads of the overhang, runs of
+  // consecutive z in the grid column
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t ncol = (int64_t)(x_hi - x_lo) * Mt;
-  if (i >= ncol * nzc) return;
-  const int zc = (int)(i / ncol);
-  const int64_t col = (int64_t)x_lo * Mt + (i - (int64_t)zc * ncol);
+  if (i >= ncol * nzc * (P - 1)) return;
+  const int64_t cc = i / (P - 1);
+  const int t = (int)(i - cc * (P - 1));
+  const int zc = (int)(cc / ncol);
+  const int64_t col = (int64_t)x_lo * Mt + (cc - (int64_t)zc * ncol);
   const int Z0 = zc * C, Ck = min(C, M - Z0);
-  const double* o = over + ((int64_t)zc * Mt * Mt + col) * (P - 1);
-  double* gcol = grid + col * M;
-  for (int t = 0; t < P - 1; ++t) {
-    int z = Z0 + Ck + t;
-    while (z >= M) z -= M;
-    gcol[z] += o[t];
-  }
+  int z = Z0 + Ck + t;
+  while (z >= M) z -= M;
+  grid[col * M + z] += over[((int64_t)zc * Mt * Mt + col) * (P - 1) + t];
 }
 
 // Items (tx | ty << 10 | zc << 20) ordered by candidate count, heaviest first (ties: index order).
+// (weights staged in shared memory when they fit: SW)
+template <bool SW>
 __global__ void k_items(int ntx, int tx_lo, int nty, int nzc, int Mfree, int P, int* __restrict__ items,
                         int* __restrict__ counter) {
+  extern __shared__ int wsm[];
   const int n = ntx * nty * nzc;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) counter[0] = 0;
-  if (i >= n) return;
   auto wt = [&](int j) {
     const int zc = j % nzc, t2 = j / nzc, ty = t2 % nty, tx = t2 / nty + tx_lo;
     (void)zc;
@@ -850,10 +852,15 @@ __global__ void k_items(int ntx, int tx_lo, int nty, int nzc, int Mfree, int P, 
     const int wy = max(0, min(Y0 + kTXY - 1, Mfree) - max(Y0 - P + 1, 1) + 1);
     return wx * wy;
   };
-  const int wi = wt(i);
+  if (SW) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) wsm[j] = wt(j);
+    __syncthreads();
+  }
+  if (i >= n) return;
+  const int wi = SW ? wsm[i] : wt(i);
   int rank = 0;
   for (int j = 0; j < n; ++j) {
-    const int wj = wt(j);
+    const int wj = SW ? wsm[j] : wt(j);
     rank += (wj > wi) || (wj == wi && j < i);
   }
   const int zc = i % nzc, t2 = i / nzc, ty = t2 % nty, tx = t2 / nty + tx_lo;
@@ -877,7 +884,7 @@ __global__ void __launch_bounds__(128) k_records(KDev dv, const double4* __restr
     const double d0[3] = {((double)s.x - P2) * dv.h - pp.x, ((double)s.y - P2) * dv.h - pp.y,
                           (double)s.z * dv.h - pp.z};
     const double ah = 2.0 * dv.alpha * dv.h;
-    double* r = srec + threadIdx.x * RD;
+    double* r = srec + threadIdx.x * (RD + 1);   // odd stride: conflict-free per-thread rows
     r[0] = __hiloint2double(s.y, s.x);
     r[kRq] = pp.w;
 #pragma unroll
@@ -903,9 +910,12 @@ __global__ void __launch_bounds__(128) k_records(KDev dv, const double4* __restr
     }
   }
   __syncthreads();
-  const double2* src = reinterpret_cast<const double2*>(srec);
   double2* dst = reinterpret_cast<double2*>(rec + i0 * RD);
-  for (int k = threadIdx.x; k < nrec * RD / 2; k += 128) dst[k] = src[k];
+  for (int k = threadIdx.x; k < nrec * RD / 2; k += 128) {
+    const int row = (2 * k) / RD, col = 2 * k - row * RD;   // RD even: a pair never straddles rows
+    const double* sp = srec + row * (RD + 1) + col;
+    dst[k] = make_double2(sp[0], sp[1]);
+  }
 }
 
 // The field's second gather pass: the z windows become 2 alpha (node - z_p) wz (d/dz_p of the
@@ -1006,7 +1016,7 @@ void k_records_stage(const KPlan& pl, KWork& w, int64_t N, cudaStream_t st, bool
   (void)field;
   const int nz = sw_nzb(pl.dv.P);
   const int RD = rec_stride(nz);
-  const size_t sm = 128 * RD * sizeof(double);
+  const size_t sm = 128 * (RD + 1) * sizeof(double);
   if (sm > 48 * 1024)
     SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_records, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_records<<<(unsigned)ceil_div(N, 128), 128, sm, st>>>(pl.dv, (const double4*)w.xs, (const int4*)w.s4, N, RD,
@@ -1028,8 +1038,12 @@ static void launch_sweep_t(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int 
   a.n_items = ntx * nty * a.nzc;
   // item table (heavy first); k_items also zeroes the work counter
   if (w.items_cap < a.n_items + 2) throw Error{6, "sweep item table not allocated"};
-  k_items<<<(unsigned)ceil_div(a.n_items, 128), 128, 0, st>>>(ntx, tx_lo, nty, a.nzc, dv.Mfree, dv.P, w.items,
-                                                              w.items + a.n_items);
+  if ((size_t)a.n_items * sizeof(int) <= 48 * 1024)
+    k_items<true><<<(unsigned)ceil_div(a.n_items, 256), 256, (size_t)a.n_items * sizeof(int), st>>>(
+        ntx, tx_lo, nty, a.nzc, dv.Mfree, dv.P, w.items, w.items + a.n_items);
+  else
+    k_items<false><<<(unsigned)ceil_div(a.n_items, 256), 256, 0, st>>>(ntx, tx_lo, nty, a.nzc, dv.Mfree, dv.P,
+                                                                       w.items, w.items + a.n_items);
   SE1P_LAUNCH_CHECK();
   a.items = w.items;
   a.counter = w.items + a.n_items;
@@ -1065,7 +1079,7 @@ static void launch_sweep_t(const KPlan& pl, KWork& w, int64_t N, int tx_lo, int 
   SE1P_LAUNCH_CHECK();
   if (!GATHER && dv.P > 1) {
     const int x_lo = tx_lo * kTXY, x_hi = std::min(tx_hi * kTXY, dv.Mt);
-    const int64_t n = (int64_t)a.nzc * (x_hi - x_lo) * dv.Mt;
+    const int64_t n = (int64_t)a.nzc * (x_hi - x_lo) * dv.Mt * (dv.P - 1);
     k_overhang<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(w.over, w.grid, dv.Mt, dv.M, dv.P, a.C, a.nzc, x_lo, x_hi);
     SE1P_LAUNCH_CHECK();
   }
