@@ -1,6 +1,8 @@
 // kplan.cu -- k-space plan: Alg. 1 step 1, FFT descriptors, scaling tables and
 // the plan-time kernel spectra of the upsampled planes.
 #include <chrono>
+#include <cstdio>
+#include <thread>
 #include <cmath>
 #include <memory>
 #include <vector>
@@ -10,7 +12,7 @@
 namespace se1p {
 
 void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* khat_out, double scale,
-                           cudaStream_t st);
+                           const KernScratch& ks, cudaStream_t st);
 
 // 1 - J0(x) without cancellation for small x (series), glibc j0 otherwise.
 static double one_minus_j0(double x) {
@@ -42,8 +44,16 @@ static uint64_t g_plan_generation = 1;   // bumped whenever a plan is built or f
 
 uint64_t kplan_generation() { return g_plan_generation; }
 
+#ifndef SE1P_PLAN_TRACE
+#define SE1P_PLAN_TRACE 0
+#endif
 static KPlan* build(const KParams& p, cudaStream_t st) {
   auto t0 = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what) {
+    if (SE1P_PLAN_TRACE)
+      fprintf(stderr, "plan %s %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   auto pl = std::make_unique<KPlan>();
   pl->prm = p;
   KDev& dv = pl->dv;
@@ -76,6 +86,7 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
   pl->const_gather = 4.0 * kPi * h * h * h * pref * pref;
   const double R = std::sqrt(2.0) * Mt * h;  // reading R-6: sqrt(L~1^2 + L~2^2), square cross-section
 
+  tr("twiddles");
   // J-plane tables
   {
     const int SJ = p.SJ;
@@ -109,29 +120,57 @@ static KPlan* build(const KParams& p, cudaStream_t st) {
     SE1P_CUDA_TRY(cudaMemcpy(pl->d_f1, f1.data(), sizeof(double) * p.P, cudaMemcpyHostToDevice));
   }
 
+  tr("tables");
   // kernel planes: k3 = 0 (extent S0) and 0 < k3 <= 2 pi n_l/L3 (extent SI)
   {
     const int LK = pl->LK;
     dev_alloc(pl->d_khat, (size_t)pl->n_kernel * LK * LK);
     const double scale = pl->const_gather / ((double)p.M * (double)LK * (double)LK);
+    auto extent = [&](int n) { return (n == 0) ? p.S0 : ((size_t)(n - 1) < p.SIn.size() ? p.SIn[n - 1] : p.SI); };
+    int Hmax = 1;
+    for (int n = 0; n < pl->n_kernel; ++n) Hmax = std::max(Hmax, extent(n) / 2 + 1);
+    // scratch allocated once; the host builds plane n + 1's table while the device transforms
+    // plane n (stream order keeps the single table buffer safe)
+    KernScratch ks{};
+    double* d_sig = nullptr;
+    if (pl->n_kernel > 0) {
+      dev_alloc(d_sig, (size_t)Hmax * Hmax);
+      dev_alloc(ks.tmp, (size_t)Mt * Hmax);
+      dev_alloc(ks.A, (size_t)LK * LK);
+      dev_alloc(ks.B, (size_t)LK * LK);
+    }
+    const int nth = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+    std::vector<double> sig;
     for (int n = 0; n < pl->n_kernel; ++n) {
-      const int S = (n == 0) ? p.S0 : ((size_t)(n - 1) < p.SIn.size() ? p.SIn[n - 1] : p.SI);
+      const int S = extent(n);
       const int H = S / 2 + 1;
       const double k3 = 2.0 * kPi * n / L3;
       const double dk = 2.0 * kPi / (S * h);
-      std::vector<double> sig((size_t)H * H);
-      for (int m1 = 0; m1 < H; ++m1)
-        for (int m2 = 0; m2 <= m1; ++m2) {
-          const double kap2 = dk * dk * ((double)m1 * m1 + (double)m2 * m2);
-          const double v = scaling(kap2, k3 * k3, eta, xi, R);
-          sig[(size_t)m1 * H + m2] = v;
-          sig[(size_t)m2 * H + m1] = v;
-        }
-      double* d_sig = nullptr;
-      dev_alloc(d_sig, sig.size());
-      SE1P_CUDA_TRY(cudaMemcpy(d_sig, sig.data(), sizeof(double) * sig.size(), cudaMemcpyHostToDevice));
-      build_kernel_spectrum(*pl, S, d_sig, pl->d_khat + (size_t)n * LK * LK, scale, st);
+      sig.assign((size_t)H * H, 0.0);
+      // the (S/2+1)^2 table on the host's cores (rows interleaved over threads)
+      std::vector<std::thread> pool;
+      for (int th = 0; th < nth; ++th)
+        pool.emplace_back([&, th]() {
+          for (int m1 = th; m1 < H; m1 += nth)
+            for (int m2 = 0; m2 <= m1; ++m2) {
+              const double kap2 = dk * dk * ((double)m1 * m1 + (double)m2 * m2);
+              const double v = scaling(kap2, k3 * k3, eta, xi, R);
+              sig[(size_t)m1 * H + m2] = v;
+              sig[(size_t)m2 * H + m1] = v;
+            }
+        });
+      for (auto& t : pool) t.join();
+      tr("sig");
+      SE1P_CUDA_TRY(cudaMemcpyAsync(d_sig, sig.data(), sizeof(double) * sig.size(), cudaMemcpyHostToDevice, st));
+      build_kernel_spectrum(*pl, S, d_sig, pl->d_khat + (size_t)n * LK * LK, scale, ks, st);
+      tr("spectrum");
+    }
+    if (pl->n_kernel > 0) {
+      SE1P_CUDA_TRY(cudaStreamSynchronize(st));
       dev_free(d_sig);
+      dev_free(ks.tmp);
+      dev_free(ks.A);
+      dev_free(ks.B);
     }
   }
   pl->t_off_total = (int64_t)pl->n_kernel * Mt * pl->LK + (int64_t)(pl->n_planes - pl->n_kernel) * Mt * p.SJ;

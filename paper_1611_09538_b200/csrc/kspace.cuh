@@ -7,6 +7,14 @@
 
 namespace se1p {
 
+// plan-time scratch of the kernel-spectrum builder (build_kernel_spectrum, modes.cu)
+struct KernScratch {
+  double* tmp;   // [Mt][S/2+1]
+  double2* A;    // [LK][LK]
+  double2* B;    // [LK][LK]
+};
+
+
 // Particle bins: x bands of kBin cells; inside a band by periodic stencil start, then y cell.
 constexpr int kBin = 4;
 

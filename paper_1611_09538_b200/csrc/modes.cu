@@ -871,13 +871,10 @@ __global__ void k_transpose(int n, const double2* __restrict__ A, double2* __res
 
 // Device part of the kernel spectrum: sig (host table, device copy) -> khat_out [LK][LK].
 void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* khat_out, double scale,
-                           cudaStream_t st) {
+                           const KernScratch& ks, cudaStream_t st) {
   const int Mt = pl.dv.Mt, LK = pl.LK, H = S / 2 + 1;
-  double* tmp = nullptr;
-  double2 *A = nullptr, *B = nullptr;
-  dev_alloc(tmp, (size_t)Mt * H);
-  dev_alloc(A, (size_t)LK * LK);
-  dev_alloc(B, (size_t)LK * LK);
+  double* tmp = ks.tmp;
+  double2 *A = ks.A, *B = ks.B;
   SE1P_CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * (size_t)LK * LK, st));
   k_kern_a<<<(unsigned)ceil_div((int64_t)Mt * H, 128), 128, 0, st>>>(S, Mt, d_sig, tmp);
   SE1P_LAUNCH_CHECK();
@@ -896,10 +893,6 @@ void build_kernel_spectrum(const KPlan& pl, int S, const double* d_sig, double* 
   // B = transpose of the 2D spectrum; transpose back while taking the (real) value
   k_transpose_scale_real<<<(unsigned)ceil_div((int64_t)LK * LK, 256), 256, 0, st>>>(LK, scale, B, khat_out);
   SE1P_LAUNCH_CHECK();
-  SE1P_CUDA_TRY(cudaStreamSynchronize(st));
-  dev_free(tmp);
-  dev_free(A);
-  dev_free(B);
 }
 
 }  // namespace se1p
