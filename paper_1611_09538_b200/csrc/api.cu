@@ -447,7 +447,7 @@ static void kspace_impl(const se1p_opts* o, cudaStream_t st, const double* x, co
     SE1P_CUDA_TRY(cudaStreamSynchronize(st));
     int kerr = 0;
     SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+    if (kerr) throw Error{6, "sweep kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
   }
   SE1P_CUDA_TRY(cudaGetLastError());
 }
@@ -527,7 +527,7 @@ static void kspace3p_impl(const se1p_opts* o, cudaStream_t st, const double* x, 
     SE1P_CUDA_TRY(cudaStreamSynchronize(st));
     int kerr = 0;
     SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+    if (kerr) throw Error{6, "sweep kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
   }
   SE1P_CUDA_TRY(cudaGetLastError());
 }
@@ -595,7 +595,7 @@ static void finish_call(const se1p_opts* o, KWork& w, cudaStream_t st) {
     SE1P_CUDA_TRY(cudaStreamSynchronize(st));
     int kerr = 0;
     SE1P_CUDA_TRY(cudaMemcpy(&kerr, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+    if (kerr) throw Error{6, "sweep kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
   }
   SE1P_CUDA_TRY(cudaGetLastError());
 }
@@ -801,7 +801,7 @@ static void energy_forces_impl(const se1p_opts* o, cudaStream_t st, const double
     SE1P_CUDA_TRY(cudaStreamSynchronize(st));
     int kerr = 0;
     SE1P_CUDA_TRY(cudaMemcpy(&kerr, ds.w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (kerr) throw Error{6, "tile kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
+    if (kerr) throw Error{6, "sweep kernel internal bounds check failed (code " + std::to_string(kerr) + ")"};
   }
   SE1P_CUDA_TRY(cudaGetLastError());
 }
