@@ -57,6 +57,11 @@ constexpr int kNB = SE1P_SWEEP_NB;
 #define SE1P_SWEEP_GU 1
 #endif
 constexpr int kGU = SE1P_SWEEP_GU;
+// gather k-step of 16 particles with the operands swapped (w_z^T as A, the frame as B; 1) or of
+// 8 particles with the frame as A (0)
+#ifndef SE1P_GATHER_T16
+#define SE1P_GATHER_T16 1
+#endif
 constexpr int kMaxP = 64;
 
 // header flags of a batch
@@ -103,7 +108,7 @@ struct SweepArgs {
 };
 
 // list capacity per (slot, consumer warp): a batch's entries plus the k-step padding
-__host__ __device__ constexpr int sw_ls(int BM) { return BM + 8; }
+__host__ __device__ constexpr int sw_ls(int BM) { return BM + 16; }
 
 struct SweepSmem {
   int off_meta, off_mask, off_lists, off_lcnt, off_cb, off_raw, off_rows, off_acc, off_ring, total;
@@ -214,6 +219,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   constexpr int COFF = FM == 2 ? 3 : 0;           // first slot value of this pass
   constexpr int ACS = kCW * NC + 1;               // acc doubles per candidate (odd: conflict-free reduce)
   constexpr bool XL = GATHER;                     // consumer lists built by the expanders
+  constexpr bool T16 = GATHER && SE1P_GATHER_T16;   // 16-particle gather k-steps
+  constexpr int KS = T16 ? 16 : 8;                 // particles per k-step
   extern __shared__ __align__(128) unsigned char smem[];
   const KDev& dv = A.dv;
   const int BM = A.BM, NB = A.NB, P = dv.P, M = dv.M, Mt = dv.Mt;
@@ -677,9 +684,62 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
           for (int cc = 0; cc < NC; ++cc) acc[(int64_t)ep * ACS + w * NC + cc] = x[cc];
         }
       };
-      int k = k0;
-      for (; k + 16 <= k1 && kGU == 2; k += 16) gstep(std::integral_constant<int, kGU>(), k);
-      for (; k < k1; k += 8) gstep(std::integral_constant<int, 1>(), k);
+      // 16 particles per k-step with the operands swapped: D_nb[16 particles x 8 cols] =
+      // w_z^T[16 particles x 8 nodes] (A: the particles' z pairs, 16-byte loads) x H~^T (B: the
+      // same frame registers, column half nb); a lane then holds particles g, g + 8 at columns
+      // 2tg, 2tg + 1 of both halves, so the column sum is a 2-round butterfly over the quad
+      // (every lane of the quad reads the same 4 weights of a particle: x nodes xA, xA + 2,
+      // y nodes yA, yA + 1)
+      auto gstep16 = [&](int k) {
+        const int eg = wl[k + g], eg8 = wl[k + 8 + g];
+        const double* zg = rows + eg * RS + kZ + ((2 * tg) ^ (eg & 2));
+        const double* zg8 = rows + eg8 * RS + kZ + ((2 * tg) ^ (eg8 & 2));
+        double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NZB; ++j) {
+          const double2 za = *reinterpret_cast<const double2*>(zg + 8 * j);
+          const double2 zb = *reinterpret_cast<const double2*>(zg8 + 8 * j);
+          const double a[4] = {za.x, zb.x, za.y, zb.y};
+          dmma_16x8x8(d0, a, c[j][0], c[j][2]);
+          dmma_16x8x8(d1, a, c[j][1], c[j][3]);
+        }
+        const int xA = 4 * bxw + (tg >> 1), yA = 4 * byw + 2 * (tg & 1);
+        const int qA = ypos(yA) ^ 1, qB = ypos(yA + 1) ^ 1;
+        double v[2][NC];
+#pragma unroll
+        for (int pb = 0; pb < 2; ++pb) {
+          const int ep = pb ? eg8 : eg;
+          const double* rp = rows + ep * RS;
+          const int sp = ep & 6;
+          const double wxA = rp[xA ^ sp], wxB = rp[(xA + 2) ^ sp];
+          const double wyA = rp[16 + (qA ^ sp)], wyB = rp[16 + (qB ^ sp)];
+          const double sA = fma(wyA, d0[2 * pb], wyB * d0[2 * pb + 1]);   // x node xA
+          const double sB = fma(wyA, d1[2 * pb], wyB * d1[2 * pb + 1]);   // x node xA + 2
+          v[pb][0] = fma(wxA, sA, wxB * sB);
+          if (FM == 1) {   // column moments in tile coordinates
+            v[pb][1] = fma((double)xA * wxA, sA, (double)(xA + 2) * wxB * sB);
+            const double yAd = (double)yA;
+            const double tA = fma(yAd * wyA, d0[2 * pb], (yAd + 1.0) * wyB * d0[2 * pb + 1]);
+            const double tB = fma(yAd * wyA, d1[2 * pb], (yAd + 1.0) * wyB * d1[2 * pb + 1]);
+            v[pb][2] = fma(wxA, tA, wxB * tB);
+          }
+        }
+        const bool b1 = tg & 1;
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const double send = b1 ? v[0][cc] : v[1][cc];
+          double x = (b1 ? v[1][cc] : v[0][cc]) + __shfl_xor_sync(0xffffffffu, send, 1);
+          x += __shfl_xor_sync(0xffffffffu, x, 2);
+          if (tg < 2) acc[(int64_t)(b1 ? eg8 : eg) * ACS + w * NC + cc] = x;
+        }
+      };
+      if (T16) {
+        for (int k = k0; k < k1; k += 16) gstep16(k);
+      } else {
+        int k = k0;
+        for (; k + 16 <= k1 && kGU == 2; k += 16) gstep(std::integral_constant<int, kGU>(), k);
+        for (; k < k1; k += 8) gstep(std::integral_constant<int, 1>(), k);
+      }
     }
   };
 
@@ -756,9 +816,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
     SW_CTRACE(9);
     // k-steps of 8 entries; the group's last batch pads and runs everything, and so does a batch
     // that cannot fill one k-step on top of held entries (at most one batch is ever held)
-    int kend = tot & ~7;
+    int kend = tot & ~(KS - 1);
     if ((h.w & kLast) || (held > 0 && kend == 0)) {
-      kend = (tot + 7) & ~7;
+      kend = (tot + KS - 1) & ~(KS - 1);
       if (lane < kend - tot) Lw[n + lane] = (unsigned short)dummy;
       __syncwarp();
     }
@@ -769,19 +829,19 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
         fr = true;
       }
       if (held > 0) {   // one mixed k-step: the held entries (batch bprev), then this batch's first
-        if (lane >= held && lane < 8) cb[lane] = Lw[lane - held];
+        if (lane >= held && lane < KS) cb[lane] = Lw[lane - held];
         __syncwarp();
-        ksteps(cb, 0, 8);
+        ksteps(cb, 0, KS);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[bprev]);
         bprev = -1;
-        ksteps(Lw + 8 - held, 0, kend - 8);
+        ksteps(Lw + KS - held, 0, kend - KS);
       } else {
         ksteps(Lw, 0, kend);
       }
     }
     SW_CTRACE(10);
-    const int rest = max(tot - kend, 0);   // < 8, all from this batch (none after padding)
+    const int rest = max(tot - kend, 0);   // < KS, all from this batch (none after padding)
     const int mv = lane < rest ? Lw[kend - held + lane] : 0;
     __syncwarp();
     if (lane < rest) cb[lane] = (unsigned short)mv;
@@ -803,7 +863,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
 #if SE1P_SWEEP_TRACE
     if (w == 0 && lane == 0) {
       SW_TRACE(kc, 5, clock64());
-      SW_TRACE(kc, 6, kend / 8);
+      SW_TRACE(kc, 6, kend / KS);
       SW_TRACE(kc, 7, h.z);
     }
 #endif
