@@ -35,6 +35,9 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 #ifndef SE1P_MODES_TWO_STREAMS
 #define SE1P_MODES_TWO_STREAMS 2   // 1: kernel planes beside J planes; 2: and the J planes in two halves
 #endif
+#ifndef SE1P_MODES_JSPLIT
+#define SE1P_MODES_JSPLIT 2
+#endif
 #ifndef SE1P_FFT_THREADS
 #define SE1P_FFT_THREADS 256
 #endif
@@ -787,11 +790,15 @@ void k_mode_stage(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& 
         SE1P_CUDA_TRY(cudaEventCreateWithFlags(&w.ev_join2, cudaEventDisableTiming));
       }
       SE1P_CUDA_TRY(cudaStreamWaitEvent(w.side2, w.ev_fork, 0));
-      const int nJ1 = nJ / 2;
-      mode_class(pl, w, planes, L, PlaneSel{glJ, liJ, pl.n_kernel}, nJ1, pl.prm.SJ, pl.fJ, pl.twJ, baseJ, 0, st);
-      const PlaneSel S2{glJ ? glJ + nJ1 : nullptr, liJ ? liJ + nJ1 : nullptr, pl.n_kernel + nJ1};
-      mode_class(pl, w, planes, L, S2, nJ - nJ1, pl.prm.SJ, pl.fJ, pl.twJ, baseJ + (int64_t)nJ1 * Mt * pl.prm.SJ, 0,
-                 w.side2);
+      // SE1P_MODES_JSPLIT chunks, alternating between the two streams (smaller chunks keep each
+      // chunk's row-transformed planes T resident in L2 between its three passes)
+      const int nch = std::max(2, std::min(SE1P_MODES_JSPLIT, nJ / 4));
+      for (int ch = 0; ch < nch; ++ch) {
+        const int a0 = (int)((int64_t)nJ * ch / nch), a1 = (int)((int64_t)nJ * (ch + 1) / nch);
+        const PlaneSel Sc{glJ ? glJ + a0 : nullptr, liJ ? liJ + a0 : nullptr, pl.n_kernel + a0};
+        mode_class(pl, w, planes, L, Sc, a1 - a0, pl.prm.SJ, pl.fJ, pl.twJ, baseJ + (int64_t)a0 * Mt * pl.prm.SJ, 0,
+                   (ch & 1) ? w.side2 : st);
+      }
       SE1P_CUDA_TRY(cudaEventRecord(w.ev_join2, w.side2));
       SE1P_CUDA_TRY(cudaStreamWaitEvent(st, w.ev_join2, 0));
     } else
