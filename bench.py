@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dist", default="slab", choices=["slab", "rs"],
+                    help="N > 1: slab (x slabs + k3 modes, every rank holds all particles) or rs (the "
+                         "particle-split baseline: each rank holds N/R particles, planes reduce-scattered)")
     return ap.parse_args()
 
 
@@ -125,9 +128,14 @@ def bench_ours(args, cfg, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     x_np, q_np = make_system(cfg.N, cfg.L, cfg.seed)        # the same system on every rank
+    rs = world > 1 and args.dist == "rs"
+    if rs:   # the particle-split baseline: this rank holds (and uploads) only its share
+        a, b = cfg.N * rank // world, cfg.N * (rank + 1) // world
+        x_np, q_np = np.ascontiguousarray(x_np[a:b]), np.ascontiguousarray(q_np[a:b])
+    n_loc = q_np.shape[0]
     x = torch.from_numpy(x_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
-    phi = torch.empty(cfg.N, dtype=torch.float64, device=dev)
+    phi = torch.empty(n_loc, dtype=torch.float64, device=dev)
     # single GPU: a side stream so the step can run as a captured CUDA graph (the legacy default
     # stream cannot be captured); multi-GPU keeps torch's current stream for NCCL
     stream = torch.cuda.Stream(device=dev) if world == 1 else torch.cuda.current_stream(dev)
@@ -136,6 +144,8 @@ def bench_ours(args, cfg, rank, world, local):
     info = se1p.plan_info(cfg.L, cfg.xi, cfg.M, cfg.P, **kw)
 
     def step(xs=x, qs=q, out=phi):
+        if rs:
+            return sdist.kspace_rs(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, stream=stream, **kw)
         if world > 1:
             return sdist.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, stream=stream, **kw)
         se1p.kspace(xs, qs, cfg.L, cfg.xi, cfg.M, cfg.P, out=out, stream=stream, sync=False, skip_checks=True,
@@ -182,7 +192,7 @@ def bench_ours(args, cfg, rank, world, local):
     # device between events on the call's stream.  Multi-GPU: the torch-staged copies below.
     xh = torch.from_numpy(x_np).pin_memory()
     qh = torch.from_numpy(q_np).pin_memory()
-    ph = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
+    ph = torch.empty(n_loc, dtype=torch.float64).pin_memory()
     ke = max(3, args.steps // 2)
     e2e_pipelined = None
     if world == 1:
@@ -204,7 +214,7 @@ def bench_ours(args, cfg, rank, world, local):
     # streams, so step i+1's H2D and step i-1's D2H overlap step i; multi-GPU: one slot, serial.
     nslot = 2 if world == 1 else 1
     slots = [dict(x=torch.empty_like(x), q=torch.empty_like(q), phi=torch.empty_like(phi),
-                  ph=torch.empty(cfg.N, dtype=torch.float64).pin_memory(),
+                  ph=torch.empty(n_loc, dtype=torch.float64).pin_memory(),
                   loaded=torch.cuda.Event(), computed=torch.cuda.Event(), read=torch.cuda.Event())
              for _ in range(nslot)]
     h2d = torch.cuda.Stream(device=dev) if world == 1 else stream
@@ -253,8 +263,14 @@ def bench_ours(args, cfg, rank, world, local):
     # per-stage device times (separate profiled single-GPU passes; events on the launching stream)
     stage_sum = {}
     nprof = max(3, min(args.steps, 10))
+    if rs:   # the stage split of the whole system on this GPU
+        xf, qf = make_system(cfg.N, cfg.L, cfg.seed)
+        xp, qp = torch.from_numpy(xf).to(dev), torch.from_numpy(qf).to(dev)
+        pp = torch.empty(cfg.N, dtype=torch.float64, device=dev)
+    else:
+        xp, qp, pp = x, q, phi
     for _ in range(nprof):
-        se1p.kspace(x, q, cfg.L, cfg.xi, cfg.M, cfg.P, out=phi, stream=stream, skip_checks=True, profile=True, **kw)
+        se1p.kspace(xp, qp, cfg.L, cfg.xi, cfg.M, cfg.P, out=pp, stream=stream, skip_checks=True, profile=True, **kw)
         for k, v in se1p.stage_times().items():
             stage_sum[k] = stage_sum.get(k, 0.0) + v / nprof
     if launches_per_step is None:
@@ -286,7 +302,9 @@ def bench_ours(args, cfg, rank, world, local):
                                f"n_l={info['n_local']} S0={info['S0']} SI={info['SI']} Ntilde={info['Ntilde']} "
                                f"LK={info['LK']}",
                    "N": cfg.N,
-                   "parallelism": f"mode-sharded x{world} (x slabs + k3 planes, 2 all-to-all + all-reduce)"
+                   "parallelism": ("particle-split x%d (N/R particles per rank, planes summed at their owners "
+                                   "and gathered back: 2 all-to-all)" % world if rs else
+                                   f"mode-sharded x{world} (x slabs + k3 planes, 2 all-to-all + all-reduce)")
                                   if world > 1 else "single GPU",
                    "l2": "per-step working set %.0f MB (particle records, grid, planes) > 126 MB L2; no flush"
                          % (info["workspace_bytes"] / 1e6 + 700 * cfg.N / 1e6)},
@@ -306,7 +324,7 @@ def bench_ours(args, cfg, rank, world, local):
                 "frac": (b_alg / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]) if peaks.get("hbm_gbs") else None,
                 "note": "the path is FP64-bound (see roofline); DESIGN.md section 5"},
         "e2e": {"value": cfg.N / e2e_s, "unit": "particles/s",
-                "h2d_bytes_per_step": 32 * cfg.N * world, "d2h_bytes_per_step": 8 * cfg.N * world,
+                "h2d_bytes_per_step": 32 * cfg.N * (1 if rs else world), "d2h_bytes_per_step": 8 * cfg.N * (1 if rs else world),
                 "how": "C ABI se1p_kspace_ex with host buffers (pinned), synchronous per call" if world == 1
                        else "torch-staged pinned copies around the distributed step"},
         "e2e_pipelined": ({"value": e2e_pipelined, "unit": "particles/s",

@@ -19,6 +19,10 @@ Plane ownership: greedy longest-processing-time on cost ~ W^2 log2 W per plane (
 plane's transform extent: LK for k3 = 0 and the upsampled I modes, Ntilde otherwise), so the
 expensive upsampled planes spread over ranks.  The index bookkeeping
 (slab bounds, owners, split sizes) is plain Python and is unit-tested on CPU with gloo.
+
+kspace_rs / kspace_rank_rs: the particle-split baseline of SURVEY 8(e) (north_star literal:
+particles split, the grid reduce-scattered, the k3 modes distributed, the inverse gathered back),
+built from the same three entries over the whole grid.
 """
 from __future__ import annotations
 
@@ -202,6 +206,71 @@ def kspace_emulated(x, q, plan: DistPlan, backend):
     return phi
 
 
+# ------------------------------------------------------------------ particle-split baseline
+def rs_chunks(plan: DistPlan) -> list:
+    """Full-grid plane buffer [M/2+1 slots in owner order][Mt][Mt] complex: the float64 sizes of
+    the owners' chunks (owner q's planes, all rows)."""
+    return [2 * plan.count(q) * plan.Mt * plan.Mt for q in range(plan.R)]
+
+
+def kspace_rank_rs(x, q, plan: DistPlan, backend, rank: int, group=None):
+    """SPMD body of the north_star-literal baseline: rank r holds only ITS particles
+    (x [N_r, 3], q [N_r]) and returns phi^F of them.
+
+      1. forward over the whole grid (x rows [0, Mt)): its particles' gridding and z-transform,
+         i.e. their partial spectrum of every plane (the transforms are linear);
+      2. reduce-scatter: owner q receives the sum over ranks of its planes (all-to-all of the plane
+         chunks, then a local sum in rank order -- deterministic, and gloo has no reduce-scatter);
+      3. the mode stage on the owned planes (one slab: bounds [0, Mt]);
+      4. all-gather: every rank receives every processed plane (all-to-all of its chunk);
+      5. backward over the whole grid: inverse z-transform and the gather of its own particles
+         (no all-reduce: each rank owns its particles' phi).
+    Against the slab path it trades the full-N gridding/gather on every rank for full-grid
+    transforms on every rank and full-grid collectives (2 x (M/2+1) Mt^2 complex per rank)."""
+    import torch
+    import torch.distributed as dist
+    R, r, Mt = plan.R, rank, plan.Mt
+    N = q.shape[0]
+    full = backend.forward(x, q, 0, Mt, plan.order)
+    shape = full.shape
+    sizes = rs_chunks(plan)
+    flat = full.reshape(-1)
+    recv = torch.empty(R * sizes[r], dtype=flat.dtype, device=flat.device)
+    dist.all_to_all_single(recv, flat, [sizes[r]] * R, sizes, group=group)
+    mine = recv[:sizes[r]].clone()
+    for src in range(1, R):
+        mine += recv[src * sizes[r]:(src + 1) * sizes[r]]
+    backend.modes(mine, plan.owned[r], [0, Mt])
+    out = torch.empty_like(flat)
+    dist.all_to_all_single(out, mine.repeat(R), sizes, [sizes[r]] * R, group=group)
+    return backend.backward(out.reshape(shape), N, 0, Mt, plan.order)
+
+
+def kspace_emulated_rs(x, q, plan: DistPlan, backend, parts):
+    """kspace_rank_rs for all ranks in turn in one process; parts[r] = (lo, hi) particle range of
+    rank r.  Returns phi^F of all particles (rank ranges concatenated)."""
+    import torch
+    R, Mt = plan.R, plan.Mt
+    sizes = rs_chunks(plan)
+    fulls = [backend.forward(x[a:b], q[a:b], 0, Mt, plan.order).reshape(-1).clone() for a, b in parts]
+    shape = None
+    owned = []
+    for r in range(R):
+        chunk = None
+        for src in range(R):
+            c = torch.split(fulls[src], sizes)[r]
+            chunk = c.clone() if chunk is None else chunk + c
+        backend.modes(chunk, plan.owned[r], [0, Mt])
+        owned.append(chunk)
+    allp = torch.cat(owned)
+    out = []
+    for r, (a, b) in enumerate(parts):
+        full = backend.forward(x[a:b], q[a:b], 0, Mt, plan.order)   # this rank's particle state
+        shape = full.shape
+        out.append(backend.backward(allp.reshape(shape).clone(), b - a, 0, Mt, plan.order).clone())
+    return torch.cat(out)
+
+
 _PLANS = {}
 
 
@@ -214,6 +283,19 @@ def cached_plan(L, xi, M, P, R, **kw):
     if key not in _PLANS:
         _PLANS[key] = make_plan(se1p.plan_info(L, xi, M, P, **pk), R)
     return _PLANS[key]
+
+
+def kspace_rs(x, q, L, xi, M, P, group=None, stream=None, **kw):
+    """phi^F of this rank's particles (x [N_r, 3], q [N_r]; CUDA float64) of one system whose
+    particles are split over the ranks of `group` (the particle-split baseline, kspace_rank_rs)."""
+    import torch
+    import torch.distributed as dist
+    R = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    plan = cached_plan(L, xi, M, P, R, **kw)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.stream(st):
+        return kspace_rank_rs(x, q, plan, CudaBackend(L, xi, M, P, stream=st, **kw), rank, group)
 
 
 def kspace(x, q, L, xi, M, P, group=None, stream=None, **kw):

@@ -39,6 +39,7 @@ class NumpyStages:
 
     def forward(self, x, q, x_lo, x_hi, order):
         d = self.d
+        self.x = x.numpy()   # the particles a later backward gathers (the device keeps them the same way)
         H = sd.gridding(x.numpy(), q.numpy(), self.xi, d["h"], self.P, self.M, self.Mt, self.Mt, d["eta"])
         Hz = np.fft.fft(H, axis=2)[:, :, :self.n_planes]
         slab = np.ascontiguousarray(np.stack([Hz[x_lo:x_hi, :, n] for n in order]))   # [slot][W][Mt]
@@ -192,3 +193,47 @@ def test_gloo_spmd_matches_alg1(world, tmp_path):
     for r in range(world):
         phi = np.load(f"{out}.{r}.npy")
         assert np.max(np.abs(phi - ref)) <= 1e-12 * np.max(np.abs(ref)), r
+
+
+# ---------------------------------------------------------------- particle-split baseline
+def _parts(N, R):
+    b = [N * r // R for r in range(R + 1)]
+    return [(b[r], b[r + 1]) for r in range(R)]
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_emulated_particle_split_matches_alg1(R):
+    """kspace_rank_rs for all ranks in turn: each rank grids and gathers only its particles over
+    the whole grid, the planes are summed at their owners (reduce-scatter), transformed, and
+    gathered back; the concatenated phi equals the single-process Alg. 1 oracle."""
+    x, q, ref = _reference()
+    st = _stages(x)
+    plan = sdist.make_plan(_info(st), R)
+    phi = sdist.kspace_emulated_rs(torch.from_numpy(x), torch.from_numpy(q), plan, st, _parts(len(q), R)).numpy()
+    assert np.max(np.abs(phi - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def _worker_rs(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, q, ref = _reference()
+        a, b = _parts(len(q), world)[rank]
+        st = _stages(x)
+        plan = sdist.make_plan(_info(st), world)
+        phi = sdist.kspace_rank_rs(torch.from_numpy(x[a:b]), torch.from_numpy(q[a:b]), plan, st, rank).numpy()
+        np.save(f"{result_path}.{rank}.npy", phi)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_particle_split_matches_alg1(world, tmp_path):
+    """The particle-split SPMD body over gloo: every rank's phi equals the oracle on its particles."""
+    x, q, ref = _reference()
+    out = str(tmp_path / "phi")
+    mp.spawn(_worker_rs, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r, (a, b) in enumerate(_parts(len(q), world)):
+        phi = np.load(f"{out}.{r}.npy")
+        assert phi.shape == (b - a,)
+        assert np.max(np.abs(phi - ref[a:b])) <= 1e-12 * np.max(np.abs(ref)), r

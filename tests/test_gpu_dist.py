@@ -54,6 +54,24 @@ def test_emulated_ranks_match_alg1_oracle():
     assert np.max(np.abs(phi - ref)) <= 1e-11 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("cfg,R", [("C2", 2), ("C3", 3), ("C4", 4)])
+def test_emulated_particle_split_matches_single_gpu(cfg, R):
+    """The particle-split baseline (dist.kspace_rank_rs): every rank grids and
+    gathers only its particles over the whole grid; the planes are summed at their owners,
+    transformed there and gathered back.  Emulated ranks in turn equal the single-GPU result."""
+    c = CONFIGS[cfg]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    kw = kspace_kwargs(c)
+    ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw).cpu().numpy()
+    plan = sdist.make_plan(se1p.plan_info(c.L, c.xi, c.M, c.P, **kw), R)
+    b = [c.N * r // R for r in range(R + 1)]
+    parts = [(b[r], b[r + 1]) for r in range(R)]
+    phi = sdist.kspace_emulated_rs(xd, qd, plan, sdist.CudaBackend(c.L, c.xi, c.M, c.P, **kw), parts)
+    got = phi.cpu().numpy()
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref)), (cfg, R)
+
+
 def test_backward_requires_matching_forward():
     c = CONFIGS["C2"]
     kw = kspace_kwargs(c)
@@ -77,6 +95,26 @@ def test_nccl_world_one():
         phi = sdist.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
         ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
         assert torch.equal(phi, ref)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_world_one_particle_split():
+    """dist.kspace_rs over NCCL with world size 1 equals the single-GPU result."""
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        c = CONFIGS["C3"]
+        x, q = make_system(c.N, c.L, c.seed)
+        xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+        kw = kspace_kwargs(c)
+        phi = sdist.kspace_rs(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+        ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+        assert np.max(np.abs((phi - ref).cpu().numpy())) <= 1e-13 * float(ref.abs().max())
     finally:
         dist.destroy_process_group()
 
