@@ -386,3 +386,47 @@ def _factors(n):
             n //= d
         d += 1
     return f + ([n] if n > 1 else [])
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_plans_and_workspaces_are_per_device():
+    """The same parameters on cuda:0 and cuda:1 (plans keyed on the device): each
+    device's result equals the other's bitwise, and releasing one device leaves the other's plan
+    usable."""
+    c = CONFIGS["C2"]
+    x, q = make_system(c.N, c.L, c.seed)
+    kw = kspace_kwargs(c)
+    outs = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            xd = torch.from_numpy(x).to(f"cuda:{d}")
+            qd = torch.from_numpy(q).to(f"cuda:{d}")
+            outs.append(se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw).cpu())
+    assert torch.equal(outs[0], outs[1])
+    with torch.cuda.device(0):
+        se1p.release()
+    with torch.cuda.device(1):
+        xd, qd = torch.from_numpy(x).to("cuda:1"), torch.from_numpy(q).to("cuda:1")
+        assert torch.equal(se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw).cpu(), outs[1])
+
+
+def test_stream_ordered_calls_on_two_streams():
+    """Asynchronous calls on two streams share the device's workspace: each call's stream waits
+    for the previous call's work, so interleaved k-space and real-space calls on
+    different streams return the results of the same calls made synchronously."""
+    c = CONFIGS["C3"]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    kw = kspace_kwargs(c)
+    ref_k = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
+    ref_r = se1p.real(xd, qd, c.L, c.xi, c.rc)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for i in range(3):
+        st = s1 if i % 2 == 0 else s2
+        outs.append(("k", se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, stream=st, sync=False, skip_checks=True, **kw)))
+        st2 = s2 if i % 2 == 0 else s1
+        outs.append(("r", se1p.real(xd, qd, c.L, c.xi, c.rc, stream=st2, sync=False, skip_checks=True)))
+    torch.cuda.synchronize()
+    for kind, o in outs:
+        assert torch.equal(o, ref_k if kind == "k" else ref_r), kind
