@@ -131,8 +131,8 @@ __host__ __device__ inline SweepSmem sweep_smem(int BM, int NB, int NZB, bool ga
   o = (o + 15) & ~15;
   s.off_lcnt = o;
   o += NB * kCW * 4;
-  s.off_cb = o;      // per-warp carry lists
-  o += kCW * 16 * 2;
+  s.off_cb = o;      // per-warp carry lists (two, alternating)
+  o += kCW * 32 * 2;
   o = (o + 127) & ~127;
   s.off_raw = o;
   o += kNR * BM * rec_stride(NZB) * 8;
@@ -528,7 +528,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
   // gridding: B lane g holds frame node sg = (g >> 1) + 4 (g & 1), so C lane tg holds nodes tg, tg + 4;
   // gather: K index tg (tg + 4) of block j is node 2 tg (2 tg + 1): one 16-byte pair of the record
   const int sg = (g >> 1) + 4 * (g & 1);
-  unsigned short* cb = reinterpret_cast<unsigned short*>(smem + L.off_cb) + w * 16;   // carried entries
+  // carried entries: two buffers per warp, so a batch's left-overs are copied out before its
+  // k-steps (the copy then does not wait behind the k-steps' shared-memory traffic)
+  unsigned short* cbw = reinterpret_cast<unsigned short*>(smem + L.off_cb) + w * 32;
+  int cbsel = 0;
   double* rg = ring + w * 16 * S;   // gridding ring [16 cols][S]
 
   int cur = -1, X0 = 0, Y0 = 0, Z0 = 0, Ck = 0, zc = 0;
@@ -822,6 +825,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       if (lane < kend - tot) Lw[n + lane] = (unsigned short)dummy;
       __syncwarp();
     }
+    unsigned short* cb = cbw + 16 * cbsel;         // this batch's held entries (from bprev)
+    unsigned short* cbn = cbw + 16 * (cbsel ^ 1);  // its own left-overs for the next batch
+    const int rest = max(tot - kend, 0);   // < KS, all from this batch (none after padding)
+    if (lane < rest) cbn[lane] = Lw[kend - held + lane];
     if (kend > 0) {
       if (!fr) {
         if (GATHER) frame_load_gather();
@@ -841,10 +848,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs A) {
       }
     }
     SW_CTRACE(10);
-    const int rest = max(tot - kend, 0);   // < KS, all from this batch (none after padding)
-    const int mv = lane < rest ? Lw[kend - held + lane] : 0;
-    __syncwarp();
-    if (lane < rest) cb[lane] = (unsigned short)mv;
+    if (rest > 0) cbsel ^= 1;
     held = rest;
     if (h.w & kLast) {
       if (!GATHER && fr) {
