@@ -273,6 +273,69 @@ __device__ double2* fft_rows(double2* buf, double2* tmp, const FftDesc& d, const
   return in;
 }
 
+// ------------------------------------------------------------------ compile-time plans
+// The same Stockham stages with the length, the rows per block and every stage's radix and
+// stride known at compile time (index splits by constants, no radix switch, no per-stage
+// branches): used where a plan's extents match one of the instantiated shapes (modes.cu).
+template <int R, int DIR, int N, int NS, int NROWS>
+__device__ __forceinline__ void stage_ct(const double2* __restrict__ in, double2* __restrict__ out,
+                                         const double2* __restrict__ tw, int rowstride, int tid, int nthr) {
+  constexpr int NB = N / R;
+  for (int t = tid; t < NB * NROWS; t += nthr) {
+    const int row = t / NB, j = t - row * NB;
+    const int k = j % NS;
+    const double2* src = in + row * rowstride + j;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = src[q * NB];
+    if (NS > 1 && k > 0) {
+#pragma unroll
+      for (int q = 1; q < R; ++q) {
+        const double2 w = tw[k * (R - 1) + q - 1];
+        v[q] = DIR < 0 ? cmul(v[q], w) : cmulc(v[q], w);
+      }
+    }
+    bfly_fixed<R, DIR>(v);
+    double2* dst = out + row * rowstride + (j / NS) * NS * R + k;
+#pragma unroll
+    for (int q = 0; q < R; ++q) dst[q * NS] = v[q];
+  }
+}
+
+template <int DIR, int N, int NROWS, int NS, int R, int... Rest>
+__device__ __forceinline__ double2* fft_ct(double2* in, double2* out, const FftDesc& d, const double2* __restrict__ tw,
+                                           int s, int rowstride, int tid, int nthr) {
+  stage_ct<R, DIR, N, NS, NROWS>(in, out, tw + d.twoff[s], rowstride, tid, nthr);
+  __syncthreads();
+  if constexpr (sizeof...(Rest) == 0) {
+    return out;
+  } else {
+    return fft_ct<DIR, N, NROWS, NS * R, Rest...>(out, in, d, tw, s + 1, rowstride, tid, nthr);
+  }
+}
+
+// plan shapes with compile-time kernels (0: the generic fft_rows)
+constexpr int kPlanGeneric = 0, kPlan320 = 1, kPlan576 = 2;
+inline int fft_plan_shape(const FftDesc& d) {
+  if (d.n == 320 && d.nst == 3 && d.rad[0] == 5 && d.rad[1] == 8 && d.rad[2] == 8) return kPlan320;
+  if (d.n == 576 && d.nst == 3 && d.rad[0] == 9 && d.rad[1] == 8 && d.rad[2] == 8) return kPlan576;
+  return kPlanGeneric;
+}
+
+// rows of a block through the compile-time plan SHAPE (NROWS rows) or the generic one
+template <int DIR, int SHAPE, int NROWS>
+__device__ __forceinline__ double2* fft_rows_sh(double2* buf, double2* tmp, const FftDesc& d,
+                                                const double2* __restrict__ tw, int nrows, int rowstride, int tid,
+                                                int nthr) {
+  if constexpr (SHAPE == kPlan320) {
+    return fft_ct<DIR, 320, NROWS, 1, 5, 8, 8>(buf, tmp, d, tw, 0, rowstride, tid, nthr);
+  } else if constexpr (SHAPE == kPlan576) {
+    return fft_ct<DIR, 576, NROWS, 1, 9, 8, 8>(buf, tmp, d, tw, 0, rowstride, tid, nthr);
+  } else {
+    return fft_rows<DIR>(buf, tmp, d, tw, nrows, rowstride, tid, nthr);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 // Factorise n into stage radices: odd ones first (9 if r8, 3, 5), then 8 (if r8), 4, 2, then any
 // other prime.  Returns false if a prime factor exceeds kMaxGenericRadix or there are too many

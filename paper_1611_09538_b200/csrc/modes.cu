@@ -229,7 +229,7 @@ __device__ __forceinline__ double rcp_nr(double d) {
 
 // Column pass: FFT along x, multiply, inverse FFT along x, keep rows < Mt.
 // kernel_class: multiplier = khat[n][a][y] (n < n_kernel); else the J-plane scaling of plane n.
-template <int CB>
+template <int CB, int SHAPE>
 __global__ void __launch_bounds__(kColMaxThreads, 2) k_colpass(int Mt, int W, int64_t base, FftDesc f, const double2* __restrict__ tw,
                           double2* __restrict__ T, int kernel_class, const double* __restrict__ khat,
                           const double* __restrict__ exJ, const double* __restrict__ k2J,
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kColMaxThreads, 2) k_colpass(int Mt, int W, in
 #ifndef SE1P_COLPASS_EXP   // experiment builds: 1 no FFTs, 2 no multiply, 3 neither
 #define SE1P_COLPASS_EXP 0
 #endif
-  double2* out = (SE1P_COLPASS_EXP & 1) ? buf : fft_rows<-1>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
+  double2* out = (SE1P_COLPASS_EXP & 1) ? buf : fft_rows_sh<-1, SHAPE, CB>(buf, tmp, f, tw, CB, SW, threadIdx.x, blockDim.x);
   double2* oth = (out == buf) ? tmp : buf;
   const double2 pn = pl[n];
   // flat loop over the CB x W entries with the (c, a) split carried incrementally (no division)
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kColMaxThreads, 2) k_colpass(int Mt, int W, in
     }
   }
   __syncthreads();
-  double2* res = (SE1P_COLPASS_EXP & 1) ? out : fft_rows<1>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
+  double2* res = (SE1P_COLPASS_EXP & 1) ? out : fft_rows_sh<1, SHAPE, CB>(out, oth, f, tw, CB, SW, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < Mt * CB; idx += blockDim.x) {
     const int a = idx / CB, c = idx - a * CB;
     if (c < nc) Tp[(int64_t)a * W + y0 + c] = res[c * SW + a];
@@ -687,14 +687,28 @@ static int col_threads(const FftDesc& f, int CB) {
   return best;
 }
 
+#ifndef SE1P_FFT_CT   // compile-time FFT plans for the shapes fft_plan_shape knows (0: generic only)
+#define SE1P_FFT_CT 1
+#endif
+template <int CB, int SHAPE>
+static void colpass_launch_sh(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
+                              int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
+  const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2) + (kernel_class ? (size_t)CB * W * sizeof(double) : 0);
+  set_smem((const void*)k_colpass<CB, SHAPE>, smc);
+  k_colpass<CB, SHAPE><<<dim3((unsigned)ceil_div(W, CB), nplanes), col_threads(f, CB), smc, st>>>(
+      pl.dv.Mt, W, base, f, tw, w.T, kernel_class, pl.d_khat, pl.d_exJ, pl.d_k2J, (const double2*)pl.d_pl, S);
+  SE1P_LAUNCH_CHECK();
+}
 template <int CB>
 static void colpass_launch(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
                            int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
-  const size_t smc = 2 * (size_t)CB * (W + 1) * sizeof(double2) + (kernel_class ? (size_t)CB * W * sizeof(double) : 0);
-  set_smem((const void*)k_colpass<CB>, smc);
-  k_colpass<CB><<<dim3((unsigned)ceil_div(W, CB), nplanes), col_threads(f, CB), smc, st>>>(
-      pl.dv.Mt, W, base, f, tw, w.T, kernel_class, pl.d_khat, pl.d_exJ, pl.d_k2J, (const double2*)pl.d_pl, S);
-  SE1P_LAUNCH_CHECK();
+  const int shape = SE1P_FFT_CT ? fft_plan_shape(f) : kPlanGeneric;
+  if (shape == kPlan320)
+    colpass_launch_sh<CB, kPlan320>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
+  else if (shape == kPlan576)
+    colpass_launch_sh<CB, kPlan576>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
+  else
+    colpass_launch_sh<CB, kPlanGeneric>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
 }
 
 static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, PlaneSel S, int nplanes,
