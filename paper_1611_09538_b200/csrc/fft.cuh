@@ -315,8 +315,9 @@ __device__ __forceinline__ double2* fft_ct(double2* in, double2* out, const FftD
 }
 
 // plan shapes with compile-time kernels (0: the generic fft_rows)
-constexpr int kPlanGeneric = 0, kPlan320 = 1, kPlan576 = 2;
+constexpr int kPlanGeneric = 0, kPlan320 = 1, kPlan576 = 2, kPlan256 = 3;
 inline int fft_plan_shape(const FftDesc& d) {
+  if (d.n == 256 && d.nst == 4 && d.rad[0] == 4 && d.rad[1] == 4 && d.rad[2] == 4 && d.rad[3] == 4) return kPlan256;
   if (d.n == 320 && d.nst == 3 && d.rad[0] == 5 && d.rad[1] == 8 && d.rad[2] == 8) return kPlan320;
   if (d.n == 576 && d.nst == 3 && d.rad[0] == 9 && d.rad[1] == 8 && d.rad[2] == 8) return kPlan576;
   return kPlanGeneric;
@@ -331,6 +332,8 @@ __device__ __forceinline__ double2* fft_rows_sh(double2* buf, double2* tmp, cons
     return fft_ct<DIR, 320, NROWS, 1, 5, 8, 8>(buf, tmp, d, tw, 0, rowstride, tid, nthr);
   } else if constexpr (SHAPE == kPlan576) {
     return fft_ct<DIR, 576, NROWS, 1, 9, 8, 8>(buf, tmp, d, tw, 0, rowstride, tid, nthr);
+  } else if constexpr (SHAPE == kPlan256) {
+    return fft_ct<DIR, 256, NROWS, 1, 4, 4, 4, 4>(buf, tmp, d, tw, 0, rowstride, tid, nthr);
   } else {
     return fft_rows<DIR>(buf, tmp, d, tw, nrows, rowstride, tid, nthr);
   }

@@ -35,6 +35,9 @@ static int zcols(int M) { return M >= 256 ? 16 : (M >= 64 ? 32 : 64); }   // col
 #ifndef SE1P_MODES_TWO_STREAMS
 #define SE1P_MODES_TWO_STREAMS 2   // 1: kernel planes beside J planes; 2: and the J planes in two halves
 #endif
+#ifndef SE1P_FFT_CT   // compile-time FFT plans for the shapes fft_plan_shape knows (0: generic only)
+#define SE1P_FFT_CT 1
+#endif
 #ifndef SE1P_MODES_JSPLIT
 #define SE1P_MODES_JSPLIT 2
 #endif
@@ -92,7 +95,7 @@ constexpr int kLdU = SE1P_LDU;
 // their spectra separate as A[n] = (Z[n] + conj Z[M-n])/2, B[n] = (Z[n] - conj Z[M-n])/(2i).
 // CB (columns per block) is a template constant and M's log2 (or -1) is passed, so the index
 // splits below are shifts, not integer divisions by runtime values.
-template <int CB>
+template <int CB, int SHAPE = kPlanGeneric>
 __global__ void SE1P_FFT_LBZ k_zfwd(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double* __restrict__ grid, double2* __restrict__ planes, SlabLayout L,
                        const int* __restrict__ slot_of) {
@@ -116,7 +119,7 @@ __global__ void SE1P_FFT_LBZ k_zfwd(int Mt, int M, int mshift, int nplanes, FftD
         bd[2 * ((c >> 1) * S + k) + (c & 1)] = v;
       });
   __syncthreads();
-  double2* out = fft_rows<-1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
+  double2* out = fft_rows_sh<-1, SHAPE, CH>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   for (int idx = threadIdx.x; idx < nplanes * CB; idx += blockDim.x) {
     const int n = idx / CB, c = idx - n * CB;
     if (y0 + c < Mt) {
@@ -130,7 +133,7 @@ __global__ void SE1P_FFT_LBZ k_zfwd(int Mt, int M, int mshift, int nplanes, FftD
 
 // Inverse: the Hermitian spectra a, b of columns 2r, 2r+1 combine into W[n] = a[n] + i b[n],
 // W[M-n] = conj a[n] + i conj b[n]; the complex inverse FFT gives col_2r + i col_2r+1.
-template <int CB>
+template <int CB, int SHAPE = kPlanGeneric>
 __global__ void SE1P_FFT_LBZ k_zinv(int Mt, int M, int mshift, int nplanes, FftDesc fz, const double2* __restrict__ tw,
                        const double2* __restrict__ planes, double* __restrict__ grid, SlabLayout L,
                        const int* __restrict__ slot_of) {
@@ -155,7 +158,7 @@ __global__ void SE1P_FFT_LBZ k_zinv(int Mt, int M, int mshift, int nplanes, FftD
         if (n > 0 && 2 * n < M) buf[r * S + (M - n)] = make_double2(ab.x + ab.w, ab.z - ab.y);   // Hermitian half
       });
   __syncthreads();
-  double2* out = fft_rows<1>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
+  double2* out = fft_rows_sh<1, SHAPE, CH>(buf, tmp, fz, tw, CH, S, threadIdx.x, blockDim.x);
   double* dst = grid + ((int64_t)x * Mt + y0) * M;
   for (int idx = threadIdx.x; idx < CB * M; idx += blockDim.x) {
     const int c = mshift >= 0 ? idx >> mshift : idx / M, k = idx - c * M;
@@ -360,6 +363,7 @@ __global__ void __launch_bounds__(SE1P_FFT_THREADS, MINB) k_persist(const PassT 
 }
 
 // rows of a plane: item = (plane by, row group); planes -> FFT along y -> T
+template <int SHAPE, int NR>   // compile-time plan and rows per item (generic: RB at run time)
 struct RowFwdPass {
   int n_items, slot, nxb, Mt, W, RB;
   int64_t base;
@@ -380,7 +384,7 @@ struct RowFwdPass {
     }
   }
   __device__ const double2* compute(int, double2* b, double2* t) const {
-    return fft_rows<-1>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
+    return fft_rows_sh<-1, SHAPE, NR>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
   }
   __device__ void store(int it, const double2* res) const {
     const int by = it / nxb, x0 = (it - by * nxb) * RB, nr = min(RB, Mt - x0);
@@ -390,6 +394,7 @@ struct RowFwdPass {
 };
 
 // inverse rows: T -> inverse FFT along y -> planes (y < Mt)
+template <int SHAPE, int NR>
 struct RowInvPass {
   int n_items, slot, nxb, Mt, W, RB;
   int64_t base;
@@ -408,7 +413,7 @@ struct RowInvPass {
     }
   }
   __device__ const double2* compute(int, double2* b, double2* t) const {
-    return fft_rows<1>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
+    return fft_rows_sh<1, SHAPE, NR>(b, t, f, tw, RB, W, threadIdx.x, blockDim.x);
   }
   __device__ void store(int it, const double2* res) const {
     const int by = it / nxb, x0 = (it - by * nxb) * RB, i = S.slot(by), nr = min(RB, Mt - x0);
@@ -482,7 +487,7 @@ struct ColPass {
 };
 
 // z-FFT: item = (grid row x, column block of CB); two real columns per complex FFT (see k_zfwd)
-template <int CB>
+template <int CB, int SHAPE = kPlanGeneric>
 struct ZfwdPass {
   int n_items, slot, ncb, Mt, M, mshift, nplanes;
   FftDesc f;
@@ -502,7 +507,7 @@ struct ZfwdPass {
     }
   }
   __device__ const double2* compute(int, double2* b, double2* t) const {
-    return fft_rows<-1>(b, t, f, tw, CB / 2, M + 1, threadIdx.x, blockDim.x);
+    return fft_rows_sh<-1, SHAPE, CB / 2>(b, t, f, tw, CB / 2, M + 1, threadIdx.x, blockDim.x);
   }
   __device__ void store(int it, const double2* out) const {
     const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB, S = M + 1;
@@ -520,7 +525,7 @@ struct ZfwdPass {
 
 // inverse z-FFT: the slot first holds the raw (a, b) spectrum pairs, combined into the FFT input
 // in the other buffer (see k_zinv)
-template <int CB>
+template <int CB, int SHAPE = kPlanGeneric>
 struct ZinvPass {
   int n_items, slot, ncb, Mt, M, mshift, nplanes;
   FftDesc f;
@@ -550,7 +555,7 @@ struct ZinvPass {
       if (n > 0 && 2 * n < M) t[r * S + (M - n)] = make_double2(a.x + bb.y, bb.x - a.y);   // Hermitian half
     }
     __syncthreads();
-    return fft_rows<1>(t, b, f, tw, CH, S, threadIdx.x, blockDim.x);
+    return fft_rows_sh<1, SHAPE, CH>(t, b, f, tw, CH, S, threadIdx.x, blockDim.x);
   }
   __device__ void store(int it, const double2* out) const {
     const int xr = it / ncb, x = L.xlo[0] + xr, y0 = (it - xr * ncb) * CB, S = M + 1;
@@ -581,13 +586,13 @@ static void persist_launch(const PassT& P, cudaStream_t st) {
   SE1P_LAUNCH_CHECK();
 }
 
-template <int CB>
-static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
-                        int rows, cudaStream_t st) {
+template <int CB, int SHAPE>
+static void zfwd_launch_sh(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
+                           int rows, cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt;
 #if SE1P_PERSIST & 1
   {
-    ZfwdPass<CB> P{};
+    ZfwdPass<CB, SHAPE> P{};
     P.ncb = (int)ceil_div(Mt, CB);
     P.n_items = P.ncb * rows;
     P.slot = (CB / 2) * (M + 1);
@@ -601,25 +606,25 @@ static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLa
     P.planes = planes;
     P.L = L;
     P.slot_of = slot_of;
-    persist_launch<ZfwdPass<CB>, SE1P_FFT_MINB_Z>(P, st);
+    persist_launch<ZfwdPass<CB, SHAPE>, SE1P_FFT_MINB_Z>(P, st);
     return;
   }
 #endif
   const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
-  set_smem((const void*)k_zfwd<CB>, smem);
+  set_smem((const void*)k_zfwd<CB, SHAPE>, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zfwd<CB><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, w.grid,
+  k_zfwd<CB, SHAPE><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, w.grid,
                                               planes, L, slot_of);
   SE1P_LAUNCH_CHECK();
 }
 
-template <int CB>
-static void zinv_launch(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
-                        int rows, cudaStream_t st) {
+template <int CB, int SHAPE>
+static void zinv_launch_sh(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
+                           int rows, cudaStream_t st) {
   const int M = pl.dv.M, Mt = pl.dv.Mt;
 #if SE1P_PERSIST & 2
   {
-    ZinvPass<CB> P{};
+    ZinvPass<CB, SHAPE> P{};
     P.ncb = (int)ceil_div(Mt, CB);
     P.n_items = P.ncb * rows;
     P.slot = std::max((CB / 2) * (M + 1), 2 * pl.n_planes * (CB / 2));
@@ -633,16 +638,36 @@ static void zinv_launch(const KPlan& pl, KWork& w, const double2* planes, const 
     P.grid = w.grid;
     P.L = L;
     P.slot_of = slot_of;
-    persist_launch<ZinvPass<CB>, SE1P_FFT_MINB_Z>(P, st);
+    persist_launch<ZinvPass<CB, SHAPE>, SE1P_FFT_MINB_Z>(P, st);
     return;
   }
 #endif
   const size_t smem = 2 * (size_t)(CB / 2) * (M + 1) * sizeof(double2);
-  set_smem((const void*)k_zinv<CB>, smem);
+  set_smem((const void*)k_zinv<CB, SHAPE>, smem);
   dim3 grid((unsigned)ceil_div(Mt, CB), (unsigned)rows);
-  k_zinv<CB><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, planes,
+  k_zinv<CB, SHAPE><<<grid, kFftThreads, smem, st>>>(Mt, M, log2_or_neg(M), pl.n_planes, pl.fz, pl.d_tw + pl.twz, planes,
                                               w.grid, L, slot_of);
   SE1P_LAUNCH_CHECK();
+}
+
+// the z-FFT with the compile-time 256-point plan where it applies (16 columns: 8 rows)
+template <int CB>
+static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
+                        int rows, cudaStream_t st) {
+  // (measured: the compile-time plan makes the forward z-FFT slower, 0.163 -> 0.179 ms at C5,
+  // while the persistent inverse gains, 0.161 -> 0.147 ms)
+  if (SE1P_FFT_CT > 1 && CB == 16 && fft_plan_shape(pl.fz) == kPlan256)
+    zfwd_launch_sh<CB, kPlan256>(pl, w, planes, L, slot_of, rows, st);
+  else
+    zfwd_launch_sh<CB, kPlanGeneric>(pl, w, planes, L, slot_of, rows, st);
+}
+template <int CB>
+static void zinv_launch(const KPlan& pl, KWork& w, const double2* planes, const SlabLayout& L, const int* slot_of,
+                        int rows, cudaStream_t st) {
+  if (SE1P_FFT_CT && CB == 16 && fft_plan_shape(pl.fz) == kPlan256)
+    zinv_launch_sh<CB, kPlan256>(pl, w, planes, L, slot_of, rows, st);
+  else
+    zinv_launch_sh<CB, kPlanGeneric>(pl, w, planes, L, slot_of, rows, st);
 }
 
 void k_zfft_forward(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
@@ -687,9 +712,6 @@ static int col_threads(const FftDesc& f, int CB) {
   return best;
 }
 
-#ifndef SE1P_FFT_CT   // compile-time FFT plans for the shapes fft_plan_shape knows (0: generic only)
-#define SE1P_FFT_CT 1
-#endif
 template <int CB, int SHAPE>
 static void colpass_launch_sh(const KPlan& pl, KWork& w, int nplanes, int W, const FftDesc& f, const double2* tw,
                               int64_t base, int kernel_class, PlaneSel S, cudaStream_t st) {
@@ -720,8 +742,27 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
   {
     const double2* tw = pl.d_tw + twoff;
     const int nxb = (int)ceil_div(Mt, RB);
-    RowFwdPass R{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, planes, w.T, L, S};
-    persist_launch<RowFwdPass, SE1P_FFT_MINB_2D>(R, st);
+    // compile-time plans where the shape and the rows per item match (C5: 320 x 4, 576 x 2)
+    const int shape = SE1P_FFT_CT ? fft_plan_shape(f) : kPlanGeneric;
+    auto rows = [&](auto sh, auto nr, bool inv) {
+      constexpr int SH = decltype(sh)::value, NR = decltype(nr)::value;
+      if (!inv) {
+        RowFwdPass<SH, NR> R{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, planes, w.T, L, S};
+        persist_launch<RowFwdPass<SH, NR>, SE1P_FFT_MINB_2D>(R, st);
+      } else {
+        RowInvPass<SH, NR> Q{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, w.T, planes, L, S};
+        persist_launch<RowInvPass<SH, NR>, SE1P_FFT_MINB_2D>(Q, st);
+      }
+    };
+    auto rows_dispatch = [&](bool inv) {
+      if (shape == kPlan320 && RB == 4)
+        rows(std::integral_constant<int, kPlan320>(), std::integral_constant<int, 4>(), inv);
+      else if (shape == kPlan576 && RB == 2)
+        rows(std::integral_constant<int, kPlan576>(), std::integral_constant<int, 2>(), inv);
+      else
+        rows(std::integral_constant<int, kPlanGeneric>(), std::integral_constant<int, 1>(), inv);
+    };
+    rows_dispatch(false);
 #if SE1P_PERSIST & 8
     const int cb = W > 400 ? SE1P_PCOLS_LARGE : SE1P_PCOLS_SMALL;
     auto col = [&](auto cbc) {
@@ -755,8 +796,7 @@ static void mode_class(const KPlan& pl, KWork& w, double2* planes, const SlabLay
       default: colpass_launch<8>(pl, w, nplanes, W, f, tw, base, kernel_class, S, st);
     }
 #endif
-    RowInvPass Q{nxb * nplanes, RB * W, nxb, Mt, W, RB, base, f, tw, w.T, planes, L, S};
-    persist_launch<RowInvPass, SE1P_FFT_MINB_2D>(Q, st);
+    rows_dispatch(true);
     return;
   }
 #endif
