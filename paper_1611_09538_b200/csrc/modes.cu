@@ -320,11 +320,12 @@ static int log2_or_neg(int n) {
 // shared buffer with cp.async (SASS LDGSTS; zero-fill for padding) while item i is transformed in
 // the other two.  Each pass supplies load (async copies into a slot), compute (returns the
 // buffer holding the result; may use both buffers) and store.
-// SE1P_PERSIST bits: 1 z-FFT, 2 inverse z-FFT, 4 row passes, 8 column passes.  Measured at C5
-// (ncu, per launch): rows 87 -> 78 us and inverse z 167 -> 158 us persistent; the column passes
-// lose (their slot budget halves the columns per item: 133 -> 170 us) and the z-FFT is even.
+// SE1P_PERSIST bits: 1 z-FFT, 2 inverse z-FFT, 4 row passes, 8 column passes.  Measured at C5:
+// rows 87 -> 78 us and inverse z 167 -> 158 us persistent (per launch, generic plans); the column
+// passes lose (their slot budget halves the columns per item: 133 -> 170 us); the z-FFT is even
+// with the generic plan and gains with the compile-time one (stage 0.163 -> 0.149 ms).
 #ifndef SE1P_PERSIST
-#define SE1P_PERSIST 6
+#define SE1P_PERSIST 7
 #endif
 __device__ __forceinline__ unsigned sm_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
@@ -654,9 +655,9 @@ static void zinv_launch_sh(const KPlan& pl, KWork& w, const double2* planes, con
 template <int CB>
 static void zfwd_launch(const KPlan& pl, KWork& w, double2* planes, const SlabLayout& L, const int* slot_of,
                         int rows, cudaStream_t st) {
-  // (measured: the compile-time plan makes the forward z-FFT slower, 0.163 -> 0.179 ms at C5,
-  // while the persistent inverse gains, 0.161 -> 0.147 ms)
-  if (SE1P_FFT_CT > 1 && CB == 16 && fft_plan_shape(pl.fz) == kPlan256)
+  // (measured at C5: the compile-time plan in the one-shot forward kernel 0.163 -> 0.179 ms, in the
+  // persistent one 0.149 ms)
+  if (SE1P_FFT_CT && (SE1P_PERSIST & 1) && CB == 16 && fft_plan_shape(pl.fz) == kPlan256)
     zfwd_launch_sh<CB, kPlan256>(pl, w, planes, L, slot_of, rows, st);
   else
     zfwd_launch_sh<CB, kPlanGeneric>(pl, w, planes, L, slot_of, rows, st);
