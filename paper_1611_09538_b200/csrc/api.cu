@@ -541,7 +541,8 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   DevState& ds = dev_state();
   WsOrder ws_order(ds, st);
   KWork& w = ds.w;
-  ensure_particles(w, N, d.nc[0] * d.nc[1] * d.nc[2]);
+  ensure_particles(w, N, real_nbins(d));
+  grow(w.scratch, w.scratch_cap, real_scratch_ints(d, N));
   const bool host_io = o && o->host_io;
   const double *dx = x, *dq = q;
   double* dphi = phi_out;

@@ -6,6 +6,7 @@
 // cells cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell (u mod nc_z)
 // shifted by floor(u/nc_z) L3; a cell whose box lies farther than rc from the target is skipped.
 // Every image within rc is visited exactly once, for any rc.
+#include <cstdio>
 #include <vector>
 
 #include "kspace.cuh"
@@ -15,13 +16,15 @@
 #ifndef SE1P_REAL_TABLE
 #define SE1P_REAL_TABLE 1
 #endif
-// 1: warp per cell with hit masks (k_real_cells); 0: thread per target (k_real_sum).  Measured at
-// C4/C5: 34.8/29.9 ms against 27.1/26.3 ms -- the box-to-box culling of a cell's neighbours scans
-// ~1.5x the candidates of per-target culling and the warp issues more instructions per pair
-// (7.1 against 5.5 per pair within rc; ncu: shared-load latency on the broadcast candidates and
-// the lane-divergent table rows).  Estrin's scheme for the polynomial: +-2 %, not kept.
-#ifndef SE1P_REAL_CELLS
-#define SE1P_REAL_CELLS 0
+// 2: warp per 32 sorted targets, candidates culled against the warp's bounding box and the pairs
+//    within rc evaluated densely after a warp-level compaction (k_real_warp);
+// 1: warp per cell with hit masks (k_real_cells); 0: thread per target (k_real_sum).
+// Measured at C4/C5 (round 2): kernel 0 27.1/26.3 ms, kernel 1 34.8/29.9 ms -- the box-to-box
+// culling of a cell's neighbours scans ~1.5x the candidates of per-target culling and the warp
+// issues more instructions per pair (7.1 against 5.5 per pair within rc; ncu: shared-load latency
+// on the broadcast candidates and the lane-divergent table rows).  Estrin's scheme: +-2 %.
+#ifndef SE1P_REAL_KERNEL
+#define SE1P_REAL_KERNEL 2
 #endif
 
 // Cell width rc/D, D in 1..4 chosen for ~32 particles per cell (measured at C3/C4/C5: D = 3/4/2
@@ -44,6 +47,20 @@ __global__ void k_real_keys(RDev d, const double* __restrict__ x, int64_t N, int
   int cy = min(max((int)floor(x[3 * i + 1] / d.cs[1]), 0), d.nc[1] - 1);
   int cz = min(max((int)floor(pz / d.cs[2]), 0), d.nc[2] - 1);
   keys[i] = (cx * d.nc[1] + cy) * d.nc[2] + cz;
+}
+
+// k_real_warp's keys: column (x cell, y cell), then a fine z bin (~2 particles per bin), so that
+// 32 consecutive sorted targets are a compact box and any z interval of a column is one index range.
+__global__ void k_real_keys_fine(RDev d, const double* __restrict__ x, int64_t N, int* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double pz = x[3 * i + 2];
+  pz -= d.L[2] * floor(pz / d.L[2]);
+  if (pz >= d.L[2]) pz -= d.L[2];
+  const int cx = min(max((int)floor(x[3 * i] / d.cs[0]), 0), d.nc[0] - 1);
+  const int cy = min(max((int)floor(x[3 * i + 1] / d.cs[1]), 0), d.nc[1] - 1);
+  const int fz = min(max((int)floor(pz / d.hz), 0), d.nzf - 1);
+  keys[i] = (cx * d.nc[1] + cy) * d.nzf + fz;
 }
 
 __global__ void k_real_permute(RDev d, const double* __restrict__ x, const double* __restrict__ q,
@@ -291,6 +308,292 @@ static void launch_real_cells(const RDev& d, const double4* P4, const int* perm,
   SE1P_LAUNCH_CHECK();
 }
 
+
+// ---------------------------------------------------------------- k_real_warp (SE1P_REAL_KERNEL 2)
+// Warp per 32 consecutive sorted targets (one per lane; the fine-bin order makes them a compact
+// box).  The warp walks the columns whose xy distance to its bounding box is <= rc; in each, the z
+// interval within rc of the box is one index range per periodic image.  Candidates are loaded 32 at
+// a time (coalesced), culled one per lane against the box, and the survivors staged in a 64-entry
+// shared ring.  A *phase* tests 32 staged candidates against every lane's target (a uniform loop,
+// broadcast reads); each lane writes its hits (r^2, ring slot) to its own column of a pair buffer.
+// A warp prefix sum over the hit counts then lays the phase's T pairs out in lane order and the
+// warp evaluates them 32 at a time -- every lane busy, whatever the hit counts -- writing each
+// pair's q_n erfc(xi r)/r back in place; finally each lane sums its own entries in candidate order
+// (deterministic: the order depends only on the sorted input).
+constexpr int kRWW = 8;                    // warps per block
+struct RWarpSm {
+  double4 cand[64];                        // staged candidates: x, y, z + image shift, q (ring)
+};
+
+// 1/sqrt(r2) for normal r2 > 0: the hardware estimate and two Newton steps (relative error of
+// the estimate < 2^-22, after two steps at the rounding level); no special-case paths.
+__device__ __forceinline__ double rw_rsqrt(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  double e = fma(-r2 * y, y, 1.0);
+  y = fma(0.5 * e, y, y);
+  e = fma(-r2 * y, y, 1.0);
+  return fma(0.5 * e, y, y);
+}
+
+// q_n erfc(xi r)/r (and, FIELD, g = q_n (erfc(xi r)/r - d/dr erfc(xi r))/r^2) of one pair, from
+// k_real_warp's shared table: K intervals of [0, rc], on each the Taylor polynomial of degree
+// 2 NP - 1 about the midpoint, stored as coefficient pairs [NP][K] (double2).  With K = 16 a load
+// of one coefficient pair by the 32 lanes touches at most 16 distinct 16-byte words: two
+// shared-memory wavefronts, where a 300-interval table in L1 costs ~12 per 16-byte load (measured:
+// the L1 data pipe saturated at 97 %).
+template <bool FIELD, int NP>
+__device__ __forceinline__ double rw_pair(const RDev& d, const double2* __restrict__ tab, double r2, double qj,
+                                          double& g) {
+  const double rinv = rw_rsqrt(r2);
+  const double r = r2 * rinv;
+  const int it = min((int)(r * d.tinvw), d.tK - 1);
+  const double u = r - ((double)it + 0.5) * d.tw;
+  const double2* cf = tab + it;
+  double2 c = cf[(NP - 1) * d.tK];
+  double pv = fma(c.y, u, c.x);
+  double dv = 0.0;
+  if (FIELD) dv = fma((double)(2 * NP - 1) * c.y, u, (double)(2 * NP - 2) * c.x);
+#pragma unroll
+  for (int j = NP - 2; j >= 0; --j) {
+    c = cf[j * d.tK];
+    pv = fma(pv, u, c.y);
+    pv = fma(pv, u, c.x);
+    if (FIELD) {
+      dv = fma(dv, u, (double)(2 * j + 1) * c.y);
+      if (j > 0) dv = fma(dv, u, (double)(2 * j) * c.x);
+    }
+  }
+  const double ec = pv * rinv;
+  if (FIELD) g = qj * (ec - dv) * (rinv * rinv);
+  return qj * ec;
+}
+
+template <bool FIELD, int NP>
+__device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bool hit, double rc2, const RDev& d,
+                                        const double2* tab, double& acc, double& ex, double& ey, double& ez) {
+  const double dx = pt.x - cc.x, dy = pt.y - cc.y, dz = pt.z - cc.z;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double g = 0.0;
+  const double v = rw_pair<FIELD, NP>(d, tab, hit ? r2 : rc2, cc.w, g);
+  acc += hit ? v : 0.0;
+  if (FIELD) {
+    const double gg = hit ? g : 0.0;
+    ex = fma(gg, dx, ex);
+    ey = fma(gg, dy, ey);
+    ez = fma(gg, dz, ez);
+  }
+}
+
+// One phase: n staged candidates from ring slot base (base + n <= 64) against the warp's targets,
+// one target per lane, candidates broadcast from shared memory.  First every lane tests its target
+// against the n candidates into a hit mask (independent, cheap); then the warp walks the
+// candidates that any lane has within rc, two at a time (independent chains), every lane
+// evaluating them and keeping its own terms by a select -- a lane-divergent "if within rc" would
+// idle the lanes outside while the others evaluate.  Misses evaluate at r^2 = rc^2 (finite).  The
+// prime in Eq. (3) (n = m in the unshifted image) is the pair at r^2 = 0 exactly: a target meets
+// itself with identical coordinates, and a distinct particle at zero distance would make phi
+// infinite (not a valid input).
+template <bool FIELD, int NP, bool FULL>
+__device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
+                                         double rc2, const RDev& d, const double2* tab, double& acc, double& ex,
+                                         double& ey, double& ez) {
+  constexpr unsigned kAll = 0xffffffffu;
+  const double4* cb = s.cand + base;   // slots base .. base + 31 stay inside the ring
+  unsigned m = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (FULL || k < n) {
+      const double4 cc = cb[k];
+      const double dx = pt.x - cc.x, dy = pt.y - cc.y, dz = pt.z - cc.z;
+      const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+      if (r2 <= rc2 && r2 > 0.0) m |= 1u << k;
+    }
+  }
+  if (!active) m = 0;
+  unsigned am = __reduce_or_sync(kAll, m);
+  while (am) {
+    const int k1 = __ffs(am) - 1;
+    am &= am - 1;
+    const bool two = am != 0;
+    const int k2 = two ? __ffs(am) - 1 : k1;
+    am &= am - 1;
+    const double4 c1 = cb[k1], c2 = cb[k2];
+    rw_eval<FIELD, NP>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
+    rw_eval<FIELD, NP>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
+  }
+}
+
+// groups per column: ceil(n/32) (k_real_warp's target groups)
+__global__ void k_real_group_counts(const int* __restrict__ bin_start, int ncol, int nzf, int* __restrict__ g) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncol) g[c] = (bin_start[(c + 1) * nzf] - bin_start[c * nzf] + 31) / 32;
+}
+
+#ifdef SE1P_REAL_COUNT   // experiment: chunks, survivors, full phases, pairs
+__device__ unsigned long long g_rw_cnt[4];
+__device__ double g_rw_ext[4];
+#endif
+template <bool FIELD, int NP>
+#ifndef SE1P_REAL_MINB
+#define SE1P_REAL_MINB 3
+#endif
+__global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d, const double4* __restrict__ P4,
+                                                         const int* __restrict__ perm,
+                                                         const int* __restrict__ bin_start,
+                                                         const int* __restrict__ gstart, int ncol,
+                                                         double* __restrict__ phi_out,
+                                                         double* __restrict__ field_out) {
+  constexpr unsigned kAll = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char rw_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  RWarpSm& s = reinterpret_cast<RWarpSm*>(rw_raw)[warp];
+  double2* tab = reinterpret_cast<double2*>(rw_raw + kRWW * sizeof(RWarpSm));
+  for (int i = threadIdx.x; i < NP * d.tK; i += blockDim.x) tab[i] = reinterpret_cast<const double2*>(d.tab2)[i];
+  __syncthreads();
+  // target group gw: column col's sorted run cut into G = ceil(n/32) near-equal pieces (groups
+  // never straddle two columns, so the box stays compact); col by a 32-ary search of gstart
+  const int gw = blockIdx.x * kRWW + warp;
+  if (gw >= gstart[ncol]) return;
+  int clo = 0, chi = ncol;   // gstart[clo] <= gw < gstart[chi]
+  while (chi - clo > 1) {
+    const int step = (chi - clo + 31) / 32;
+    const int ci = clo + lane * step;
+    const unsigned le = __ballot_sync(kAll, ci < chi && gstart[ci] <= gw);
+    clo += (31 - __clz(le)) * step;
+    chi = min(chi, clo + step);
+  }
+  const int cbeg = bin_start[clo * d.nzf], nsrc = bin_start[(clo + 1) * d.nzf] - cbeg;
+  const int G = (nsrc + 31) / 32, kg = gw - gstart[clo];
+  const int t0 = cbeg + (int)(((int64_t)kg * nsrc) / G), t1 = cbeg + (int)(((int64_t)(kg + 1) * nsrc) / G);
+  const int tl = t0 + lane;
+  const bool active = tl < t1;
+  const double4 pt = P4[active ? tl : t0];
+  double lo0 = pt.x, lo1 = pt.y, lo2 = pt.z, hi0 = pt.x, hi1 = pt.y, hi2 = pt.z;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo0 = fmin(lo0, __shfl_xor_sync(kAll, lo0, o));
+    lo1 = fmin(lo1, __shfl_xor_sync(kAll, lo1, o));
+    lo2 = fmin(lo2, __shfl_xor_sync(kAll, lo2, o));
+    hi0 = fmax(hi0, __shfl_xor_sync(kAll, hi0, o));
+    hi1 = fmax(hi1, __shfl_xor_sync(kAll, hi1, o));
+    hi2 = fmax(hi2, __shfl_xor_sync(kAll, hi2, o));
+  }
+  const double rc2 = d.rc * d.rc;
+  const double rc2c = rc2 * (1.0 + 1e-12);   // culling bound: never drops a pair within rc
+  const int nc1 = d.nc[1], nzf = d.nzf;
+  double acc = 0.0, ex = 0.0, ey = 0.0, ez = 0.0;
+  int base = 0, ns = 0;                       // staged ring: first slot and count (warp-uniform)
+  const int ax0 = max(0, (int)floor((lo0 - d.rc) / d.cs[0])), ax1 = min(d.nc[0] - 1, (int)floor((hi0 + d.rc) / d.cs[0]));
+  const int ay0 = max(0, (int)floor((lo1 - d.rc) / d.cs[1])), ay1 = min(nc1 - 1, (int)floor((hi1 + d.rc) / d.cs[1]));
+  for (int ax = ax0; ax <= ax1; ++ax) {
+    const double gx = fmax(fmax(ax * d.cs[0] - hi0, lo0 - (ax + 1) * d.cs[0]), 0.0);
+    for (int ay = ay0; ay <= ay1; ++ay) {
+      const double gy = fmax(fmax(ay * d.cs[1] - hi1, lo1 - (ay + 1) * d.cs[1]), 0.0);
+      const double rem = rc2c - gx * gx - gy * gy;
+      if (rem < 0.0) continue;
+      const double rz = sqrt(rem);
+      // fine bins of the z interval [lo2 - rz, hi2 + rz], one bin of margin each side (rounding)
+      const int fl = (int)floor((lo2 - rz) / d.hz) - 1, fh = (int)floor((hi2 + rz) / d.hz) + 1;
+      const int colbase = (ax * nc1 + ay) * nzf;
+      const int w1 = rfloordiv(fh, nzf);
+      for (int w = rfloordiv(fl, nzf); w <= w1; ++w) {
+        const int fa = max(fl - w * nzf, 0), fb = min(fh - w * nzf, nzf - 1);
+        const int js = bin_start[colbase + fa], je = bin_start[colbase + fb + 1];
+        const double shift = w * d.L[2];
+        for (int j0 = js; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          const bool ok = j < je;
+          double4 cc = ok ? P4[j] : make_double4(0.0, 0.0, 0.0, 0.0);
+          cc.z += shift;
+          const double g0 = fmax(fmax(lo0 - cc.x, cc.x - hi0), 0.0);
+          const double g1 = fmax(fmax(lo1 - cc.y, cc.y - hi1), 0.0);
+          const double g2 = fmax(fmax(lo2 - cc.z, cc.z - hi2), 0.0);
+          const bool keep = ok && fma(g0, g0, fma(g1, g1, g2 * g2)) <= rc2c;
+          const unsigned m = __ballot_sync(kAll, keep);
+          if (keep) {
+            const int pos = (base + ns + __popc(m & ((1u << lane) - 1u))) & 63;
+            s.cand[pos] = cc;
+          }
+          ns += __popc(m);
+#ifdef SE1P_REAL_COUNT
+          const unsigned mok = __ballot_sync(kAll, ok);
+          if (lane == 0) { atomicAdd(&g_rw_cnt[0], 1ull); atomicAdd(&g_rw_cnt[1], (unsigned long long)__popc(m));
+                           atomicAdd(&g_rw_ext[3], (double)__popc(mok)); }
+#endif
+          __syncwarp();
+          if (ns >= 32) {
+            rw_phase<FIELD, NP, true>(s, base, 32, pt, active, rc2, d, tab, acc, ex, ey, ez);
+            base = (base + 32) & 63;
+            ns -= 32;
+#ifdef SE1P_REAL_COUNT
+            if (lane == 0) atomicAdd(&g_rw_cnt[2], 1ull);
+#endif
+          }
+        }
+      }
+    }
+  }
+#ifdef SE1P_REAL_COUNT
+  if (lane == 0) {
+    atomicAdd(&g_rw_cnt[3], 1ull);
+    atomicAdd(&g_rw_ext[0], hi0 - lo0);
+    atomicAdd(&g_rw_ext[1], hi1 - lo1);
+    atomicAdd(&g_rw_ext[2], hi2 - lo2);
+  }
+#endif
+  if (ns > 0) rw_phase<FIELD, NP, false>(s, base, ns, pt, active, rc2, d, tab, acc, ex, ey, ez);
+  if (active) {
+    const int64_t uo = perm[tl];
+    if (phi_out) phi_out[uo] = acc - 2.0 * d.xi * pt.w * 0.564189583547756286948079451560772586;  // 1/sqrt(pi)
+    if (FIELD) {
+      field_out[3 * uo] = ex;
+      field_out[3 * uo + 1] = ey;
+      field_out[3 * uo + 2] = ez;
+    }
+  }
+}
+
+template <bool FIELD, int NP>
+static void launch_real_warp_np(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
+                                const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
+  const size_t smem = kRWW * sizeof(RWarpSm) + (size_t)NP * d.tK * sizeof(double2);
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_real_warp<FIELD, NP>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int ncol = d.nc[0] * d.nc[1];
+  const unsigned nb = (unsigned)ceil_div(ceil_div(N, 32) + ncol, kRWW);   // >= the number of groups
+#ifdef SE1P_REAL_COUNT
+  unsigned long long z[4] = {0, 0, 0, 0};
+  SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_cnt, z, sizeof(z)));
+  double ze[4] = {0, 0, 0, 0};
+  SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_ext, ze, sizeof(ze)));
+#endif
+  k_real_warp<FIELD, NP><<<nb, kRWW * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
+  SE1P_LAUNCH_CHECK();
+#ifdef SE1P_REAL_COUNT
+  SE1P_CUDA_TRY(cudaMemcpyFromSymbol(z, g_rw_cnt, sizeof(z)));
+  SE1P_CUDA_TRY(cudaMemcpyFromSymbol(ze, g_rw_ext, sizeof(ze)));
+  fprintf(stderr, "bbox mean %g %g %g loaded %g\n", ze[0] / z[3], ze[1] / z[3], ze[2] / z[3], ze[3] / z[3]);
+  fprintf(stderr, "k_real_warp N=%lld nzf=%d K=%d NP=%d: chunks %llu survivors %llu full phases %llu warps %llu\n",
+          (long long)N, d.nzf, d.tK, NP, z[0], z[1], z[2], z[3]);
+#endif
+}
+
+// coefficient pairs per interval: the compiled sizes (the table's degree is padded up to 2 NP - 1)
+constexpr int kRealNP[] = {6, 7, 8, 10, 12};
+template <bool FIELD>
+static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
+                             const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
+  switch (d.tNP) {
+    case 6: launch_real_warp_np<FIELD, 6>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    case 7: launch_real_warp_np<FIELD, 7>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    case 8: launch_real_warp_np<FIELD, 8>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    case 10: launch_real_warp_np<FIELD, 10>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    case 12: launch_real_warp_np<FIELD, 12>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    default: throw Error{6, "real space: no kernel for this table size"};
+  }
+}
+
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
   RDev d;
   const double rho = (double)std::max<int64_t>(N, 1) / (L[0] * L[1] * L[2]);
@@ -306,7 +609,25 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
   d.Ky = (int)std::ceil(rc / d.cs[1]);
   d.xi = xi;
   d.rc = rc;
+  // ~2 particles per fine z bin, at most 2^22 bins in all
+  const int64_t ncol = (int64_t)d.nc[0] * d.nc[1];
+  const int64_t nz = std::max<int64_t>(1, (N + 2 * ncol - 1) / (2 * ncol));
+  d.nzf = (int)std::min<int64_t>(nz, std::max<int64_t>(1, ((int64_t)1 << 22) / ncol));
+  d.hz = L[2] / d.nzf;
   return d;
+}
+
+int64_t real_scratch_ints(const RDev& d, int64_t N) {
+  const int64_t ncol = (int64_t)d.nc[0] * d.nc[1];
+  return std::max<int64_t>(sort_scratch_ints(N, real_nbins(d)), 2 * ncol + 1 + scan_scratch_ints(ncol));
+}
+
+int real_nbins(const RDev& d) {
+#if SE1P_REAL_KERNEL == 2
+  return d.nc[0] * d.nc[1] * d.nzf;
+#else
+  return d.nc[0] * d.nc[1] * d.nc[2];
+#endif
 }
 
 // Taylor coefficients of erfc(xi r) about the interval midpoints r_i = (i + 1/2) dr:
@@ -336,17 +657,86 @@ static std::vector<double> erfc_table(double xi, double rc, int ntab) {
   return t;
 }
 
+// k_real_warp's few-interval table.  Each interval's Taylor series of erfc(xi r) about its
+// midpoint (the Hermite recurrence above, long double) is cut at the first degree n whose next
+// two terms at the interval's edge are below 2e-16 of erfc there (the same relative target as the
+// 300-interval table); K = 16 intervals unless that needs a degree above 23, then 32, 64, ...
+// The degree is padded up to a compiled size 2 NP - 1 (kRealNP).
+struct SmallTab {
+  int K = 0, NP = 0;
+  std::vector<double> pairs;   // [NP][K][2]
+};
+static SmallTab erfc_small_table(double xi, double rc) {
+  const long double two_over_sqrtpi = 1.128379167095512573896158903121545172L;
+  constexpr int kMaxN = 48;
+  for (int K = 16;; K *= 2) {
+    const long double w = (long double)rc / K, hw = 0.5L * w;
+    std::vector<long double> c((size_t)K * (kMaxN + 1));
+    int need = 0;
+    for (int i = 0; i < K; ++i) {
+      const long double x0 = (long double)xi * ((long double)i + 0.5L) * w;
+      const long double g = two_over_sqrtpi * expl(-x0 * x0);
+      long double* ci = &c[(size_t)i * (kMaxN + 1)];
+      ci[0] = erfcl(x0);
+      long double hm1 = 0.0L, h = 1.0L, xin = 1.0L, fact = 1.0L;
+      for (int n = 1; n <= kMaxN; ++n) {
+        xin *= (long double)xi;
+        fact *= (long double)n;
+        ci[n] = ((n & 1) ? -1.0L : 1.0L) * g * h * xin / fact;
+        const long double hn = 2.0L * x0 * h - 2.0L * (long double)(n - 1) * hm1;
+        hm1 = h;
+        h = hn;
+      }
+      const long double edge = erfcl((long double)xi * ((long double)i + 1.0L) * w);
+      int n = 1;
+      while (n + 2 <= kMaxN &&
+             fabsl(ci[n + 1]) * powl(hw, n + 1) + fabsl(ci[n + 2]) * powl(hw, n + 2) >= 2e-16L * edge)
+        ++n;
+      need = std::max(need, n);
+    }
+    int NP = 0;
+    for (int np : kRealNP)
+      if (2 * np - 1 >= need) {
+        NP = np;
+        break;
+      }
+    if (NP == 0 && K < 4096) continue;
+    if (NP == 0) throw Error{4, "real space: xi*rc too large for the erfc table"};
+    SmallTab t;
+    t.K = K;
+    t.NP = NP;
+    t.pairs.assign((size_t)NP * K * 2, 0.0);
+    for (int j = 0; j < NP; ++j)
+      for (int i = 0; i < K; ++i)
+        for (int e = 0; e < 2; ++e) {
+          const int n = 2 * j + e;
+          t.pairs[((size_t)j * K + i) * 2 + e] = n <= need ? (double)c[(size_t)i * (kMaxN + 1) + n] : 0.0;
+        }
+    return t;
+  }
+}
+
 struct TabCache {
   double xi = 0, rc = 0;
   double* dev = nullptr;
   int64_t cap = 0;
 };
 static TabCache g_tab[64];
+struct SmallTabCache {
+  double xi = 0, rc = 0;
+  double* dev = nullptr;
+  int64_t cap = 0;
+  int K = 0, NP = 0;
+};
+static SmallTabCache g_tab2[64];
 
 void real_release_tables(int dev) {
   TabCache& tc = g_tab[dev & 63];
   if (tc.dev) dev_free(tc.dev);
   tc = TabCache{};
+  SmallTabCache& t2 = g_tab2[dev & 63];
+  if (t2.dev) dev_free(t2.dev);
+  t2 = SmallTabCache{};
 }
 
 void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
@@ -379,18 +769,65 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     d.inv_dr = ntab / d.rc;
   }
 #endif
-  const int ncell = d.nc[0] * d.nc[1] * d.nc[2];
+#if SE1P_REAL_KERNEL == 2
+  {
+    int dev = 0;
+    SE1P_CUDA_TRY(cudaGetDevice(&dev));
+    SmallTabCache& tc = g_tab2[dev & 63];
+    if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
+      const SmallTab t = erfc_small_table(d.xi, d.rc);
+      if (tc.dev && tc.cap < (int64_t)t.pairs.size()) {
+        dev_free(tc.dev);
+        tc.dev = nullptr;
+      }
+      if (!tc.dev) {
+        dev_alloc(tc.dev, t.pairs.size());
+        tc.cap = (int64_t)t.pairs.size();
+      }
+      SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.pairs.data(), sizeof(double) * t.pairs.size(), cudaMemcpyHostToDevice, st));
+      SE1P_CUDA_TRY(cudaStreamSynchronize(st));
+      tc.xi = d.xi;
+      tc.rc = d.rc;
+      tc.K = t.K;
+      tc.NP = t.NP;
+    }
+    d.tab2 = tc.dev;
+    d.tK = tc.K;
+    d.tNP = tc.NP;
+    d.tw = d.rc / tc.K;
+    d.tinvw = tc.K / d.rc;
+  }
+#endif
+  const int nbins = real_nbins(d);
   const unsigned nb = (unsigned)ceil_div(N, 256);
+#if SE1P_REAL_KERNEL == 2
+  k_real_keys_fine<<<nb, 256, 0, st>>>(d, x, N, w.keys);
+#else
   k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
+#endif
   SE1P_LAUNCH_CHECK();
-  stable_bin_sort(w.keys, N, ncell, w.perm, w.bin_start, w.scratch, st);
+  stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.scratch, st);
   k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
   SE1P_LAUNCH_CHECK();
-#if SE1P_REAL_CELLS && SE1P_REAL_TABLE
+#if SE1P_REAL_KERNEL == 2 && SE1P_REAL_TABLE
+  {
+    const int ncol = d.nc[0] * d.nc[1];
+    int* gcnt = w.scratch;   // the sort's scratch is free again (real_scratch_ints sizes it)
+    int* gstart = gcnt + ncol;
+    k_real_group_counts<<<(unsigned)ceil_div(ncol, 256), 256, 0, st>>>(w.bin_start, ncol, d.nzf, gcnt);
+    SE1P_LAUNCH_CHECK();
+    exclusive_scan_ints(gcnt, ncol, gstart, gstart + ncol + 1, st);
+    if (field_out)
+      launch_real_warp<true>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, field_out, st);
+    else
+      launch_real_warp<false>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, nullptr, st);
+  }
+  return;
+#elif SE1P_REAL_KERNEL == 1 && SE1P_REAL_TABLE
   if (field_out)
-    launch_real_cells<true>(d, (const double4*)w.xs, w.perm, w.bin_start, ncell, phi_out, field_out, st);
+    launch_real_cells<true>(d, (const double4*)w.xs, w.perm, w.bin_start, nbins, phi_out, field_out, st);
   else
-    launch_real_cells<false>(d, (const double4*)w.xs, w.perm, w.bin_start, ncell, phi_out, nullptr, st);
+    launch_real_cells<false>(d, (const double4*)w.xs, w.perm, w.bin_start, nbins, phi_out, nullptr, st);
   return;
 #endif
   const unsigned nt = (unsigned)ceil_div(N, 128);

@@ -14,10 +14,18 @@ struct RDev {
   int K;          // periodic-axis cell reach
   int Kx, Ky;     // free-axis cell reach (cells are >= rc/D wide)
   double xi, rc;
+  // k_real_warp's sort bins: columns (x cell, y cell) of nzf fine z bins hz = L3/nzf wide
+  int nzf = 1;
+  double hz = 0.0;
   // erfc(xi r) on [0, rc] as ntab local Taylor polynomials of degree kTabDeg in r - r_mid
   const double* tab = nullptr;
   int ntab = 0;
   double inv_dr = 0.0, dr = 0.0;
+  // k_real_warp's table: tK intervals of [0, rc] (width tw), Taylor polynomials of degree 2 tNP - 1
+  // about the midpoints, coefficient pairs [tNP][tK] (double2)
+  const double* tab2 = nullptr;
+  int tK = 0, tNP = 0;
+  double tw = 0.0, tinvw = 0.0;
 };
 // degree 7 (8 coefficients, four 16-byte loads per pair); the interval count grows with
 // X = xi rc so that the remainder (2 X dx)^8/8! (dx the interval half-width in xi r) stays
@@ -29,6 +37,8 @@ inline int real_table_intervals(double xi, double rc) {
 }
 
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
+int real_nbins(const RDev& d);   // bins of the real-space sort (workspace sizing)
+int64_t real_scratch_ints(const RDev& d, int64_t N);   // ints of KWork::scratch the real-space sum needs
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out = nullptr);
 void real_release_tables(int dev);   // the cached erfc table of device dev
