@@ -342,21 +342,37 @@ __device__ __forceinline__ double rw_rsqrt(double r2) {
 // of one coefficient pair by the 32 lanes touches at most 16 distinct 16-byte words: two
 // shared-memory wavefronts, where a 300-interval table in L1 costs ~12 per 16-byte load (measured:
 // the L1 data pipe saturated at 97 %).
+#ifndef SE1P_REAL_TABLAYOUT
+#define SE1P_REAL_TABLAYOUT 1   // 1: coefficients [2 NP][K] read as 8-byte words; 0: pairs [NP][K] as 16-byte words
+#endif
+constexpr int kRealK = 16;      // intervals of the shared table
 template <bool FIELD, int NP>
-__device__ __forceinline__ double rw_pair(const RDev& d, const double2* __restrict__ tab, double r2, double qj,
+__device__ __forceinline__ double rw_pair(const RDev& d, const double* __restrict__ tab, double r2, double qj,
                                           double& g) {
   const double rinv = rw_rsqrt(r2);
   const double r = r2 * rinv;
-  const int it = min((int)(r * d.tinvw), d.tK - 1);
+  const int it = min((int)(r * d.tinvw), kRealK - 1);
   const double u = r - ((double)it + 0.5) * d.tw;
-  const double2* cf = tab + it;
-  double2 c = cf[(NP - 1) * d.tK];
+#if SE1P_REAL_TABLAYOUT
+  const double* cf = tab + it;
+  double pv = cf[(2 * NP - 1) * kRealK];
+  double dv = 0.0;
+  if (FIELD) dv = (double)(2 * NP - 1) * pv;
+#pragma unroll
+  for (int n = 2 * NP - 2; n >= 0; --n) {
+    const double c = cf[n * kRealK];
+    pv = fma(pv, u, c);
+    if (FIELD && n > 0) dv = fma(dv, u, (double)n * c);
+  }
+#else
+  const double2* cf = reinterpret_cast<const double2*>(tab) + it;
+  double2 c = cf[(NP - 1) * kRealK];
   double pv = fma(c.y, u, c.x);
   double dv = 0.0;
   if (FIELD) dv = fma((double)(2 * NP - 1) * c.y, u, (double)(2 * NP - 2) * c.x);
 #pragma unroll
   for (int j = NP - 2; j >= 0; --j) {
-    c = cf[j * d.tK];
+    c = cf[j * kRealK];
     pv = fma(pv, u, c.y);
     pv = fma(pv, u, c.x);
     if (FIELD) {
@@ -364,6 +380,7 @@ __device__ __forceinline__ double rw_pair(const RDev& d, const double2* __restri
       if (j > 0) dv = fma(dv, u, (double)(2 * j) * c.x);
     }
   }
+#endif
   const double ec = pv * rinv;
   if (FIELD) g = qj * (ec - dv) * (rinv * rinv);
   return qj * ec;
@@ -371,7 +388,7 @@ __device__ __forceinline__ double rw_pair(const RDev& d, const double2* __restri
 
 template <bool FIELD, int NP>
 __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bool hit, double rc2, const RDev& d,
-                                        const double2* tab, double& acc, double& ex, double& ey, double& ez) {
+                                        const double* tab, double& acc, double& ex, double& ey, double& ez) {
   const double dx = pt.x - cc.x, dy = pt.y - cc.y, dz = pt.z - cc.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double g = 0.0;
@@ -396,7 +413,7 @@ __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bo
 // infinite (not a valid input).
 template <bool FIELD, int NP, bool FULL>
 __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
-                                         double rc2, const RDev& d, const double2* tab, double& acc, double& ex,
+                                         double rc2, const RDev& d, const double* tab, double& acc, double& ex,
                                          double& ey, double& ez) {
   constexpr unsigned kAll = 0xffffffffu;
   const double4* cb = s.cand + base;   // slots base .. base + 31 stay inside the ring
@@ -448,8 +465,8 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
   extern __shared__ __align__(16) unsigned char rw_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RWarpSm& s = reinterpret_cast<RWarpSm*>(rw_raw)[warp];
-  double2* tab = reinterpret_cast<double2*>(rw_raw + kRWW * sizeof(RWarpSm));
-  for (int i = threadIdx.x; i < NP * d.tK; i += blockDim.x) tab[i] = reinterpret_cast<const double2*>(d.tab2)[i];
+  double* tab = reinterpret_cast<double*>(rw_raw + kRWW * sizeof(RWarpSm));
+  for (int i = threadIdx.x; i < 2 * NP * kRealK; i += blockDim.x) tab[i] = d.tab2[i];
   __syncthreads();
   // target group gw: column col's sorted run cut into G = ceil(n/32) near-equal pieces (groups
   // never straddle two columns, so the box stays compact); col by a 32-ary search of gstart
@@ -557,7 +574,7 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
 template <bool FIELD, int NP>
 static void launch_real_warp_np(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                                 const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
-  const size_t smem = kRWW * sizeof(RWarpSm) + (size_t)NP * d.tK * sizeof(double2);
+  const size_t smem = kRWW * sizeof(RWarpSm) + (size_t)NP * kRealK * sizeof(double2);
   SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_real_warp<FIELD, NP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int ncol = d.nc[0] * d.nc[1];
@@ -580,7 +597,7 @@ static void launch_real_warp_np(const RDev& d, const double4* P4, const int* per
 }
 
 // coefficient pairs per interval: the compiled sizes (the table's degree is padded up to 2 NP - 1)
-constexpr int kRealNP[] = {6, 7, 8, 10, 12};
+constexpr int kRealNP[] = {6, 7, 8, 10, 12, 16};
 template <bool FIELD>
 static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                              const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
@@ -590,6 +607,7 @@ static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, 
     case 8: launch_real_warp_np<FIELD, 8>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     case 10: launch_real_warp_np<FIELD, 10>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     case 12: launch_real_warp_np<FIELD, 12>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+    case 16: launch_real_warp_np<FIELD, 16>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     default: throw Error{6, "real space: no kernel for this table size"};
   }
 }
@@ -614,6 +632,9 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
   const int64_t nz = std::max<int64_t>(1, (N + 2 * ncol - 1) / (2 * ncol));
   d.nzf = (int)std::min<int64_t>(nz, std::max<int64_t>(1, ((int64_t)1 << 22) / ncol));
   d.hz = L[2] / d.nzf;
+#if SE1P_REAL_KERNEL == 2 && SE1P_REAL_TABLE
+  d.tNP = real_table_np(xi, rc);   // 0: xi rc beyond the shared table, thread-per-target kernel
+#endif
   return d;
 }
 
@@ -623,11 +644,7 @@ int64_t real_scratch_ints(const RDev& d, int64_t N) {
 }
 
 int real_nbins(const RDev& d) {
-#if SE1P_REAL_KERNEL == 2
-  return d.nc[0] * d.nc[1] * d.nzf;
-#else
-  return d.nc[0] * d.nc[1] * d.nc[2];
-#endif
+  return d.tNP > 0 ? d.nc[0] * d.nc[1] * d.nzf : d.nc[0] * d.nc[1] * d.nc[2];
 }
 
 // Taylor coefficients of erfc(xi r) about the interval midpoints r_i = (i + 1/2) dr:
@@ -657,63 +674,66 @@ static std::vector<double> erfc_table(double xi, double rc, int ntab) {
   return t;
 }
 
-// k_real_warp's few-interval table.  Each interval's Taylor series of erfc(xi r) about its
-// midpoint (the Hermite recurrence above, long double) is cut at the first degree n whose next
-// two terms at the interval's edge are below 2e-16 of erfc there (the same relative target as the
-// 300-interval table); K = 16 intervals unless that needs a degree above 23, then 32, 64, ...
-// The degree is padded up to a compiled size 2 NP - 1 (kRealNP).
-struct SmallTab {
-  int K = 0, NP = 0;
-  std::vector<double> pairs;   // [NP][K][2]
-};
-static SmallTab erfc_small_table(double xi, double rc) {
+// k_real_warp's few-interval table: kRealK = 16 intervals of [0, rc].  Each interval's Taylor
+// series of erfc(xi r) about its midpoint (the Hermite recurrence above, long double) is cut at
+// the first degree n whose next two terms at the interval's edge are below 2e-16 of erfc there
+// (the same relative target as the 300-interval table), the worst interval deciding; the degree
+// is padded up to a compiled size 2 NP - 1 (kRealNP).  xi rc = 3 (C5) takes degree 13, 4.9
+// (C1-C4, C5 at rc = 0.164) degree 19; beyond degree 31 (xi rc > ~7.5, erfc(xi rc) < 1e-25)
+// real_space falls back to the thread-per-target kernel and its 300+-interval table.
+static std::vector<long double> erfc_taylor16(double xi, double rc, int& need) {
   const long double two_over_sqrtpi = 1.128379167095512573896158903121545172L;
   constexpr int kMaxN = 48;
-  for (int K = 16;; K *= 2) {
-    const long double w = (long double)rc / K, hw = 0.5L * w;
-    std::vector<long double> c((size_t)K * (kMaxN + 1));
-    int need = 0;
-    for (int i = 0; i < K; ++i) {
-      const long double x0 = (long double)xi * ((long double)i + 0.5L) * w;
-      const long double g = two_over_sqrtpi * expl(-x0 * x0);
-      long double* ci = &c[(size_t)i * (kMaxN + 1)];
-      ci[0] = erfcl(x0);
-      long double hm1 = 0.0L, h = 1.0L, xin = 1.0L, fact = 1.0L;
-      for (int n = 1; n <= kMaxN; ++n) {
-        xin *= (long double)xi;
-        fact *= (long double)n;
-        ci[n] = ((n & 1) ? -1.0L : 1.0L) * g * h * xin / fact;
-        const long double hn = 2.0L * x0 * h - 2.0L * (long double)(n - 1) * hm1;
-        hm1 = h;
-        h = hn;
-      }
-      const long double edge = erfcl((long double)xi * ((long double)i + 1.0L) * w);
-      int n = 1;
-      while (n + 2 <= kMaxN &&
-             fabsl(ci[n + 1]) * powl(hw, n + 1) + fabsl(ci[n + 2]) * powl(hw, n + 2) >= 2e-16L * edge)
-        ++n;
-      need = std::max(need, n);
+  const int K = kRealK;
+  const long double w = (long double)rc / K, hw = 0.5L * w;
+  std::vector<long double> c((size_t)K * (kMaxN + 1));
+  need = 0;
+  for (int i = 0; i < K; ++i) {
+    const long double x0 = (long double)xi * ((long double)i + 0.5L) * w;
+    const long double g = two_over_sqrtpi * expl(-x0 * x0);
+    long double* ci = &c[(size_t)i * (kMaxN + 1)];
+    ci[0] = erfcl(x0);
+    long double hm1 = 0.0L, h = 1.0L, xin = 1.0L, fact = 1.0L;
+    for (int n = 1; n <= kMaxN; ++n) {   // coefficient of u^n: (-1)^n (2/sqrt(pi)) H_{n-1}(x0) e^{-x0^2} xi^n / n!
+      xin *= (long double)xi;
+      fact *= (long double)n;
+      ci[n] = ((n & 1) ? -1.0L : 1.0L) * g * h * xin / fact;
+      const long double hn = 2.0L * x0 * h - 2.0L * (long double)(n - 1) * hm1;
+      hm1 = h;
+      h = hn;
     }
-    int NP = 0;
-    for (int np : kRealNP)
-      if (2 * np - 1 >= need) {
-        NP = np;
-        break;
-      }
-    if (NP == 0 && K < 4096) continue;
-    if (NP == 0) throw Error{4, "real space: xi*rc too large for the erfc table"};
-    SmallTab t;
-    t.K = K;
-    t.NP = NP;
-    t.pairs.assign((size_t)NP * K * 2, 0.0);
-    for (int j = 0; j < NP; ++j)
-      for (int i = 0; i < K; ++i)
-        for (int e = 0; e < 2; ++e) {
-          const int n = 2 * j + e;
-          t.pairs[((size_t)j * K + i) * 2 + e] = n <= need ? (double)c[(size_t)i * (kMaxN + 1) + n] : 0.0;
-        }
-    return t;
+    const long double edge = erfcl((long double)xi * ((long double)i + 1.0L) * w);
+    int n = 1;
+    while (n + 2 <= kMaxN && fabsl(ci[n + 1]) * powl(hw, n + 1) + fabsl(ci[n + 2]) * powl(hw, n + 2) >= 2e-16L * edge)
+      ++n;
+    need = std::max(need, n);
   }
+  return c;
+}
+
+int real_table_np(double xi, double rc) {
+  int need = 0;
+  erfc_taylor16(xi, rc, need);
+  for (int np : kRealNP)
+    if (2 * np - 1 >= need) return np;
+  return 0;
+}
+
+static std::vector<double> erfc_small_table(double xi, double rc, int NP) {
+  int need = 0;
+  const std::vector<long double> c = erfc_taylor16(xi, rc, need);
+  const int K = kRealK;
+  std::vector<double> t((size_t)2 * NP * K, 0.0);
+  for (int n = 0; n < 2 * NP; ++n)
+    for (int i = 0; i < K; ++i) {
+      const double v = n <= need ? (double)c[(size_t)i * 49 + n] : 0.0;
+#if SE1P_REAL_TABLAYOUT
+      t[(size_t)n * K + i] = v;
+#else
+      t[((size_t)(n / 2) * K + i) * 2 + (n & 1)] = v;
+#endif
+    }
+  return t;
 }
 
 struct TabCache {
@@ -726,7 +746,6 @@ struct SmallTabCache {
   double xi = 0, rc = 0;
   double* dev = nullptr;
   int64_t cap = 0;
-  int K = 0, NP = 0;
 };
 static SmallTabCache g_tab2[64];
 
@@ -743,7 +762,7 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
                 cudaStream_t st, double* field_out) {
   RDev d = d0;
 #if SE1P_REAL_TABLE
-  {
+  if (d.tNP == 0) {
     int dev = 0;
     SE1P_CUDA_TRY(cudaGetDevice(&dev));
     TabCache& tc = g_tab[dev & 63];
@@ -769,48 +788,40 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     d.inv_dr = ntab / d.rc;
   }
 #endif
-#if SE1P_REAL_KERNEL == 2
-  {
+  if (d.tNP > 0) {   // k_real_warp's shared table
     int dev = 0;
     SE1P_CUDA_TRY(cudaGetDevice(&dev));
     SmallTabCache& tc = g_tab2[dev & 63];
     if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
-      const SmallTab t = erfc_small_table(d.xi, d.rc);
-      if (tc.dev && tc.cap < (int64_t)t.pairs.size()) {
+      const std::vector<double> t = erfc_small_table(d.xi, d.rc, d.tNP);
+      if (tc.dev && tc.cap < (int64_t)t.size()) {
         dev_free(tc.dev);
         tc.dev = nullptr;
       }
       if (!tc.dev) {
-        dev_alloc(tc.dev, t.pairs.size());
-        tc.cap = (int64_t)t.pairs.size();
+        dev_alloc(tc.dev, t.size());
+        tc.cap = (int64_t)t.size();
       }
-      SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.pairs.data(), sizeof(double) * t.pairs.size(), cudaMemcpyHostToDevice, st));
+      SE1P_CUDA_TRY(cudaMemcpyAsync(tc.dev, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
       SE1P_CUDA_TRY(cudaStreamSynchronize(st));
       tc.xi = d.xi;
       tc.rc = d.rc;
-      tc.K = t.K;
-      tc.NP = t.NP;
     }
     d.tab2 = tc.dev;
-    d.tK = tc.K;
-    d.tNP = tc.NP;
-    d.tw = d.rc / tc.K;
-    d.tinvw = tc.K / d.rc;
+    d.tw = d.rc / kRealK;
+    d.tinvw = kRealK / d.rc;
   }
-#endif
   const int nbins = real_nbins(d);
   const unsigned nb = (unsigned)ceil_div(N, 256);
-#if SE1P_REAL_KERNEL == 2
-  k_real_keys_fine<<<nb, 256, 0, st>>>(d, x, N, w.keys);
-#else
-  k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
-#endif
+  if (d.tNP > 0)
+    k_real_keys_fine<<<nb, 256, 0, st>>>(d, x, N, w.keys);
+  else
+    k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
   SE1P_LAUNCH_CHECK();
   stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.scratch, st);
   k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
   SE1P_LAUNCH_CHECK();
-#if SE1P_REAL_KERNEL == 2 && SE1P_REAL_TABLE
-  {
+  if (d.tNP > 0) {
     const int ncol = d.nc[0] * d.nc[1];
     int* gcnt = w.scratch;   // the sort's scratch is free again (real_scratch_ints sizes it)
     int* gstart = gcnt + ncol;
@@ -821,9 +832,9 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
       launch_real_warp<true>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, field_out, st);
     else
       launch_real_warp<false>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, nullptr, st);
+    return;
   }
-  return;
-#elif SE1P_REAL_KERNEL == 1 && SE1P_REAL_TABLE
+#if SE1P_REAL_KERNEL == 1 && SE1P_REAL_TABLE
   if (field_out)
     launch_real_cells<true>(d, (const double4*)w.xs, w.perm, w.bin_start, nbins, phi_out, field_out, st);
   else

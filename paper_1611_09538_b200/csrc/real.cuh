@@ -38,7 +38,8 @@ inline int real_table_intervals(double xi, double rc) {
 
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 int real_nbins(const RDev& d);   // bins of the real-space sort (workspace sizing)
-int64_t real_scratch_ints(const RDev& d, int64_t N);   // ints of KWork::scratch the real-space sum needs
+int64_t real_scratch_ints(const RDev& d, int64_t N);
+int real_table_np(double xi, double rc);   // k_real_warp's coefficient pairs per interval, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out = nullptr);
 void real_release_tables(int dev);   // the cached erfc table of device dev

@@ -30,7 +30,7 @@ torch.cuda.synchronize()
 print("ok")
 PY
 python /tmp/real1.py > /dev/null 2>&1 &&
-ncu --set full --clock-control none -k regex:k_real_sum -c 1 -f -o /tmp/ev/real python /tmp/real1.py > /tmp/ev/ncu3.log 2>&1
+ncu --set full --clock-control none -k regex:"k_real_warp|k_real_sum" -c 1 -f -o /tmp/ev/real python /tmp/real1.py > /tmp/ev/ncu3.log 2>&1
 tail -1 /tmp/ev/ncu3.log
 PROFILES_DIR=gpurun_out/${T}_profiles python tools/summarize_profiles.py /tmp/ev/launches.csv /tmp/ev/all.ncu-rep ${T} /tmp/ev/real.ncu-rep > gpurun_out/${T}_summary.log 2>&1
 cp /tmp/ev/launches.csv gpurun_out/${T}_profiles/${T}_launches_C5.csv
