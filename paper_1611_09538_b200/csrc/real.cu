@@ -345,7 +345,10 @@ __device__ __forceinline__ double rw_rsqrt(double r2) {
 #ifndef SE1P_REAL_TABLAYOUT
 #define SE1P_REAL_TABLAYOUT 1   // 1: coefficients [2 NP][K] read as 8-byte words; 0: pairs [NP][K] as 16-byte words
 #endif
-constexpr int kRealK = 16;      // intervals of the shared table
+#ifndef SE1P_REAL_K
+#define SE1P_REAL_K 32
+#endif
+constexpr int kRealK = SE1P_REAL_K;   // intervals of the shared table
 template <bool FIELD, int NP>
 __device__ __forceinline__ double rw_pair(const RDev& d, const double* __restrict__ tab, double r2, double qj,
                                           double& g) {
@@ -681,7 +684,7 @@ static std::vector<double> erfc_table(double xi, double rc, int ntab) {
 // is padded up to a compiled size 2 NP - 1 (kRealNP).  xi rc = 3 (C5) takes degree 13, 4.9
 // (C1-C4, C5 at rc = 0.164) degree 19; beyond degree 31 (xi rc > ~7.5, erfc(xi rc) < 1e-25)
 // real_space falls back to the thread-per-target kernel and its 300+-interval table.
-static std::vector<long double> erfc_taylor16(double xi, double rc, int& need) {
+static std::vector<long double> erfc_taylor_k(double xi, double rc, int& need) {
   const long double two_over_sqrtpi = 1.128379167095512573896158903121545172L;
   constexpr int kMaxN = 48;
   const int K = kRealK;
@@ -713,7 +716,7 @@ static std::vector<long double> erfc_taylor16(double xi, double rc, int& need) {
 
 int real_table_np(double xi, double rc) {
   int need = 0;
-  erfc_taylor16(xi, rc, need);
+  erfc_taylor_k(xi, rc, need);
   for (int np : kRealNP)
     if (2 * np - 1 >= need) return np;
   return 0;
@@ -721,7 +724,7 @@ int real_table_np(double xi, double rc) {
 
 static std::vector<double> erfc_small_table(double xi, double rc, int NP) {
   int need = 0;
-  const std::vector<long double> c = erfc_taylor16(xi, rc, need);
+  const std::vector<long double> c = erfc_taylor_k(xi, rc, need);
   const int K = kRealK;
   std::vector<double> t((size_t)2 * NP * K, 0.0);
   for (int n = 0; n < 2 * NP; ++n)
