@@ -6,7 +6,9 @@
 // cells cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell (u mod nc_z)
 // shifted by floor(u/nc_z) L3; a cell whose box lies farther than rc from the target is skipped.
 // Every image within rc is visited exactly once, for any rc.
+#include <array>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "kspace.cuh"
@@ -320,7 +322,7 @@ static void launch_real_cells(const RDev& d, const double4* P4, const int* perm,
 // warp evaluates them 32 at a time -- every lane busy, whatever the hit counts -- writing each
 // pair's q_n erfc(xi r)/r back in place; finally each lane sums its own entries in candidate order
 // (deterministic: the order depends only on the sorted input).
-constexpr int kRWW = 8;                    // warps per block
+constexpr int kRWW = 8;                    // warps per block (at most; fewer for small systems)
 struct RWarpSm {
   double4 cand[64];                        // staged candidates: x, y, z + image shift, q (ring)
 };
@@ -468,12 +470,13 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
   extern __shared__ __align__(16) unsigned char rw_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RWarpSm& s = reinterpret_cast<RWarpSm*>(rw_raw)[warp];
-  double* tab = reinterpret_cast<double*>(rw_raw + kRWW * sizeof(RWarpSm));
+  const int nw = blockDim.x >> 5;
+  double* tab = reinterpret_cast<double*>(rw_raw + nw * sizeof(RWarpSm));
   for (int i = threadIdx.x; i < 2 * NP * kRealK; i += blockDim.x) tab[i] = d.tab2[i];
   __syncthreads();
   // target group gw: column col's sorted run cut into G = ceil(n/32) near-equal pieces (groups
   // never straddle two columns, so the box stays compact); col by a 32-ary search of gstart
-  const int gw = blockIdx.x * kRWW + warp;
+  const int gw = blockIdx.x * nw + warp;
   if (gw >= gstart[ncol]) return;
   int clo = 0, chi = ncol;   // gstart[clo] <= gw < gstart[chi]
   while (chi - clo > 1) {
@@ -577,18 +580,22 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
 template <bool FIELD, int NP>
 static void launch_real_warp_np(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                                 const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
-  const size_t smem = kRWW * sizeof(RWarpSm) + (size_t)NP * kRealK * sizeof(double2);
+  // warps per block: 8, halved while that leaves fewer than two blocks per SM (small systems)
+  const int ncol = d.nc[0] * d.nc[1];
+  const int64_t groups = ceil_div(N, 32) + ncol;   // >= the number of groups
+  int nw = kRWW;
+  while (nw > 1 && ceil_div(groups, nw) < 2 * 148) nw /= 2;
+  const size_t smem = nw * sizeof(RWarpSm) + (size_t)NP * kRealK * sizeof(double2);
   SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_real_warp<FIELD, NP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int ncol = d.nc[0] * d.nc[1];
-  const unsigned nb = (unsigned)ceil_div(ceil_div(N, 32) + ncol, kRWW);   // >= the number of groups
+  const unsigned nb = (unsigned)ceil_div(groups, nw);
 #ifdef SE1P_REAL_COUNT
   unsigned long long z[4] = {0, 0, 0, 0};
   SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_cnt, z, sizeof(z)));
   double ze[4] = {0, 0, 0, 0};
   SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_ext, ze, sizeof(ze)));
 #endif
-  k_real_warp<FIELD, NP><<<nb, kRWW * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
+  k_real_warp<FIELD, NP><<<nb, nw * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
   SE1P_LAUNCH_CHECK();
 #ifdef SE1P_REAL_COUNT
   SE1P_CUDA_TRY(cudaMemcpyFromSymbol(z, g_rw_cnt, sizeof(z)));
@@ -600,11 +607,12 @@ static void launch_real_warp_np(const RDev& d, const double4* P4, const int* per
 }
 
 // coefficient pairs per interval: the compiled sizes (the table's degree is padded up to 2 NP - 1)
-constexpr int kRealNP[] = {6, 7, 8, 10, 12, 16};
+constexpr int kRealNP[] = {5, 6, 7, 8, 10, 12, 16};
 template <bool FIELD>
 static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                              const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
   switch (d.tNP) {
+    case 5: launch_real_warp_np<FIELD, 5>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     case 6: launch_real_warp_np<FIELD, 6>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     case 7: launch_real_warp_np<FIELD, 7>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
     case 8: launch_real_warp_np<FIELD, 8>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
@@ -677,59 +685,91 @@ static std::vector<double> erfc_table(double xi, double rc, int ntab) {
   return t;
 }
 
-// k_real_warp's few-interval table: kRealK = 16 intervals of [0, rc].  Each interval's Taylor
-// series of erfc(xi r) about its midpoint (the Hermite recurrence above, long double) is cut at
-// the first degree n whose next two terms at the interval's edge are below 2e-16 of erfc there
-// (the same relative target as the 300-interval table), the worst interval deciding; the degree
-// is padded up to a compiled size 2 NP - 1 (kRealNP).  xi rc = 3 (C5) takes degree 13, 4.9
-// (C1-C4, C5 at rc = 0.164) degree 19; beyond degree 31 (xi rc > ~7.5, erfc(xi rc) < 1e-25)
-// real_space falls back to the thread-per-target kernel and its 300+-interval table.
-static std::vector<long double> erfc_taylor_k(double xi, double rc, int& need) {
-  const long double two_over_sqrtpi = 1.128379167095512573896158903121545172L;
-  constexpr int kMaxN = 48;
+// k_real_warp's few-interval table: kRealK = 32 intervals of [0, rc]; on each, the polynomial in
+// u = r - r_mid interpolating erfc(xi r) at the Chebyshev points of the interval (erfcl, long
+// double), converted to monomial coefficients.  The degree is the smallest for which every
+// interval's interpolant stays within 2e-16 of erfc (relative, checked on 64 points per interval in
+// long double) -- the 300-interval Taylor table's target; interpolation at Chebyshev points needs
+// ~3 degrees fewer than the Taylor polynomial about the midpoint (degree 9 instead of 11 at
+// xi rc = 3, 12 instead of 15 at 4.9).  The degree is padded up to a compiled size 2 NP - 1
+// (kRealNP).  Beyond degree 31 (xi rc >~ 10) real_space falls back to the thread-per-target
+// kernel and its long Taylor table.
+static bool cheb_interval(double xi, long double rmid, long double hw, int n, long double* mono) {
+  long double f[32], a[32], T[32][32] = {}, tm[32] = {};
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int k = 0; k <= n; ++k) f[k] = erfcl((long double)xi * (rmid + hw * cosl(pi * (k + 0.5L) / (n + 1))));
+  for (int j = 0; j <= n; ++j) {
+    long double sum = 0.0L;
+    for (int k = 0; k <= n; ++k) sum += f[k] * cosl(pi * j * (k + 0.5L) / (n + 1));
+    a[j] = sum * 2.0L / (n + 1);
+  }
+  a[0] *= 0.5L;
+  T[0][0] = 1.0L;   // monomial coefficients of T_j(t)
+  if (n >= 1) T[1][1] = 1.0L;
+  for (int j = 2; j <= n; ++j)
+    for (int m = 0; m <= j; ++m) T[j][m] = (m > 0 ? 2.0L * T[j - 1][m - 1] : 0.0L) - T[j - 2][m];
+  for (int j = 0; j <= n; ++j)
+    for (int m = 0; m <= j; ++m) tm[m] += a[j] * T[j][m];
+  long double sc = 1.0L;   // t = u / hw
+  for (int m = 0; m <= n; ++m) {
+    mono[m] = tm[m] / sc;
+    sc *= hw;
+  }
+  for (int k = 0; k <= 64; ++k) {   // relative error on a fine grid
+    const long double u = hw * (-1.0L + 2.0L * k / 64.0L);
+    long double pv = mono[n];
+    for (int m = n - 1; m >= 0; --m) pv = pv * u + mono[m];
+    const long double e = erfcl((long double)xi * (rmid + u));
+    if (fabsl(pv - e) > 2e-16L * e) return false;
+  }
+  return true;
+}
+
+// degree and monomial coefficients [K][32] (0 past the degree); degree 0: not representable
+static std::vector<long double> erfc_cheb_k(double xi, double rc, int& deg) {
   const int K = kRealK;
   const long double w = (long double)rc / K, hw = 0.5L * w;
-  std::vector<long double> c((size_t)K * (kMaxN + 1));
-  need = 0;
-  for (int i = 0; i < K; ++i) {
-    const long double x0 = (long double)xi * ((long double)i + 0.5L) * w;
-    const long double g = two_over_sqrtpi * expl(-x0 * x0);
-    long double* ci = &c[(size_t)i * (kMaxN + 1)];
-    ci[0] = erfcl(x0);
-    long double hm1 = 0.0L, h = 1.0L, xin = 1.0L, fact = 1.0L;
-    for (int n = 1; n <= kMaxN; ++n) {   // coefficient of u^n: (-1)^n (2/sqrt(pi)) H_{n-1}(x0) e^{-x0^2} xi^n / n!
-      xin *= (long double)xi;
-      fact *= (long double)n;
-      ci[n] = ((n & 1) ? -1.0L : 1.0L) * g * h * xin / fact;
-      const long double hn = 2.0L * x0 * h - 2.0L * (long double)(n - 1) * hm1;
-      hm1 = h;
-      h = hn;
-    }
-    const long double edge = erfcl((long double)xi * ((long double)i + 1.0L) * w);
-    int n = 1;
-    while (n + 2 <= kMaxN && fabsl(ci[n + 1]) * powl(hw, n + 1) + fabsl(ci[n + 2]) * powl(hw, n + 2) >= 2e-16L * edge)
-      ++n;
-    need = std::max(need, n);
+  std::vector<long double> c((size_t)K * 32, 0.0L);
+  for (deg = 3; deg <= 31; ++deg) {
+    bool ok = true;
+    for (int i = 0; i < K && ok; ++i) ok = cheb_interval(xi, ((long double)i + 0.5L) * w, hw, deg, &c[(size_t)i * 32]);
+    if (ok) return c;
+    std::fill(c.begin(), c.end(), 0.0L);
   }
+  deg = 0;
   return c;
 }
 
-int real_table_np(double xi, double rc) {
-  int need = 0;
-  erfc_taylor_k(xi, rc, need);
-  for (int np : kRealNP)
-    if (2 * np - 1 >= need) return np;
-  return 0;
+int real_table_np(double xi, double rc) {   // memoised: the fit costs milliseconds of host time
+  static std::mutex mu;
+  static std::vector<std::array<double, 3>> memo;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& m : memo)
+      if (m[0] == xi && m[1] == rc) return (int)m[2];
+  }
+  int deg = 0, np = 0;
+  erfc_cheb_k(xi, rc, deg);
+  if (deg > 0)
+    for (int v : kRealNP)
+      if (2 * v - 1 >= deg) {
+        np = v;
+        break;
+      }
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() > 64) memo.clear();
+  memo.push_back({xi, rc, (double)np});
+  return np;
 }
 
 static std::vector<double> erfc_small_table(double xi, double rc, int NP) {
-  int need = 0;
-  const std::vector<long double> c = erfc_taylor_k(xi, rc, need);
+  int deg = 0;
+  const std::vector<long double> c = erfc_cheb_k(xi, rc, deg);
   const int K = kRealK;
   std::vector<double> t((size_t)2 * NP * K, 0.0);
   for (int n = 0; n < 2 * NP; ++n)
     for (int i = 0; i < K; ++i) {
-      const double v = n <= need ? (double)c[(size_t)i * 49 + n] : 0.0;
+      const double v = n <= deg ? (double)c[(size_t)i * 32 + n] : 0.0;
 #if SE1P_REAL_TABLAYOUT
       t[(size_t)n * K + i] = v;
 #else

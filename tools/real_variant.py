@@ -11,7 +11,7 @@ from se1p_synth import CONFIGS, make_system  # noqa: E402
 
 if sys.argv[1] != "product":
     se1p.LIB_PATH = os.path.join(os.path.dirname(se1p.LIB_PATH), f"libse1p_{sys.argv[1]}.so")
-for name in ["C4", "C5"]:
+for name in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["C4", "C5"]):
     c = CONFIGS[name]
     x, q = make_system(c.N, c.L, c.seed)
     xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
