@@ -127,6 +127,46 @@ def test_real_space_vs_oracle():
         assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)), (L, xi, rc)
 
 
+def test_real_space_edge_cases():
+    """k_real_warp's target groups and candidate ranges on awkward layouts, against the direct sum
+    (Eq. (3) + Eq. (6)): one particle, a pair inside / outside rc, every particle in one column,
+    a dense cluster (heavy groups next to near-empty columns), rc below the cell size with most
+    particles alone, a rectangular box with z images, and particles on the box faces."""
+    rng = np.random.default_rng(11)
+    cases = []
+    cases.append(((1, 1, 1), 6.0, 0.3, np.array([[0.5, 0.5, 0.5]]), np.array([0.7])))
+    cases.append(((1, 1, 1), 6.0, 0.3, np.array([[0.1, 0.1, 0.1], [0.2, 0.15, 0.95]]), np.array([1.0, -1.0])))
+    cases.append(((1, 1, 1), 6.0, 0.3, np.array([[0.1, 0.1, 0.1], [0.9, 0.9, 0.5]]), np.array([1.0, -1.0])))
+    n = 600   # one column
+    x = np.column_stack([0.5 + 1e-3 * rng.random(n), 0.5 + 1e-3 * rng.random(n), rng.random(n)])
+    cases.append(((1, 1, 1), 10.0, 0.25, x, rng.uniform(-1, 1, n)))
+    n = 3000   # a dense cluster plus a uniform background
+    x = np.concatenate([0.3 + 0.02 * rng.random((n // 2, 3)), rng.random((n - n // 2, 3))])
+    cases.append(((1, 1, 1), 12.0, 0.2, x, rng.uniform(-1, 1, n)))
+    n = 2000   # rc far below the cell size
+    cases.append(((1, 1, 1), 300.0, 0.01, rng.random((n, 3)), rng.uniform(-1, 1, n)))
+    n = 1500   # rectangular, z images (rc > L3 / 2)
+    L = (1.0, 2.0, 0.5)
+    cases.append((L, 8.0, 0.3, rng.random((n, 3)) * np.array(L), rng.uniform(-1, 1, n)))
+    n = 800   # on the faces: x = 0, y = 0, z = 0 and z just below L3
+    x = rng.random((n, 3))
+    x[: n // 4, 0] = 0.0
+    x[n // 4: n // 2, 1] = 0.0
+    x[n // 2: 3 * n // 4, 2] = 0.0
+    x[3 * n // 4:, 2] = np.nextafter(1.0, 0.0)
+    cases.append(((1, 1, 1), 8.0, 0.4, x, rng.uniform(-1, 1, n)))
+    for L, xi, rc, x, q in cases:
+        q = q - (q.mean() if q.size > 1 else 0.0)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        xd, qd = _dev(x, q)
+        got = se1p.real(xd, qd, L, xi, rc, skip_checks=True).cpu().numpy()
+        ref = oracle.phi_real(x, q, L, xi, rc) + oracle.phi_self(q, xi)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300), (L, xi, rc, x.shape)
+        _, fg = se1p.real(xd, qd, L, xi, rc, skip_checks=True, field=True)
+        fr = oracle.field_real(x, q, L, xi, rc)
+        assert np.max(np.abs(fg.cpu().numpy() - fr)) <= 1e-12 * max(np.max(np.abs(fr)), 1e-300), (L, xi, rc)
+
+
 def test_bitwise_determinism_and_host_io():
     c = CONFIGS["C2"]
     x, q = make_system(c.N, c.L, c.seed)
