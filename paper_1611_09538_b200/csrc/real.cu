@@ -312,16 +312,16 @@ static void launch_real_cells(const RDev& d, const double4* P4, const int* perm,
 
 
 // ---------------------------------------------------------------- k_real_warp (SE1P_REAL_KERNEL 2)
-// Warp per 32 consecutive sorted targets (one per lane; the fine-bin order makes them a compact
-// box).  The warp walks the columns whose xy distance to its bounding box is <= rc; in each, the z
-// interval within rc of the box is one index range per periodic image.  Candidates are loaded 32 at
-// a time (coalesced), culled one per lane against the box, and the survivors staged in a 64-entry
-// shared ring.  A *phase* tests 32 staged candidates against every lane's target (a uniform loop,
-// broadcast reads); each lane writes its hits (r^2, ring slot) to its own column of a pair buffer.
-// A warp prefix sum over the hit counts then lays the phase's T pairs out in lane order and the
-// warp evaluates them 32 at a time -- every lane busy, whatever the hit counts -- writing each
-// pair's q_n erfc(xi r)/r back in place; finally each lane sums its own entries in candidate order
-// (deterministic: the order depends only on the sorted input).
+// Warp per group of <= 32 targets of one column (one per lane; the column-then-fine-z order makes a
+// group a compact box).  The warp walks the columns whose xy distance to its bounding box is <= rc;
+// in each, the z interval within rc of the box is one index range per periodic image.  Candidates
+// are loaded 32 at a time (coalesced), culled one per lane against the box, and the survivors
+// staged in a 64-entry shared ring.  A *phase* (rw_phase) tests 32 staged candidates against every
+// lane's target into hit masks, then walks the candidates any lane hits with every lane evaluating
+// each and keeping its own term by a select.  erfc(xi r) from a small shared-memory table
+// (rw_pair).  Each target sums its terms in candidate order: deterministic.  (Measured and not
+// kept: the hit test in fp32 with a safe margin and an fp64 re-test at evaluation, +5 % at C5:
+// the extra fp32 copy of the ring costs more than the cheaper test saves.)
 constexpr int kRWW = 8;                    // warps per block (at most; fewer for small systems)
 struct RWarpSm {
   double4 cand[64];                        // staged candidates: x, y, z + image shift, q (ring)
