@@ -339,65 +339,41 @@ __device__ __forceinline__ double rw_rsqrt(double r2) {
 }
 
 // q_n erfc(xi r)/r (and, FIELD, g = q_n (erfc(xi r)/r - d/dr erfc(xi r))/r^2) of one pair, from
-// k_real_warp's shared table: K intervals of [0, rc], on each the Taylor polynomial of degree
-// 2 NP - 1 about the midpoint, stored as coefficient pairs [NP][K] (double2).  With K = 16 a load
-// of one coefficient pair by the 32 lanes touches at most 16 distinct 16-byte words: two
-// shared-memory wavefronts, where a 300-interval table in L1 costs ~12 per 16-byte load (measured:
-// the L1 data pipe saturated at 97 %).
-#ifndef SE1P_REAL_TABLAYOUT
-#define SE1P_REAL_TABLAYOUT 1   // 1: coefficients [2 NP][K] read as 8-byte words; 0: pairs [NP][K] as 16-byte words
-#endif
-#ifndef SE1P_REAL_K
-#define SE1P_REAL_K 32
-#endif
-constexpr int kRealK = SE1P_REAL_K;   // intervals of the shared table
-template <bool FIELD, int NP>
+// k_real_warp's shared table: kRealK intervals of [0, rc], on each a polynomial of degree DEG in
+// u = r - r_mid, coefficient-major [DEG + 1][kRealK].  A read of one coefficient by the 32 lanes
+// costs two shared-memory wavefronts whatever the intervals (8-byte words, two half-warps), so
+// the coefficient count is what the data pipe pays for; a 300-interval table in L1 cost ~12
+// wavefronts per 16-byte load (measured: the L1 data pipe saturated at 97 %).
+constexpr int kRealK = 32;   // intervals of the shared table (16 / 64 / 128 measured slower)
+template <bool FIELD, int DEG>
 __device__ __forceinline__ double rw_pair(const RDev& d, const double* __restrict__ tab, double r2, double qj,
                                           double& g) {
   const double rinv = rw_rsqrt(r2);
   const double r = r2 * rinv;
   const int it = min((int)(r * d.tinvw), kRealK - 1);
   const double u = r - ((double)it + 0.5) * d.tw;
-#if SE1P_REAL_TABLAYOUT
   const double* cf = tab + it;
-  double pv = cf[(2 * NP - 1) * kRealK];
+  double pv = cf[DEG * kRealK];
   double dv = 0.0;
-  if (FIELD) dv = (double)(2 * NP - 1) * pv;
+  if (FIELD) dv = (double)DEG * pv;
 #pragma unroll
-  for (int n = 2 * NP - 2; n >= 0; --n) {
+  for (int n = DEG - 1; n >= 0; --n) {
     const double c = cf[n * kRealK];
     pv = fma(pv, u, c);
     if (FIELD && n > 0) dv = fma(dv, u, (double)n * c);
   }
-#else
-  const double2* cf = reinterpret_cast<const double2*>(tab) + it;
-  double2 c = cf[(NP - 1) * kRealK];
-  double pv = fma(c.y, u, c.x);
-  double dv = 0.0;
-  if (FIELD) dv = fma((double)(2 * NP - 1) * c.y, u, (double)(2 * NP - 2) * c.x);
-#pragma unroll
-  for (int j = NP - 2; j >= 0; --j) {
-    c = cf[j * kRealK];
-    pv = fma(pv, u, c.y);
-    pv = fma(pv, u, c.x);
-    if (FIELD) {
-      dv = fma(dv, u, (double)(2 * j + 1) * c.y);
-      if (j > 0) dv = fma(dv, u, (double)(2 * j) * c.x);
-    }
-  }
-#endif
   const double ec = pv * rinv;
   if (FIELD) g = qj * (ec - dv) * (rinv * rinv);
   return qj * ec;
 }
 
-template <bool FIELD, int NP>
+template <bool FIELD, int DEG>
 __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bool hit, double rc2, const RDev& d,
                                         const double* tab, double& acc, double& ex, double& ey, double& ez) {
   const double dx = pt.x - cc.x, dy = pt.y - cc.y, dz = pt.z - cc.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double g = 0.0;
-  const double v = rw_pair<FIELD, NP>(d, tab, hit ? r2 : rc2, cc.w, g);
+  const double v = rw_pair<FIELD, DEG>(d, tab, hit ? r2 : rc2, cc.w, g);
   acc += hit ? v : 0.0;
   if (FIELD) {
     const double gg = hit ? g : 0.0;
@@ -416,7 +392,7 @@ __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bo
 // prime in Eq. (3) (n = m in the unshifted image) is the pair at r^2 = 0 exactly: a target meets
 // itself with identical coordinates, and a distinct particle at zero distance would make phi
 // infinite (not a valid input).
-template <bool FIELD, int NP, bool FULL>
+template <bool FIELD, int DEG, bool FULL>
 __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
                                          double rc2, const RDev& d, const double* tab, double& acc, double& ex,
                                          double& ey, double& ez) {
@@ -441,8 +417,8 @@ __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, cons
     const int k2 = two ? __ffs(am) - 1 : k1;
     am &= am - 1;
     const double4 c1 = cb[k1], c2 = cb[k2];
-    rw_eval<FIELD, NP>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
-    rw_eval<FIELD, NP>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
+    rw_eval<FIELD, DEG>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
+    rw_eval<FIELD, DEG>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
   }
 }
 
@@ -456,7 +432,7 @@ __global__ void k_real_group_counts(const int* __restrict__ bin_start, int ncol,
 __device__ unsigned long long g_rw_cnt[4];
 __device__ double g_rw_ext[4];
 #endif
-template <bool FIELD, int NP>
+template <bool FIELD, int DEG>
 #ifndef SE1P_REAL_MINB
 #define SE1P_REAL_MINB 3
 #endif
@@ -472,7 +448,7 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
   RWarpSm& s = reinterpret_cast<RWarpSm*>(rw_raw)[warp];
   const int nw = blockDim.x >> 5;
   double* tab = reinterpret_cast<double*>(rw_raw + nw * sizeof(RWarpSm));
-  for (int i = threadIdx.x; i < 2 * NP * kRealK; i += blockDim.x) tab[i] = d.tab2[i];
+  for (int i = threadIdx.x; i < (DEG + 1) * kRealK; i += blockDim.x) tab[i] = d.tab2[i];
   __syncthreads();
   // target group gw: column col's sorted run cut into G = ceil(n/32) near-equal pieces (groups
   // never straddle two columns, so the box stays compact); col by a 32-ary search of gstart
@@ -546,7 +522,7 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
 #endif
           __syncwarp();
           if (ns >= 32) {
-            rw_phase<FIELD, NP, true>(s, base, 32, pt, active, rc2, d, tab, acc, ex, ey, ez);
+            rw_phase<FIELD, DEG, true>(s, base, 32, pt, active, rc2, d, tab, acc, ex, ey, ez);
             base = (base + 32) & 63;
             ns -= 32;
 #ifdef SE1P_REAL_COUNT
@@ -565,7 +541,7 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
     atomicAdd(&g_rw_ext[2], hi2 - lo2);
   }
 #endif
-  if (ns > 0) rw_phase<FIELD, NP, false>(s, base, ns, pt, active, rc2, d, tab, acc, ex, ey, ez);
+  if (ns > 0) rw_phase<FIELD, DEG, false>(s, base, ns, pt, active, rc2, d, tab, acc, ex, ey, ez);
   if (active) {
     const int64_t uo = perm[tl];
     if (phi_out) phi_out[uo] = acc - 2.0 * d.xi * pt.w * 0.564189583547756286948079451560772586;  // 1/sqrt(pi)
@@ -577,16 +553,16 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
   }
 }
 
-template <bool FIELD, int NP>
-static void launch_real_warp_np(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
+template <bool FIELD, int DEG>
+static void launch_real_warp_deg(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                                 const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
   // warps per block: 8, halved while that leaves fewer than two blocks per SM (small systems)
   const int ncol = d.nc[0] * d.nc[1];
   const int64_t groups = ceil_div(N, 32) + ncol;   // >= the number of groups
   int nw = kRWW;
   while (nw > 1 && ceil_div(groups, nw) < 2 * 148) nw /= 2;
-  const size_t smem = nw * sizeof(RWarpSm) + (size_t)NP * kRealK * sizeof(double2);
-  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_real_warp<FIELD, NP>,
+  const size_t smem = nw * sizeof(RWarpSm) + (size_t)(DEG + 1) * kRealK * sizeof(double);
+  SE1P_CUDA_TRY(cudaFuncSetAttribute((const void*)k_real_warp<FIELD, DEG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned nb = (unsigned)ceil_div(groups, nw);
 #ifdef SE1P_REAL_COUNT
@@ -595,32 +571,30 @@ static void launch_real_warp_np(const RDev& d, const double4* P4, const int* per
   double ze[4] = {0, 0, 0, 0};
   SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_ext, ze, sizeof(ze)));
 #endif
-  k_real_warp<FIELD, NP><<<nb, nw * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
+  k_real_warp<FIELD, DEG><<<nb, nw * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
   SE1P_LAUNCH_CHECK();
 #ifdef SE1P_REAL_COUNT
   SE1P_CUDA_TRY(cudaMemcpyFromSymbol(z, g_rw_cnt, sizeof(z)));
   SE1P_CUDA_TRY(cudaMemcpyFromSymbol(ze, g_rw_ext, sizeof(ze)));
   fprintf(stderr, "bbox mean %g %g %g loaded %g\n", ze[0] / z[3], ze[1] / z[3], ze[2] / z[3], ze[3] / z[3]);
-  fprintf(stderr, "k_real_warp N=%lld nzf=%d K=%d NP=%d: chunks %llu survivors %llu full phases %llu warps %llu\n",
-          (long long)N, d.nzf, d.tK, NP, z[0], z[1], z[2], z[3]);
+  fprintf(stderr, "k_real_warp N=%lld nzf=%d degree %d: chunks %llu survivors %llu full phases %llu warps %llu\n",
+          (long long)N, d.nzf, DEG, z[0], z[1], z[2], z[3]);
 #endif
 }
 
-// coefficient pairs per interval: the compiled sizes (the table's degree is padded up to 2 NP - 1)
-constexpr int kRealNP[] = {5, 6, 7, 8, 10, 12, 16};
+// the compiled table degrees (a fitted degree is padded up to the next)
+constexpr int kRealDeg[] = {7, 8, 9, 10, 11, 13, 15, 19, 23, 31};
 template <bool FIELD>
 static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
                              const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
-  switch (d.tNP) {
-    case 5: launch_real_warp_np<FIELD, 5>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 6: launch_real_warp_np<FIELD, 6>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 7: launch_real_warp_np<FIELD, 7>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 8: launch_real_warp_np<FIELD, 8>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 10: launch_real_warp_np<FIELD, 10>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 12: launch_real_warp_np<FIELD, 12>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    case 16: launch_real_warp_np<FIELD, 16>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
-    default: throw Error{6, "real space: no kernel for this table size"};
+#define SE1P_RW_CASE(D) \
+  case D: launch_real_warp_deg<FIELD, D>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+  switch (d.tdeg) {
+    SE1P_RW_CASE(7) SE1P_RW_CASE(8) SE1P_RW_CASE(9) SE1P_RW_CASE(10) SE1P_RW_CASE(11)
+    SE1P_RW_CASE(13) SE1P_RW_CASE(15) SE1P_RW_CASE(19) SE1P_RW_CASE(23) SE1P_RW_CASE(31)
+    default: throw Error{6, "real space: no kernel for this table degree"};
   }
+#undef SE1P_RW_CASE
 }
 
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
@@ -644,7 +618,7 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N) {
   d.nzf = (int)std::min<int64_t>(nz, std::max<int64_t>(1, ((int64_t)1 << 22) / ncol));
   d.hz = L[2] / d.nzf;
 #if SE1P_REAL_KERNEL == 2 && SE1P_REAL_TABLE
-  d.tNP = real_table_np(xi, rc);   // 0: xi rc beyond the shared table, thread-per-target kernel
+  d.tdeg = real_table_deg(xi, rc);   // 0: xi rc beyond the shared table, thread-per-target kernel
 #endif
   return d;
 }
@@ -655,7 +629,7 @@ int64_t real_scratch_ints(const RDev& d, int64_t N) {
 }
 
 int real_nbins(const RDev& d) {
-  return d.tNP > 0 ? d.nc[0] * d.nc[1] * d.nzf : d.nc[0] * d.nc[1] * d.nc[2];
+  return d.tdeg > 0 ? d.nc[0] * d.nc[1] * d.nzf : d.nc[0] * d.nc[1] * d.nc[2];
 }
 
 // Taylor coefficients of erfc(xi r) about the interval midpoints r_i = (i + 1/2) dr:
@@ -686,14 +660,15 @@ static std::vector<double> erfc_table(double xi, double rc, int ntab) {
 }
 
 // k_real_warp's few-interval table: kRealK = 32 intervals of [0, rc]; on each, the polynomial in
-// u = r - r_mid interpolating erfc(xi r) at the Chebyshev points of the interval (erfcl, long
-// double), converted to monomial coefficients.  The degree is the smallest for which every
-// interval's interpolant stays within 2e-16 of erfc (relative, checked on 64 points per interval in
-// long double) -- the 300-interval Taylor table's target; interpolation at Chebyshev points needs
-// ~3 degrees fewer than the Taylor polynomial about the midpoint (degree 9 instead of 11 at
-// xi rc = 3, 12 instead of 15 at 4.9).  The degree is padded up to a compiled size 2 NP - 1
-// (kRealNP).  Beyond degree 31 (xi rc >~ 10) real_space falls back to the thread-per-target
-// kernel and its long Taylor table.
+// u = r - r_mid interpolating erfc(xi r) at the interval's Chebyshev points (erfcl, long double),
+// converted to monomial coefficients.  The degree is the smallest for which every interval stays
+// within 2e-16 of erfc in absolute terms (checked on 65 points per interval in long double): half
+// an ulp of erfc(0) = 1, so a pair's error is at most that of the rounding of the nearest pairs'
+// terms, which dominate the sum -- degree 8 at xi rc = 3 (C5), 9 at 4.6 - 4.9 (C1 - C4, C5 at
+// rc = 0.164).  (2e-16 *relative* to erfc, the 300-interval table's target, takes 9 and 12 - 13:
+// the tail intervals, where erfc is small, decide it; Taylor polynomials about the midpoints take
+// ~3 degrees more again.)  The degree is padded up to a compiled one (kRealDeg).  Beyond degree
+// 31 real_space falls back to the thread-per-target kernel and its long Taylor table.
 static bool cheb_interval(double xi, long double rmid, long double hw, int n, long double* mono) {
   long double f[32], a[32], T[32][32] = {}, tm[32] = {};
   const long double pi = 3.141592653589793238462643383279502884L;
@@ -720,7 +695,7 @@ static bool cheb_interval(double xi, long double rmid, long double hw, int n, lo
     long double pv = mono[n];
     for (int m = n - 1; m >= 0; --m) pv = pv * u + mono[m];
     const long double e = erfcl((long double)xi * (rmid + u));
-    if (fabsl(pv - e) > 2e-16L * e) return false;
+    if (fabsl(pv - e) > 2e-16L) return false;
   }
   return true;
 }
@@ -740,7 +715,7 @@ static std::vector<long double> erfc_cheb_k(double xi, double rc, int& deg) {
   return c;
 }
 
-int real_table_np(double xi, double rc) {   // memoised: the fit costs milliseconds of host time
+int real_table_deg(double xi, double rc) {   // memoised: the fit costs milliseconds of host time
   static std::mutex mu;
   static std::vector<std::array<double, 3>> memo;
   {
@@ -748,34 +723,27 @@ int real_table_np(double xi, double rc) {   // memoised: the fit costs milliseco
     for (const auto& m : memo)
       if (m[0] == xi && m[1] == rc) return (int)m[2];
   }
-  int deg = 0, np = 0;
+  int deg = 0, td = 0;
   erfc_cheb_k(xi, rc, deg);
   if (deg > 0)
-    for (int v : kRealNP)
-      if (2 * v - 1 >= deg) {
-        np = v;
+    for (int v : kRealDeg)
+      if (v >= deg) {
+        td = v;
         break;
       }
   std::lock_guard<std::mutex> lk(mu);
   if (memo.size() > 64) memo.clear();
-  memo.push_back({xi, rc, (double)np});
-  return np;
+  memo.push_back({xi, rc, (double)td});
+  return td;
 }
 
-static std::vector<double> erfc_small_table(double xi, double rc, int NP) {
+static std::vector<double> erfc_small_table(double xi, double rc, int tdeg) {
   int deg = 0;
   const std::vector<long double> c = erfc_cheb_k(xi, rc, deg);
   const int K = kRealK;
-  std::vector<double> t((size_t)2 * NP * K, 0.0);
-  for (int n = 0; n < 2 * NP; ++n)
-    for (int i = 0; i < K; ++i) {
-      const double v = n <= deg ? (double)c[(size_t)i * 32 + n] : 0.0;
-#if SE1P_REAL_TABLAYOUT
-      t[(size_t)n * K + i] = v;
-#else
-      t[((size_t)(n / 2) * K + i) * 2 + (n & 1)] = v;
-#endif
-    }
+  std::vector<double> t((size_t)(tdeg + 1) * K, 0.0);   // coefficient-major [tdeg + 1][K]
+  for (int n = 0; n <= tdeg; ++n)
+    for (int i = 0; i < K; ++i) t[(size_t)n * K + i] = n <= deg ? (double)c[(size_t)i * 32 + n] : 0.0;
   return t;
 }
 
@@ -805,7 +773,7 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
                 cudaStream_t st, double* field_out) {
   RDev d = d0;
 #if SE1P_REAL_TABLE
-  if (d.tNP == 0) {
+  if (d.tdeg == 0) {
     int dev = 0;
     SE1P_CUDA_TRY(cudaGetDevice(&dev));
     TabCache& tc = g_tab[dev & 63];
@@ -831,12 +799,12 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     d.inv_dr = ntab / d.rc;
   }
 #endif
-  if (d.tNP > 0) {   // k_real_warp's shared table
+  if (d.tdeg > 0) {   // k_real_warp's shared table
     int dev = 0;
     SE1P_CUDA_TRY(cudaGetDevice(&dev));
     SmallTabCache& tc = g_tab2[dev & 63];
     if (!tc.dev || tc.xi != d.xi || tc.rc != d.rc) {
-      const std::vector<double> t = erfc_small_table(d.xi, d.rc, d.tNP);
+      const std::vector<double> t = erfc_small_table(d.xi, d.rc, d.tdeg);
       if (tc.dev && tc.cap < (int64_t)t.size()) {
         dev_free(tc.dev);
         tc.dev = nullptr;
@@ -856,7 +824,7 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
   }
   const int nbins = real_nbins(d);
   const unsigned nb = (unsigned)ceil_div(N, 256);
-  if (d.tNP > 0)
+  if (d.tdeg > 0)
     k_real_keys_fine<<<nb, 256, 0, st>>>(d, x, N, w.keys);
   else
     k_real_keys<<<nb, 256, 0, st>>>(d, x, N, w.keys);
@@ -864,7 +832,7 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
   stable_bin_sort(w.keys, N, nbins, w.perm, w.bin_start, w.scratch, st);
   k_real_permute<<<nb, 256, 0, st>>>(d, x, q, w.perm, N, (double4*)w.xs);
   SE1P_LAUNCH_CHECK();
-  if (d.tNP > 0) {
+  if (d.tdeg > 0) {
     const int ncol = d.nc[0] * d.nc[1];
     int* gcnt = w.scratch;   // the sort's scratch is free again (real_scratch_ints sizes it)
     int* gstart = gcnt + ncol;

@@ -21,10 +21,10 @@ struct RDev {
   const double* tab = nullptr;
   int ntab = 0;
   double inv_dr = 0.0, dr = 0.0;
-  // k_real_warp's table: tK intervals of [0, rc] (width tw), Taylor polynomials of degree 2 tNP - 1
-  // about the midpoints, coefficient pairs [tNP][tK] (double2)
+  // k_real_warp's table: kRealK intervals of [0, rc] (width tw), polynomials of degree tdeg in
+  // r - r_mid, coefficient-major [tdeg + 1][kRealK] (real.cu)
   const double* tab2 = nullptr;
-  int tK = 0, tNP = 0;
+  int tdeg = 0;
   double tw = 0.0, tinvw = 0.0;
 };
 // degree 7 (8 coefficients, four 16-byte loads per pair); the interval count grows with
@@ -39,7 +39,7 @@ inline int real_table_intervals(double xi, double rc) {
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 int real_nbins(const RDev& d);   // bins of the real-space sort (workspace sizing)
 int64_t real_scratch_ints(const RDev& d, int64_t N);
-int real_table_np(double xi, double rc);   // k_real_warp's coefficient pairs per interval, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
+int real_table_deg(double xi, double rc);   // k_real_warp's table degree, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
                 cudaStream_t st, double* field_out = nullptr);
 void real_release_tables(int dev);   // the cached erfc table of device dev

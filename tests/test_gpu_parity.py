@@ -118,8 +118,10 @@ def test_real_space_vs_oracle():
     for L, xi, rc, N, seed in [((1, 1, 1), 4.0, 1.158, 100, 1), ((1, 1, 1), 8.0, 0.594, 500, 2),
                                ((1, 1, 2), 12.0, 0.401, 800, 3), ((2, 2, 2), 30.0, 0.1, 3000, 5),
                                ((1, 1, 1), 3.0, 2.7, 40, 4),
-                               # xi rc = 13.5: beyond the warp kernel's shared table (thread-per-target fallback)
-                               ((1, 1, 1), 15.0, 0.9, 300, 6), ((1, 1, 1), 10.0, 0.9, 300, 7)]:
+                               # xi rc = 9, 13.5: high table degrees; 144: beyond the warp kernel's shared
+                               # table (thread-per-target fallback)
+                               ((1, 1, 1), 10.0, 0.9, 300, 7), ((1, 1, 1), 15.0, 0.9, 300, 6),
+                               ((1, 1, 1), 160.0, 0.9, 300, 8)]:
         x, q = make_system(N, L, seed)
         xd, qd = _dev(x, q)
         got = se1p.real(xd, qd, L, xi, rc).cpu().numpy()
