@@ -344,7 +344,10 @@ __device__ __forceinline__ double rw_rsqrt(double r2) {
 // costs two shared-memory wavefronts whatever the intervals (8-byte words, two half-warps), so
 // the coefficient count is what the data pipe pays for; a 300-interval table in L1 cost ~12
 // wavefronts per 16-byte load (measured: the L1 data pipe saturated at 97 %).
-constexpr int kRealK = 32;   // intervals of the shared table (16 / 64 / 128 measured slower)
+#ifndef SE1P_REAL_K
+#define SE1P_REAL_K 32
+#endif
+constexpr int kRealK = SE1P_REAL_K;   // intervals of the shared table (16 / 64 / 128 measured slower)
 template <bool FIELD, int DEG>
 __device__ __forceinline__ double rw_pair(const RDev& d, const double* __restrict__ tab, double r2, double qj,
                                           double& g) {
