@@ -169,6 +169,31 @@ def test_real_space_edge_cases():
         assert np.max(np.abs(fg.cpu().numpy() - fr)) <= 1e-12 * max(np.max(np.abs(fr)), 1e-300), (L, xi, rc)
 
 
+def test_real_space_random_configurations():
+    """Seeded random real-space configurations -- box shape (rectangular, long or short periodic
+    axis), density, xi rc from 1 to 12 (table degrees 7 .. 15), rc from a fraction of a cell to
+    beyond L3 (several z images), uniform or half-clustered positions -- potential and field
+    against the direct sum (Eq. (3) + Eq. (6)) at 1e-12 of the largest value."""
+    rng = np.random.default_rng(2024)
+    for case in range(30):
+        L = tuple(float(v) for v in rng.choice([0.5, 1.0, 1.5, 2.0], size=3))
+        N = int(rng.integers(2, 2500))
+        rc = float(rng.uniform(0.05, 1.2) * min(L))
+        xi = float(rng.uniform(1.0, 12.0) / rc)
+        x = rng.random((N, 3)) * np.array(L)
+        if case % 3 == 0:   # half of the particles in a small cluster
+            k = N // 2
+            x[:k] = np.array(L) * (0.2 + 0.1 * rng.random((k, 3)))
+        q = rng.uniform(-1, 1, N)
+        q -= q.mean()
+        xd, qd = _dev(x, q)
+        got, fg = se1p.real(xd, qd, L, xi, rc, skip_checks=True, field=True)
+        ref = oracle.phi_real(x, q, L, xi, rc) + oracle.phi_self(q, xi)
+        fr = oracle.field_real(x, q, L, xi, rc)
+        assert np.max(np.abs(got.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref)), (case, L, N, xi, rc)
+        assert np.max(np.abs(fg.cpu().numpy() - fr)) <= 1e-12 * max(np.max(np.abs(fr)), 1e-300), (case, L, N, xi, rc)
+
+
 def test_bitwise_determinism_and_host_io():
     c = CONFIGS["C2"]
     x, q = make_system(c.N, c.L, c.seed)
