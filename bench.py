@@ -278,8 +278,8 @@ def bench_ours(args, cfg, rank, world, local):
 
     # full SE1P at this config (BASELINE C5: real-space erfc sum with cell lists at rc plus k-space):
     # the real-space call timed alone on the same stream, reported beside the k-space metric
-    full = None
-    if not rs and getattr(cfg, "rc", None):
+    full = None   # single GPU only (the real-space sum is not sharded over ranks)
+    if world == 1 and getattr(cfg, "rc", None):
         rbuf = torch.empty(cfg.N, dtype=torch.float64, device=dev)
         se1p.real(x, q, cfg.L, cfg.xi, cfg.rc, out=rbuf, stream=stream)   # erfc table, workspace, checked
         torch.cuda.synchronize(dev)
