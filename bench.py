@@ -254,6 +254,38 @@ def bench_ours(args, cfg, rank, world, local):
     else:
         e2e_s = pipe_s
 
+    # full SE1P at this config (BASELINE C5: real-space erfc sum with cell lists at rc plus k-space):
+    # the real-space call timed alone on the step's stream (N > 1: dist.real, each rank its part of
+    # the targets and one all-reduce, max over ranks), reported beside the k-space metric
+    full = None
+    if not rs and getattr(cfg, "rc", None):
+        rbuf = torch.empty(n_loc, dtype=torch.float64, device=dev)
+
+        def real_step():
+            if world > 1:
+                return sdist.real(x, q, cfg.L, cfg.xi, cfg.rc, stream=stream)
+            return se1p.real(x, q, cfg.L, cfg.xi, cfg.rc, out=rbuf, stream=stream, sync=False, skip_checks=True)
+
+        se1p.real(x, q, cfg.L, cfg.xi, cfg.rc, out=rbuf, stream=stream)   # erfc table, workspace, checked
+        real_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        nreal = 3
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(nreal):
+            real_step()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        real_ms = max_over_ranks(g0.elapsed_time(g1) / nreal)
+        full = {"value": cfg.N / ((ms + real_ms) * 1e-3), "unit": "particles/s", "rc": cfg.rc,
+                "real_ms": real_ms, "kspace_ms": ms,
+                "how": ("se1p_real_ex (k_real_warp) timed alone with CUDA events on the step's stream, "
+                        "added to the k-space step time" if world == 1 else
+                        "dist.real (each rank its part of the targets + one NCCL all-reduce), max over ranks, "
+                        "added to the k-space step time")}
+
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -276,26 +308,6 @@ def bench_ours(args, cfg, rank, world, local):
     if launches_per_step is None:
         launches_per_step = se1p.launch_count()
 
-    # full SE1P at this config (BASELINE C5: real-space erfc sum with cell lists at rc plus k-space):
-    # the real-space call timed alone on the same stream, reported beside the k-space metric
-    full = None   # single GPU only (the real-space sum is not sharded over ranks)
-    if world == 1 and getattr(cfg, "rc", None):
-        rbuf = torch.empty(cfg.N, dtype=torch.float64, device=dev)
-        se1p.real(x, q, cfg.L, cfg.xi, cfg.rc, out=rbuf, stream=stream)   # erfc table, workspace, checked
-        torch.cuda.synchronize(dev)
-        nreal = 3
-        g0 = torch.cuda.Event(enable_timing=True)
-        g1 = torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        for _ in range(nreal):
-            se1p.real(x, q, cfg.L, cfg.xi, cfg.rc, out=rbuf, stream=stream, sync=False, skip_checks=True)
-        g1.record(stream)
-        torch.cuda.synchronize(dev)
-        real_ms = g0.elapsed_time(g1) / nreal
-        full = {"value": cfg.N / ((ms + real_ms) * 1e-3), "unit": "particles/s", "rc": cfg.rc,
-                "real_ms": real_ms, "kspace_ms": ms,
-                "how": "se1p_real_ex (k_real_warp) timed alone with CUDA events on the step's stream, "
-                       "added to the k-space step time"}
     spread_ms = stage_sum.get("spread", float("nan"))
     gather_ms = stage_sum.get("gather", float("nan"))
     dom_name, dom_ms = ("gather", gather_ms) if gather_ms >= spread_ms else ("spread", spread_ms)

@@ -161,6 +161,12 @@ int se1p_kspace_slab_backward(const se1p_opts* opts, void* stream, int64_t N, co
 int se1p_real(const double* x, const double* q, int64_t N, const double L[3], double xi,
               double rc, double* phi_out);
 
+/* se1p_real_ex / se1p_real_field_ex with opts->reserved[4] = R > 1 and opts->reserved[5] = r
+   (0 <= r < R): part r of R of the sum -- the targets are split into R near-equal parts (the
+   warp kernel's target groups in sorted order) and only part r's entries of phi_out (and
+   field_out) are computed; the others are set to 0, so the R parts sum exactly (bitwise) to the
+   whole.  For ranks sharing the real-space sum (dist.real: each rank its part, one all-reduce).
+   reserved[4] = 0 or 1: the whole sum.  Errors: SE1P_EINVAL for R < 0 or r outside [0, R). */
 int se1p_real_ex(const se1p_opts* opts, void* stream, const double* x, const double* q,
                  int64_t N, const double L[3], double xi, double rc, double* phi_out);
 

@@ -114,7 +114,7 @@ def _check(code):
 
 
 def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=True, profile=False, stop_after=0,
-          graph=False):
+          graph=False, part=None):
     o = Opts()
     o.Ntilde = int(Ntilde or 0)
     o.S0 = int(S0 or 0)
@@ -125,6 +125,8 @@ def _opts(Ntilde=None, S0=None, SI=None, host_io=False, skip_checks=False, sync=
     o.reserved[0] = 1 if profile else 0
     o.reserved[1] = int(stop_after)
     o.reserved[3] = 1 if graph else 0
+    if part is not None:   # (r, R): part r of R of the real-space sum (include/se1p.h)
+        o.reserved[5], o.reserved[4] = int(part[0]), int(part[1])
     return o
 
 
@@ -236,13 +238,15 @@ def kspace3p(x, q, L, xi, M, P, eta=None, out=None, stream=None, sync=True, skip
     return out
 
 
-def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False, field=False, field_out=None):
+def real(x, q, L, xi, rc, out=None, stream=None, sync=True, skip_checks=False, field=False, field_out=None,
+         part=None):
     """phi^R + phi^self (Eq. (3) truncated at rc, Eq. (6)).
-    field=True returns (phi^R + phi^self, E^R), E^R = -grad phi^R, [N,3]."""
+    field=True returns (phi^R + phi^self, E^R), E^R = -grad phi^R, [N,3].
+    part=(r, R): only part r of R of the targets, the other entries 0 (the R parts sum exactly)."""
     lib = load()
     xp, qp, N, host, keep = _args(x, q)
     out, fo, optr, fptr = _outputs(x, N, field, out, field_out)
-    o = _opts(host_io=host, skip_checks=skip_checks, sync=sync)
+    o = _opts(host_io=host, skip_checks=skip_checks, sync=sync, part=part)
     args = (ctypes.addressof(o), _stream_ptr(stream, x), xp, qp, N, _Larr(L), float(xi), float(rc), optr)
     if field:
         _check(lib.se1p_real_field_ex(*args, fptr))

@@ -537,6 +537,9 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
   if (!x || !q || (!phi_out && !field_out) || !L) throw Error{1, "null pointer"};
   if (N < 1) throw Error{1, "N must be >= 1"};
   if (!(xi > 0) || !(rc > 0) || !(L[0] > 0) || !(L[1] > 0) || !(L[2] > 0)) throw Error{1, "xi, rc, L must be > 0"};
+  const int nparts = o ? std::max(1, o->reserved[4]) : 1, part = o ? o->reserved[5] : 0;
+  if (o && (o->reserved[4] < 0 || part < 0 || part >= nparts))
+    throw Error{1, "opts->reserved[4] (parts) >= 0 and 0 <= opts->reserved[5] (part) < max(parts, 1) required"};
   const RDev d = real_geometry(L, xi, rc, N);
   DevState& ds = dev_state();
   WsOrder ws_order(ds, st);
@@ -557,7 +560,11 @@ static void real_impl(const se1p_opts* o, cudaStream_t st, const double* x, cons
     SE1P_CUDA_TRY(cudaMemcpyAsync((void*)dq, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
   }
   if (!(o && o->skip_checks)) check_inputs(w, dx, dq, N, L, false, st);
-  real_space(d, w, dx, dq, N, dphi, st, dfield);
+  if (nparts > 1) {   // the other parts' entries are 0, so the parts of all ranks sum exactly
+    if (dphi) SE1P_CUDA_TRY(cudaMemsetAsync(dphi, 0, sizeof(double) * N, st));
+    if (dfield) SE1P_CUDA_TRY(cudaMemsetAsync(dfield, 0, sizeof(double) * 3 * N, st));
+  }
+  real_space(d, w, dx, dq, N, dphi, st, dfield, part, nparts);
   if (host_io && phi_out)
     SE1P_CUDA_TRY(cudaMemcpyAsync(phi_out, dphi, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   if (host_io && field_out)
@@ -788,6 +795,7 @@ static void energy_forces_impl(const se1p_opts* o, cudaStream_t st, const double
   od.sync = 0;
   kspace_impl(&od, st, dx, dq, N, L, xi, M, P, eta, s0, sf, n_local, pk, ek);
   od.skip_checks = 1;
+  od.reserved[4] = od.reserved[5] = 0;   // the whole real-space sum
   real_impl(&od, st, dx, dq, N, L, xi, rc, pr, er);
   k_combine_forces<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(dq, pk, ek, pr, er, N, dphi, dF);
   SE1P_LAUNCH_CHECK();

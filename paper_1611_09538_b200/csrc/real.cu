@@ -81,10 +81,10 @@ __global__ void k_real_permute(RDev d, const double* __restrict__ x, const doubl
 // r_vec = x_m - x_n - alpha L3 e3 (Eq. (3) differentiated; the self term has no gradient).
 template <bool FIELD>
 __global__ void __launch_bounds__(128) k_real_sum(RDev d, const double4* __restrict__ P4, const int* __restrict__ perm,
-                                                  const int* __restrict__ cell_start, int64_t N,
+                                                  const int* __restrict__ cell_start, int64_t t_lo, int64_t t_hi,
                                                   double* __restrict__ phi_out, double* __restrict__ field_out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= N) return;
+  const int64_t t = t_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= t_hi) return;
   const double4 pt = P4[t];
   const int cx = min(max((int)floor(pt.x / d.cs[0]), 0), d.nc[0] - 1);
   const int cy = min(max((int)floor(pt.y / d.cs[1]), 0), d.nc[1] - 1);
@@ -442,8 +442,8 @@ template <bool FIELD, int DEG>
 __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d, const double4* __restrict__ P4,
                                                          const int* __restrict__ perm,
                                                          const int* __restrict__ bin_start,
-                                                         const int* __restrict__ gstart, int ncol,
-                                                         double* __restrict__ phi_out,
+                                                         const int* __restrict__ gstart, int ncol, int part,
+                                                         int nparts, double* __restrict__ phi_out,
                                                          double* __restrict__ field_out) {
   constexpr unsigned kAll = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char rw_raw[];
@@ -455,8 +455,11 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
   __syncthreads();
   // target group gw: column col's sorted run cut into G = ceil(n/32) near-equal pieces (groups
   // never straddle two columns, so the box stays compact); col by a 32-ary search of gstart
-  const int gw = blockIdx.x * nw + warp;
-  if (gw >= gstart[ncol]) return;
+  // part `part` of `nparts` (ranks sharing the sum): groups [G part / nparts, G (part+1) / nparts)
+  const int gtot = gstart[ncol];
+  const int g_hi = (int)(((int64_t)gtot * (part + 1)) / nparts);
+  const int gw = (int)(((int64_t)gtot * part) / nparts) + blockIdx.x * nw + warp;
+  if (gw >= g_hi) return;
   int clo = 0, chi = ncol;   // gstart[clo] <= gw < gstart[chi]
   while (chi - clo > 1) {
     const int step = (chi - clo + 31) / 32;
@@ -558,10 +561,11 @@ __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d,
 
 template <bool FIELD, int DEG>
 static void launch_real_warp_deg(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
-                                const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
+                                 const int* gstart, int64_t N, int part, int nparts, double* phi_out,
+                                 double* field_out, cudaStream_t st) {
   // warps per block: 8, halved while that leaves fewer than two blocks per SM (small systems)
   const int ncol = d.nc[0] * d.nc[1];
-  const int64_t groups = ceil_div(N, 32) + ncol;   // >= the number of groups
+  const int64_t groups = ceil_div(ceil_div(N, 32) + ncol, nparts) + 1;   // >= this part's groups
   int nw = kRWW;
   while (nw > 1 && ceil_div(groups, nw) < 2 * 148) nw /= 2;
   const size_t smem = nw * sizeof(RWarpSm) + (size_t)(DEG + 1) * kRealK * sizeof(double);
@@ -574,7 +578,8 @@ static void launch_real_warp_deg(const RDev& d, const double4* P4, const int* pe
   double ze[4] = {0, 0, 0, 0};
   SE1P_CUDA_TRY(cudaMemcpyToSymbol(g_rw_ext, ze, sizeof(ze)));
 #endif
-  k_real_warp<FIELD, DEG><<<nb, nw * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, phi_out, field_out);
+  k_real_warp<FIELD, DEG><<<nb, nw * 32, smem, st>>>(d, P4, perm, bin_start, gstart, ncol, part, nparts, phi_out,
+                                                       field_out);
   SE1P_LAUNCH_CHECK();
 #ifdef SE1P_REAL_COUNT
   SE1P_CUDA_TRY(cudaMemcpyFromSymbol(z, g_rw_cnt, sizeof(z)));
@@ -589,9 +594,12 @@ static void launch_real_warp_deg(const RDev& d, const double4* P4, const int* pe
 constexpr int kRealDeg[] = {7, 8, 9, 10, 11, 13, 15, 19, 23, 31};
 template <bool FIELD>
 static void launch_real_warp(const RDev& d, const double4* P4, const int* perm, const int* bin_start,
-                             const int* gstart, int64_t N, double* phi_out, double* field_out, cudaStream_t st) {
-#define SE1P_RW_CASE(D) \
-  case D: launch_real_warp_deg<FIELD, D>(d, P4, perm, bin_start, gstart, N, phi_out, field_out, st); break;
+                             const int* gstart, int64_t N, int part, int nparts, double* phi_out, double* field_out,
+                             cudaStream_t st) {
+#define SE1P_RW_CASE(D)                                                                                    \
+  case D:                                                                                                  \
+    launch_real_warp_deg<FIELD, D>(d, P4, perm, bin_start, gstart, N, part, nparts, phi_out, field_out, st); \
+    break;
   switch (d.tdeg) {
     SE1P_RW_CASE(7) SE1P_RW_CASE(8) SE1P_RW_CASE(9) SE1P_RW_CASE(10) SE1P_RW_CASE(11)
     SE1P_RW_CASE(13) SE1P_RW_CASE(15) SE1P_RW_CASE(19) SE1P_RW_CASE(23) SE1P_RW_CASE(31)
@@ -773,7 +781,7 @@ void real_release_tables(int dev) {
 }
 
 void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
-                cudaStream_t st, double* field_out) {
+                cudaStream_t st, double* field_out, int part, int nparts) {
   RDev d = d0;
 #if SE1P_REAL_TABLE
   if (d.tdeg == 0) {
@@ -843,23 +851,27 @@ void real_space(const RDev& d0, KWork& w, const double* x, const double* q, int6
     SE1P_LAUNCH_CHECK();
     exclusive_scan_ints(gcnt, ncol, gstart, gstart + ncol + 1, st);
     if (field_out)
-      launch_real_warp<true>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, field_out, st);
+      launch_real_warp<true>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, part, nparts, phi_out,
+                             field_out, st);
     else
-      launch_real_warp<false>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, phi_out, nullptr, st);
+      launch_real_warp<false>(d, (const double4*)w.xs, w.perm, w.bin_start, gstart, N, part, nparts, phi_out,
+                              nullptr, st);
     return;
   }
 #if SE1P_REAL_KERNEL == 1 && SE1P_REAL_TABLE
+  if (nparts > 1) throw Error{1, "real space: parts need the warp or thread-per-target kernel"};
   if (field_out)
     launch_real_cells<true>(d, (const double4*)w.xs, w.perm, w.bin_start, nbins, phi_out, field_out, st);
   else
     launch_real_cells<false>(d, (const double4*)w.xs, w.perm, w.bin_start, nbins, phi_out, nullptr, st);
   return;
 #endif
-  const unsigned nt = (unsigned)ceil_div(N, 128);
+  const int64_t t_lo = N * part / nparts, t_hi = N * (part + 1) / nparts;   // this part's sorted targets
+  const unsigned nt = (unsigned)std::max<int64_t>(1, ceil_div(t_hi - t_lo, 128));
   if (field_out)
-    k_real_sum<true><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out, field_out);
+    k_real_sum<true><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, t_lo, t_hi, phi_out, field_out);
   else
-    k_real_sum<false><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, N, phi_out, nullptr);
+    k_real_sum<false><<<nt, 128, 0, st>>>(d, (const double4*)w.xs, w.perm, w.bin_start, t_lo, t_hi, phi_out, nullptr);
   SE1P_LAUNCH_CHECK();
 }
 

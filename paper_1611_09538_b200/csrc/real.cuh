@@ -40,8 +40,10 @@ RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 int real_nbins(const RDev& d);   // bins of the real-space sort (workspace sizing)
 int64_t real_scratch_ints(const RDev& d, int64_t N);
 int real_table_deg(double xi, double rc);   // k_real_warp's table degree, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
+// part/nparts: only the targets of part `part` (the warp kernel's target groups, or sorted targets
+// for the fallback kernel, split in nparts near-equal ranges) are written
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
-                cudaStream_t st, double* field_out = nullptr);
+                cudaStream_t st, double* field_out = nullptr, int part = 0, int nparts = 1);
 void real_release_tables(int dev);   // the cached erfc table of device dev
 
 }  // namespace se1p

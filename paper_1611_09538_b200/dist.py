@@ -311,3 +311,24 @@ def kspace(x, q, L, xi, M, P, group=None, stream=None, **kw):
     st = stream if stream is not None else torch.cuda.current_stream(x.device)
     with torch.cuda.stream(st):
         return kspace_rank(x, q, plan, CudaBackend(L, xi, M, P, stream=st, **kw), rank, group)
+
+
+def real(x, q, L, xi, rc, group=None, stream=None, field=False, skip_checks=True):
+    """phi^R + phi^self (se1p.real) of one system shared by the ranks of `group`: every rank passes
+    the same x, q, computes its part of the targets (include/se1p.h: the target groups split in
+    R near-equal parts, the other entries 0) and one all-reduce (sum) on the stream gives every
+    rank the whole result -- bitwise equal to the single-GPU call (each entry has one nonzero
+    contributor).  field=True also returns E^R."""
+    import torch
+    import torch.distributed as dist
+    import paper_1611_09538_b200 as se1p
+    R = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.stream(st):
+        res = se1p.real(x, q, L, xi, rc, stream=st, sync=False, skip_checks=skip_checks, field=field,
+                        part=(rank, R) if R > 1 else None)
+        for t in (res if field else (res,)):
+            if R > 1:
+                dist.all_reduce(t, group=group)
+    return res

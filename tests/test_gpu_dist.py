@@ -80,6 +80,41 @@ def test_backward_requires_matching_forward():
         se1p.slab_backward(buf, 12345, c.L, c.xi, c.M, c.P, 0, 16, list(range(c.M // 2 + 1)), **kw)
 
 
+@pytest.mark.parametrize("cfg,R", [("C3", 2), ("C3", 3), ("C4", 8), ("C1", 8)])
+def test_real_space_parts_sum_to_the_whole(cfg, R):
+    """The real-space sum split over R emulated ranks (se1p.real part=(r, R), as dist.real runs
+    it): every part writes only its targets (the rest 0) and the parts sum bitwise to the
+    single-GPU call, potential and field (C1: 100 particles, fewer target groups than parts)."""
+    c = CONFIGS[cfg]
+    x, q = make_system(c.N, c.L, c.seed)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    ref, eref = se1p.real(xd, qd, c.L, c.xi, c.rc, field=True)
+    acc, eacc = torch.zeros_like(ref), torch.zeros_like(eref)
+    nonzero = torch.zeros(c.N, dtype=torch.int32, device="cuda")
+    for r in range(R):
+        p, e = se1p.real(xd, qd, c.L, c.xi, c.rc, field=True, part=(r, R))
+        nonzero += (p != 0).int()
+        acc += p
+        eacc += e
+    assert torch.equal(acc, ref) and torch.equal(eacc, eref)
+    assert int(nonzero.max()) == 1   # each target written by exactly one part
+
+
+def test_real_space_parts_fallback_kernel_and_errors():
+    """The split on the thread-per-target fallback (xi rc beyond the shared table) and the
+    argument checks of opts->reserved[4..5]."""
+    L, xi, rc = (1.0, 1.0, 1.0), 160.0, 0.9
+    x, q = make_system(300, L, 8)
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    ref = se1p.real(xd, qd, L, xi, rc)
+    acc = sum(se1p.real(xd, qd, L, xi, rc, part=(r, 3)) for r in range(3))
+    assert torch.equal(acc, ref)
+    for bad in [(3, 3), (-1, 2), (0, -2)]:
+        with pytest.raises(se1p.SE1PError) as e:
+            se1p.real(xd, qd, L, 8.0, 0.3, part=bad)
+        assert e.value.code == 1
+
+
 def test_nccl_world_one():
     import torch.distributed as dist
     with socket.socket() as s:
@@ -95,6 +130,9 @@ def test_nccl_world_one():
         phi = sdist.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
         ref = se1p.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kw)
         assert torch.equal(phi, ref)
+        pr, er = sdist.real(xd, qd, c.L, c.xi, c.rc, field=True)   # the shared real-space sum
+        rr, re = se1p.real(xd, qd, c.L, c.xi, c.rc, field=True)
+        assert torch.equal(pr, rr) and torch.equal(er, re)
     finally:
         dist.destroy_process_group()
 
@@ -128,9 +166,11 @@ def _nccl_worker(rank, world, port, cfgname, out):
     x, q = make_system(c.N, c.L, c.seed)
     xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
     phi = sdist.kspace(xd, qd, c.L, c.xi, c.M, c.P, **kspace_kwargs(c))
+    pr = sdist.real(xd, qd, c.L, c.xi, c.rc)
     torch.cuda.synchronize()
     if rank == 0:
         np.save(out, phi.cpu().numpy())
+        np.save(out + ".real.npy", pr.cpu().numpy())
     dist.destroy_process_group()
 
 
@@ -149,3 +189,5 @@ def test_nccl_two_ranks_match_single_gpu(tmp_path):
                       **kspace_kwargs(c)).cpu().numpy()
     got = np.load(out)
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+    rr = se1p.real(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda(), c.L, c.xi, c.rc).cpu().numpy()
+    assert np.array_equal(np.load(out + ".real.npy"), rr)   # dist.real: bitwise
