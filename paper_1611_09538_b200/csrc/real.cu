@@ -1,11 +1,15 @@
-// real.cu -- real-space sum phi^R (Eq. (3)) truncated at rc with linked cells
+// real.cu -- real-space sum phi^R (Eq. (3)) truncated at rc with cell lists
 // and the self term (Eq. (6)).
 //
-// Cells: nc_d = max(1, floor(D L_d/rc)) per axis, so a cell is at least rc/D wide; free axes
-// scan the cells within K_d = ceil(rc/cell_d) (no images), the periodic axis scans the unwrapped
-// cells cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell (u mod nc_z)
-// shifted by floor(u/nc_z) L3; a cell whose box lies farther than rc from the target is skipped.
-// Every image within rc is visited exactly once, for any rc.
+// Product kernel: k_real_warp (warp per group of <= 32 targets of one (x, y) column, candidates
+// from the columns within rc of the group's box, erfc from a 32-interval table in shared memory;
+// see its header below and DESIGN.md section 4).  Kept as build options / fallback: k_real_sum
+// (thread per target; also used when xi rc is beyond the shared table) and k_real_cells (warp per
+// cell).  Their cells: nc_d = max(1, floor(D L_d/rc)) per axis, so a cell is at least rc/D wide;
+// free axes scan the cells within K_d = ceil(rc/cell_d) (no images), the periodic axis scans the
+// unwrapped cells cz-K .. cz+K, K = ceil(rc/cell_z), each unwrapped cell u standing for cell
+// (u mod nc_z) shifted by floor(u/nc_z) L3; a cell whose box lies farther than rc from the target
+// is skipped.  Every image within rc is visited exactly once, for any rc (all three kernels).
 #include <array>
 #include <cstdio>
 #include <mutex>
