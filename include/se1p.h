@@ -256,6 +256,15 @@ typedef struct se1p_tol_plan {
 
 int se1p_plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_tol_plan* out);
 
+/* The erfc table of the real-space kernel (host only, no device needed; for inspection and
+   tests).  On kRealK = *intervals equal intervals of [0, rc], erfc(xi r) is the polynomial
+   sum_n c[n][i] (r - (i + 1/2) rc/K)^n of degree *degree (Chebyshev interpolant, within 2e-16 of
+   erfc in absolute terms); *degree = 0 means xi rc is beyond the table and
+   the thread-per-target kernel is used.  coeffs: caller-owned, (degree + 1) * intervals doubles,
+   coefficient-major c[n][i]; written only if capacity is large enough (query with coeffs = NULL).
+   Errors: SE1P_EINVAL for null degree/intervals or xi, rc <= 0. */
+int se1p_real_table(double xi, double rc, int* degree, int* intervals, double* coeffs, int capacity);
+
 /* Per-stage device time of the last _ex call on this thread, in milliseconds, measured
    with CUDA events on the call's stream when opts->reserved[0] == 1 (profiling mode).
    Stages: 0 bin/sort, 1 particle records (window weights), 2 gridding tiles, 3 z-FFT,

@@ -26,7 +26,8 @@ EXPORTS = ["se1p_kspace", "se1p_kspace_ex", "se1p_real", "se1p_real_ex", "se1p_p
            "se1p_last_stage_times", "se1p_last_launch_count", "se1p_release", "se1p_last_error",
            "se1p_version", "se1p_debug_copy", "se1p_kspace_slab_forward", "se1p_kspace_modes",
            "se1p_kspace_slab_backward", "se1p_kspace_field_ex", "se1p_real_field_ex", "se1p_plan_from_tol",
-           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex", "se1p_set_allocator", "se1p_energy_forces"]
+           "se1p_kspace3p_ex", "se1p_kspace_tiers_ex", "se1p_set_allocator", "se1p_energy_forces",
+           "se1p_real_table"]
 
 
 class SE1PError(RuntimeError):
@@ -95,6 +96,8 @@ def load(build_if_needed: bool = True):
     lib.se1p_debug_copy.restype = i32
     lib.se1p_set_allocator.argtypes = [vp, vp, vp]
     lib.se1p_set_allocator.restype = i32
+    lib.se1p_real_table.argtypes = [d, d, vp, vp, vp, i32]
+    lib.se1p_real_table.restype = i32
     ip = ctypes.POINTER(ctypes.c_int)
     lib.se1p_kspace_slab_forward.argtypes = [vp, vp, vp, vp, i64, vp, d, i32, i32, d, d, d, i32,
                                              i32, i32, ip, vp]
@@ -373,6 +376,20 @@ def plan_from_tol(L, Q, xi, tol):
     out = TolPlan()
     _check(lib.se1p_plan_from_tol(_Larr(L), float(Q), float(xi), float(tol), ctypes.addressof(out)))
     return out.as_dict()
+
+
+def real_table(xi, rc):
+    """(degree, intervals, coefficients [degree + 1, intervals]) of the real-space kernel's erfc
+    table (host only; include/se1p.h se1p_real_table); degree 0: fallback kernel, no table."""
+    import numpy as np
+    lib = load()
+    deg, K = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib.se1p_real_table(ctypes.c_double(xi), ctypes.c_double(rc), ctypes.byref(deg), ctypes.byref(K), None, 0))
+    c = np.zeros((deg.value + 1) * K.value if deg.value > 0 else 0)
+    if deg.value > 0:
+        _check(lib.se1p_real_table(ctypes.c_double(xi), ctypes.c_double(rc), ctypes.byref(deg), ctypes.byref(K),
+                                   c.ctypes.data_as(ctypes.c_void_p), int(c.size)))
+    return deg.value, K.value, c.reshape(deg.value + 1, K.value) if deg.value > 0 else c
 
 
 def kspace_args(plan):

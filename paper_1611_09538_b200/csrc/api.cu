@@ -971,6 +971,15 @@ int se1p_plan_from_tol(const double L[3], double Q, double xi, double tol, se1p_
   return guarded([&] { plan_from_tol(L, Q, xi, tol, out); });
 }
 
+int se1p_real_table(double xi, double rc, int* degree, int* intervals, double* coeffs, int capacity) {
+  return guarded([&] {
+    if (!degree || !intervals) throw Error{1, "null pointer"};
+    if (!(xi > 0) || !(rc > 0)) throw Error{1, "xi, rc must be > 0"};
+    const std::vector<double> t = real_table_host(xi, rc, *degree, *intervals);
+    if (coeffs && capacity >= (int)t.size()) std::copy(t.begin(), t.end(), coeffs);
+  });
+}
+
 int se1p_last_stage_times(double* ms, int max_stages) {
   int n = std::min(max_stages, g_nstages);
   for (int i = 0; i < n; ++i) ms[i] = g_stage_ms[i];

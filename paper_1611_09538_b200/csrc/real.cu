@@ -762,6 +762,12 @@ static std::vector<double> erfc_small_table(double xi, double rc, int tdeg) {
   return t;
 }
 
+std::vector<double> real_table_host(double xi, double rc, int& degree, int& intervals) {
+  degree = real_table_deg(xi, rc);
+  intervals = kRealK;
+  return degree > 0 ? erfc_small_table(xi, rc, degree) : std::vector<double>();
+}
+
 struct TabCache {
   double xi = 0, rc = 0;
   double* dev = nullptr;

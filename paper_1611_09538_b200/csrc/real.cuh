@@ -2,6 +2,7 @@
 #pragma once
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "kspace.cuh"
 
@@ -39,7 +40,9 @@ inline int real_table_intervals(double xi, double rc) {
 RDev real_geometry(const double L[3], double xi, double rc, int64_t N);
 int real_nbins(const RDev& d);   // bins of the real-space sort (workspace sizing)
 int64_t real_scratch_ints(const RDev& d, int64_t N);
-int real_table_deg(double xi, double rc);   // k_real_warp's table degree, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
+int real_table_deg(double xi, double rc);
+// the shared table k_real_warp uses (coefficient-major [degree + 1][intervals]; empty if degree 0)
+std::vector<double> real_table_host(double xi, double rc, int& degree, int& intervals);   // k_real_warp's table degree, 0 if unsupported   // ints of KWork::scratch the real-space sum needs
 // part/nparts: only the targets of part `part` (the warp kernel's target groups, or sorted targets
 // for the fallback kernel, split in nparts near-equal ranges) are written
 void real_space(const RDev& d, KWork& w, const double* x, const double* q, int64_t N, double* phi_out,
