@@ -326,7 +326,10 @@ static void launch_real_cells(const RDev& d, const double4* P4, const int* perm,
 // (rw_pair).  Each target sums its terms in candidate order: deterministic.  (Measured and not
 // kept: the hit test in fp32 with a safe margin and an fp64 re-test at evaluation, +5 % at C5:
 // the extra fp32 copy of the ring costs more than the cheaper test saves.)
-constexpr int kRWW = 8;                    // warps per block (at most; fewer for small systems)
+#ifndef SE1P_REAL_RWW
+#define SE1P_REAL_RWW 4
+#endif
+constexpr int kRWW = SE1P_REAL_RWW;        // warps per block (at most; fewer for small systems)
 struct RWarpSm {
   double4 cand[64];                        // staged candidates: x, y, z + image shift, q (ring)
 };
@@ -441,7 +444,7 @@ __device__ double g_rw_ext[4];
 #endif
 template <bool FIELD, int DEG>
 #ifndef SE1P_REAL_MINB
-#define SE1P_REAL_MINB 3
+#define SE1P_REAL_MINB 6
 #endif
 __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d, const double4* __restrict__ P4,
                                                          const int* __restrict__ perm,
