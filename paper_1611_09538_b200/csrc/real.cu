@@ -396,12 +396,15 @@ __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bo
 // One phase: n staged candidates from ring slot base (base + n <= 64) against the warp's targets,
 // one target per lane, candidates broadcast from shared memory.  First every lane tests its target
 // against the n candidates into a hit mask (independent, cheap); then the warp walks the
-// candidates that any lane has within rc, two at a time (independent chains), every lane
+// candidates that any lane has within rc, four at a time (independent chains), every lane
 // evaluating them and keeping its own terms by a select -- a lane-divergent "if within rc" would
 // idle the lanes outside while the others evaluate.  Misses evaluate at r^2 = rc^2 (finite).  The
 // prime in Eq. (3) (n = m in the unshifted image) is the pair at r^2 = 0 exactly: a target meets
 // itself with identical coordinates, and a distinct particle at zero distance would make phi
 // infinite (not a valid input).
+#ifndef SE1P_REAL_WALK
+#define SE1P_REAL_WALK 4   // candidates per round of the walk (2 or 4)
+#endif
 template <bool FIELD, int DEG, bool FULL>
 __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
                                          double rc2, const RDev& d, const double* tab, double& acc, double& ex,
@@ -420,6 +423,21 @@ __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, cons
   }
   if (!active) m = 0;
   unsigned am = __reduce_or_sync(kAll, m);
+#if SE1P_REAL_WALK == 4
+  while (am) {   // four candidates per round (independent chains)
+    int kk[4];
+    bool ok[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ok[i] = am != 0;
+      kk[i] = ok[i] ? __ffs(am) - 1 : 0;
+      am &= am - 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      rw_eval<FIELD, DEG>(pt, cb[kk[i]], ok[i] && ((m >> kk[i]) & 1u), rc2, d, tab, acc, ex, ey, ez);
+  }
+#else
   while (am) {
     const int k1 = __ffs(am) - 1;
     am &= am - 1;
@@ -430,6 +448,7 @@ __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, cons
     rw_eval<FIELD, DEG>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
     rw_eval<FIELD, DEG>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
   }
+#endif
 }
 
 // groups per column: ceil(n/32) (k_real_warp's target groups)
@@ -444,7 +463,7 @@ __device__ double g_rw_ext[4];
 #endif
 template <bool FIELD, int DEG>
 #ifndef SE1P_REAL_MINB
-#define SE1P_REAL_MINB 6
+#define SE1P_REAL_MINB 4
 #endif
 __global__ void __launch_bounds__(kRWW * 32, SE1P_REAL_MINB) k_real_warp(RDev d, const double4* __restrict__ P4,
                                                          const int* __restrict__ perm,
