@@ -403,7 +403,7 @@ __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bo
 // itself with identical coordinates, and a distinct particle at zero distance would make phi
 // infinite (not a valid input).
 #ifndef SE1P_REAL_WALK
-#define SE1P_REAL_WALK 4   // candidates per round of the walk (2 or 4)
+#define SE1P_REAL_WALK 4   // candidates per round of the walk (2, 4 or 8)
 #endif
 template <bool FIELD, int DEG, bool FULL>
 __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
@@ -423,18 +423,18 @@ __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, cons
   }
   if (!active) m = 0;
   unsigned am = __reduce_or_sync(kAll, m);
-#if SE1P_REAL_WALK == 4
-  while (am) {   // four candidates per round (independent chains)
-    int kk[4];
-    bool ok[4];
+#if SE1P_REAL_WALK >= 4
+  while (am) {   // SE1P_REAL_WALK candidates per round (independent chains)
+    int kk[SE1P_REAL_WALK];
+    bool ok[SE1P_REAL_WALK];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < SE1P_REAL_WALK; ++i) {
       ok[i] = am != 0;
       kk[i] = ok[i] ? __ffs(am) - 1 : 0;
       am &= am - 1;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < SE1P_REAL_WALK; ++i)
       rw_eval<FIELD, DEG>(pt, cb[kk[i]], ok[i] && ((m >> kk[i]) & 1u), rc2, d, tab, acc, ex, ey, ez);
   }
 #else
