@@ -405,6 +405,9 @@ __device__ __forceinline__ void rw_eval(const double4& pt, const double4& cc, bo
 #ifndef SE1P_REAL_WALK
 #define SE1P_REAL_WALK 4   // candidates per round of the walk (2, 4 or 8)
 #endif
+#ifndef SE1P_REAL_WALK_F
+#define SE1P_REAL_WALK_F SE1P_REAL_WALK   // the same for the field kernels
+#endif
 template <bool FIELD, int DEG, bool FULL>
 __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, const double4& pt, bool active,
                                          double rc2, const RDev& d, const double* tab, double& acc, double& ex,
@@ -423,32 +426,33 @@ __device__ __forceinline__ void rw_phase(const RWarpSm& s, int base, int n, cons
   }
   if (!active) m = 0;
   unsigned am = __reduce_or_sync(kAll, m);
-#if SE1P_REAL_WALK >= 4
-  while (am) {   // SE1P_REAL_WALK candidates per round (independent chains)
-    int kk[SE1P_REAL_WALK];
-    bool ok[SE1P_REAL_WALK];
+  constexpr int W = FIELD ? SE1P_REAL_WALK_F : SE1P_REAL_WALK;
+  if (W >= 4) {
+    while (am) {   // W candidates per round (independent chains)
+      int kk[W >= 4 ? W : 4];
+      bool ok[W >= 4 ? W : 4];
 #pragma unroll
-    for (int i = 0; i < SE1P_REAL_WALK; ++i) {
-      ok[i] = am != 0;
-      kk[i] = ok[i] ? __ffs(am) - 1 : 0;
-      am &= am - 1;
+      for (int i = 0; i < W; ++i) {
+        ok[i] = am != 0;
+        kk[i] = ok[i] ? __ffs(am) - 1 : 0;
+        am &= am - 1;
+      }
+#pragma unroll
+      for (int i = 0; i < W; ++i)
+        rw_eval<FIELD, DEG>(pt, cb[kk[i]], ok[i] && ((m >> kk[i]) & 1u), rc2, d, tab, acc, ex, ey, ez);
     }
-#pragma unroll
-    for (int i = 0; i < SE1P_REAL_WALK; ++i)
-      rw_eval<FIELD, DEG>(pt, cb[kk[i]], ok[i] && ((m >> kk[i]) & 1u), rc2, d, tab, acc, ex, ey, ez);
+  } else {
+    while (am) {
+      const int k1 = __ffs(am) - 1;
+      am &= am - 1;
+      const bool two = am != 0;
+      const int k2 = two ? __ffs(am) - 1 : k1;
+      am &= am - 1;
+      const double4 c1 = cb[k1], c2 = cb[k2];
+      rw_eval<FIELD, DEG>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
+      rw_eval<FIELD, DEG>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
+    }
   }
-#else
-  while (am) {
-    const int k1 = __ffs(am) - 1;
-    am &= am - 1;
-    const bool two = am != 0;
-    const int k2 = two ? __ffs(am) - 1 : k1;
-    am &= am - 1;
-    const double4 c1 = cb[k1], c2 = cb[k2];
-    rw_eval<FIELD, DEG>(pt, c1, (m >> k1) & 1u, rc2, d, tab, acc, ex, ey, ez);
-    rw_eval<FIELD, DEG>(pt, c2, two && ((m >> k2) & 1u), rc2, d, tab, acc, ex, ey, ez);
-  }
-#endif
 }
 
 // groups per column: ceil(n/32) (k_real_warp's target groups)

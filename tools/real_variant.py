@@ -1,4 +1,5 @@
-"""Real-space device time with a library variant (tools/build_variant.py).  python tools/real_variant.py NAME"""
+"""Real-space device time with a library variant (tools/build_variant.py).
+    python tools/real_variant.py NAME [C4,C5] [field]"""
 import os
 import sys
 
@@ -15,12 +16,13 @@ for name in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["C4", "C5"]):
     c = CONFIGS[name]
     x, q = make_system(c.N, c.L, c.seed)
     xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
-    se1p.real(xd, qd, c.L, c.xi, c.rc)
+    field = len(sys.argv) > 3 and sys.argv[3] == "field"
+    se1p.real(xd, qd, c.L, c.xi, c.rc, field=field)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(3):
-        se1p.real(xd, qd, c.L, c.xi, c.rc, skip_checks=True, sync=False)
+        se1p.real(xd, qd, c.L, c.xi, c.rc, skip_checks=True, sync=False, field=field)
     e1.record()
     torch.cuda.synchronize()
-    print(sys.argv[1], name, f"{e0.elapsed_time(e1) / 3:.3f} ms", flush=True)
+    print(sys.argv[1], name, "field" if field else "", f"{e0.elapsed_time(e1) / 3:.3f} ms", flush=True)
